@@ -1,0 +1,155 @@
+/*
+ * infllm2.h — C ABI of the B200-native InfLLM v2 block-sparse attention library
+ * (libinfllm2.so, sm_100a).
+ *
+ * The reference (/root/reference, "deskinfer") is pure Python/NumPy and exposes
+ * this path only as Python functions; there is no FFI of its own.  Each entry
+ * point below replaces one reference interface, cited as file:line into
+ * /root/reference/pkg/src/deskinfer/.  INTEGRATION.md shows the ctypes binding a
+ * maintainer would add on the reference side.
+ *
+ * Conventions (all entry points):
+ *   - every pointer is a DEVICE pointer unless its comment says "host";
+ *   - the library never allocates or frees device memory: the caller passes
+ *     workspace (size it with the *_workspace_bytes queries);
+ *   - work is enqueued on `stream`; no entry point synchronises the host;
+ *   - arguments are validated on the host before any launch; a negative return
+ *     is an error code (infllm2_strerror), 0 is success;
+ *   - inputs are post-RoPE (the operator never applies rotary embeddings,
+ *     matching model.py:427-432).
+ *
+ * Memory layout in HBM (the "blockized cache"):
+ *   K, V cache   bf16  [HKV][cap][D]        (head-major: one KV group's 64-row
+ *                                            block is one contiguous 16 KB run)
+ *   fine means   f32   [HKV][means_cap][D]  window j = rows [j*s, min(j*s+p, L))
+ *   means hi/lo  bf16  [HKV][means_cap][D]  optional split copy of the fine
+ *                                            means (hi = bf16(mu), lo = bf16(mu-hi))
+ *                                            feeding the tensor-core scorer
+ *   q            bf16  (n, HQ, D) rows `q_row_stride` elements apart
+ *   out          bf16 or f32 (n, HQ, D) contiguous
+ *   lse          f32   (n, HQ)  natural-log normaliser of the stage-2 scores
+ *   selection    i32   (n, HKV, max_sel)  ascending block ids, -1 padded,
+ *                      max_sel = top_k + n_init_blocks + n_local_blocks
+ */
+#ifndef INFLLM2_H_
+#define INFLLM2_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* infllm2_stream_t; /* a cudaStream_t (CUstream); NULL = legacy default */
+
+/* Error codes.  ValidationError in the reference maps to -1..-5 and -9
+ * (container.py:48-49, raised at sparse.py:42-51,407-420,265-266,365-374);
+ * NumericError (model.py:24-25, sparse.py:176-177) maps to -8. */
+enum {
+  INFLLM2_OK = 0,
+  INFLLM2_ERR_CONFIG = -1,       /* bad SparseAttentionConfig (sparse.py:42-51)        */
+  INFLLM2_ERR_SHAPE = -2,        /* head counts / dims inconsistent (sparse.py:407-408) */
+  INFLLM2_ERR_POSITION = -3,     /* query position beyond cache length (sparse.py:417) */
+  INFLLM2_ERR_CAPACITY = -4,     /* cache or means capacity too small                  */
+  INFLLM2_ERR_WORKSPACE = -5,    /* workspace missing or too small                     */
+  INFLLM2_ERR_UNSUPPORTED = -6,  /* shape outside every kernel's envelope (D > 256 ...) */
+  INFLLM2_ERR_CUDA = -7,         /* a launch failed                                    */
+  INFLLM2_ERR_NUMERIC = -8,      /* non-finite input (debug check only)                */
+  INFLLM2_ERR_EMPTY = -9         /* empty selection / nothing to attend                */
+};
+
+/* Mirrors SparseAttentionConfig (sparse.py:31-40). */
+typedef struct infllm2_geometry {
+  int32_t block_size;            /* m   */
+  int32_t kernel_size;           /* p   */
+  int32_t kernel_stride;         /* s   */
+  int32_t coarse_stride;         /* s_c */
+  int32_t top_k;                 /* k   */
+  int32_t n_init_blocks;
+  int32_t n_local_blocks;
+  int32_t forced_consume_budget; /* 0/1 */
+} infllm2_geometry;
+
+/* flags for infllm2_select / infllm2_attend / infllm2_forward */
+enum {
+  INFLLM2_FLAG_EXACT_SIMT = 1 << 0,  /* force the CUDA-core float64 scorer (verifier) */
+  INFLLM2_FLAG_CHECK_FINITE = 1 << 1,/* report non-finite q / means (costs a sync)    */
+  INFLLM2_FLAG_OUT_F32 = 1 << 2      /* `out` is float32 instead of bf16              */
+};
+
+const char* infllm2_strerror(int code);
+int infllm2_version(void);            /* major*10000 + minor*100 + patch */
+int infllm2_validate_geometry(const infllm2_geometry* g);  /* sparse.py:42-51 */
+int32_t infllm2_max_selected(const infllm2_geometry* g);
+
+/* Append n_new rows to the blockized cache at rows [l_old, l_old+n_new).
+ * k_new/v_new are (n_new, HKV, D), rows `src_row_stride` elements apart,
+ * dtype bf16 (src_is_f32 = 0) or f32 (src_is_f32 = 1, rounded to bf16).
+ * Replaces LayerCache.append's copy (model.py:322-336). */
+int infllm2_append_kv(void* k_cache, void* v_cache, int64_t cap, int32_t hkv, int32_t d,
+                      const void* k_new, const void* v_new, int64_t n_new,
+                      int64_t src_row_stride, int32_t src_is_f32, int64_t l_old,
+                      infllm2_stream_t stream);
+
+/* Re-synchronise kernel means with stride `stride` after the cache length went
+ * from l_old to l_new (append: l_new > l_old; truncate: l_new < l_old; full
+ * build: l_old = 0).  Recomputes windows j >= first, first = the first window
+ * whose rows changed (sparse.py:116-127), clipped to the windows that already
+ * existed (reference defect F18).  means_count_old is the number of
+ * windows valid before the call (l_old // stride for a cache kept in sync).
+ * means_hi / means_lo may be NULL.  Bitwise equal to build_kernels
+ * (sparse.py:70-91): sequential f64 sum, f64 divide, f32 round-to-nearest. */
+int infllm2_compress(const void* k_cache, int64_t cap, int32_t hkv, int32_t d,
+                     int64_t l_old, int64_t l_new, int64_t means_count_old,
+                     int32_t kernel_size, int32_t stride,
+                     float* means, void* means_hi, void* means_lo, int64_t means_cap,
+                     infllm2_stream_t stream);
+
+/* Workspace for infllm2_select / infllm2_forward (bytes). */
+size_t infllm2_select_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hq,
+                                      int32_t hkv, int32_t d, int64_t cache_len, int32_t flags);
+
+/* Stage 1: per (query row, KV group) block selection.
+ * Replaces the per-row scoring/selection of two_stage_attention
+ * (sparse.py:415-451): kernel_scores (:163-180) + softmax_f64 (model.py:185-191)
+ * + group_scores (:183-188) + block_scores (:201-215) + force_blocks (:218-227)
+ * + select_topk (:247-277).  Query row i is at absolute position start + i and
+ * sees kernels j < min((start+i)//s + 1, cache_len//s) (sparse.py:426).
+ * sel_scores (optional, may be NULL): f64 (n, HKV, max_sel) relevance score of
+ * each selected block (the traces' "scores_topk", sparse.py:465). */
+int infllm2_select(const infllm2_geometry* g,
+                   const void* q, int64_t q_row_stride, int64_t n, int64_t start,
+                   int32_t hq, int32_t hkv, int32_t d,
+                   const float* fine_means, const void* means_hi, const void* means_lo,
+                   int64_t means_cap, int64_t cache_len,
+                   int32_t* selection, double* sel_scores,
+                   void* workspace, size_t workspace_bytes, int32_t flags,
+                   infllm2_stream_t stream);
+
+/* Stage 2: attention over the selected blocks, causally clipped
+ * (sparse_attend, sparse.py:347-384).  Writes out (n, HQ, D) and lse (n, HQ)
+ * (lse may be NULL). */
+int infllm2_attend(const infllm2_geometry* g,
+                   const void* q, int64_t q_row_stride, int64_t n, int64_t start,
+                   int32_t hq, int32_t hkv, int32_t d,
+                   const void* k_cache, const void* v_cache, int64_t cap, int64_t cache_len,
+                   const int32_t* selection, void* out, float* lse, int32_t flags,
+                   infllm2_stream_t stream);
+
+/* Stage 1 + stage 2: the whole two_stage_attention call (sparse.py:387-468). */
+int infllm2_forward(const infllm2_geometry* g,
+                    const void* q, int64_t q_row_stride, int64_t n, int64_t start,
+                    int32_t hq, int32_t hkv, int32_t d,
+                    const void* k_cache, const void* v_cache, int64_t cap, int64_t cache_len,
+                    const float* fine_means, const void* means_hi, const void* means_lo,
+                    int64_t means_cap,
+                    int32_t* selection, double* sel_scores, void* out, float* lse,
+                    void* workspace, size_t workspace_bytes, int32_t flags,
+                    infllm2_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INFLLM2_H_ */

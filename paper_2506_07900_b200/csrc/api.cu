@@ -1,0 +1,174 @@
+// C ABI of libinfllm2 (include/infllm2.h): host-side validation and dispatch.
+//
+// Validation mirrors the reference's ValidationError sites so the Python mirror
+// can raise the same exception types: SparseAttentionConfig.__post_init__
+// (sparse.py:42-51), two_stage_attention's head/position checks
+// (sparse.py:407-420).
+#include <math.h>
+
+#include "common.cuh"
+#include "tc_dispatch.cuh"
+
+using namespace infllm2;
+
+namespace {
+
+constexpr int kMaxHeadDim = 256;
+constexpr int kMaxGroup = 256;
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? INFLLM2_OK : INFLLM2_ERR_CUDA; }
+
+int make_shape(const infllm2_geometry* g, int64_t n, int64_t start, int32_t hq, int32_t hkv,
+               int32_t d, int64_t cache_len, CallShape* cs) {
+  int rc = infllm2_validate_geometry(g);
+  if (rc) return rc;
+  if (n < 0 || start < 0 || hq <= 0 || hkv <= 0 || d <= 0) return INFLLM2_ERR_SHAPE;
+  if (hq % hkv) return INFLLM2_ERR_SHAPE;                       // sparse.py:407-408
+  if (d > kMaxHeadDim || hq / hkv > kMaxGroup) return INFLLM2_ERR_UNSUPPORTED;
+  if (n > 0 && start + n > cache_len) return INFLLM2_ERR_POSITION;  // sparse.py:417-420
+  cs->n = n;
+  cs->start = start;
+  cs->cache_len = cache_len;
+  cs->hq = hq;
+  cs->hkv = hkv;
+  cs->d = d;
+  cs->group = hq / hkv;
+  cs->max_sel = infllm2_max_selected(g);
+  cs->nk_total = cache_len / g->kernel_stride;
+  cs->nb_max = n > 0 ? (start + n - 1) / g->block_size + 1 : 0;
+  return INFLLM2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* infllm2_strerror(int code) {
+  switch (code) {
+    case INFLLM2_OK: return "ok";
+    case INFLLM2_ERR_CONFIG: return "invalid sparse attention geometry";
+    case INFLLM2_ERR_SHAPE: return "query heads not divisible by KV heads or bad dims";
+    case INFLLM2_ERR_POSITION: return "query position beyond cache length";
+    case INFLLM2_ERR_CAPACITY: return "cache capacity exceeded";
+    case INFLLM2_ERR_WORKSPACE: return "workspace missing or too small";
+    case INFLLM2_ERR_UNSUPPORTED: return "shape outside the supported envelope";
+    case INFLLM2_ERR_CUDA: return "CUDA launch failed";
+    case INFLLM2_ERR_NUMERIC: return "non-finite values in kernel scoring";
+    case INFLLM2_ERR_EMPTY: return "empty block selection";
+    default: return "unknown error";
+  }
+}
+
+int infllm2_version(void) { return 100; }
+
+int infllm2_validate_geometry(const infllm2_geometry* g) {
+  if (!g) return INFLLM2_ERR_CONFIG;
+  const int32_t mn = g->block_size < g->kernel_size ? g->block_size : g->kernel_size;
+  int32_t smallest = mn < g->kernel_stride ? mn : g->kernel_stride;
+  smallest = smallest < g->coarse_stride ? smallest : g->coarse_stride;
+  smallest = smallest < g->top_k ? smallest : g->top_k;
+  if (smallest <= 0) return INFLLM2_ERR_CONFIG;
+  if (g->kernel_stride > g->kernel_size) return INFLLM2_ERR_CONFIG;
+  if (g->coarse_stride < g->kernel_stride || g->coarse_stride % g->kernel_stride) return INFLLM2_ERR_CONFIG;
+  if (g->n_init_blocks < 0 || g->n_local_blocks < 0) return INFLLM2_ERR_CONFIG;
+  return INFLLM2_OK;
+}
+
+int32_t infllm2_max_selected(const infllm2_geometry* g) {
+  return g->top_k + g->n_init_blocks + g->n_local_blocks;
+}
+
+int infllm2_append_kv(void* k_cache, void* v_cache, int64_t cap, int32_t hkv, int32_t d,
+                      const void* k_new, const void* v_new, int64_t n_new, int64_t src_row_stride,
+                      int32_t src_is_f32, int64_t l_old, infllm2_stream_t stream) {
+  if (hkv <= 0 || d <= 0 || n_new < 0 || l_old < 0) return INFLLM2_ERR_SHAPE;
+  if (l_old + n_new > cap) return INFLLM2_ERR_CAPACITY;
+  return cuda_status(launch_append_kv(k_cache, v_cache, cap, hkv, d, k_new, v_new, n_new,
+                                      src_row_stride, src_is_f32, l_old, (cudaStream_t)stream));
+}
+
+int infllm2_compress(const void* k_cache, int64_t cap, int32_t hkv, int32_t d, int64_t l_old,
+                     int64_t l_new, int64_t means_count_old, int32_t kernel_size, int32_t stride,
+                     float* means, void* means_hi, void* means_lo, int64_t means_cap,
+                     infllm2_stream_t stream) {
+  if (kernel_size <= 0 || stride <= 0 || hkv <= 0 || d <= 0) return INFLLM2_ERR_CONFIG;
+  if (l_old < 0 || l_new < 0 || l_new > cap) return INFLLM2_ERR_CAPACITY;
+  if ((means_hi == nullptr) != (means_lo == nullptr)) return INFLLM2_ERR_SHAPE;
+  const int64_t count = l_new / stride;
+  if (count > means_cap) return INFLLM2_ERR_CAPACITY;
+  // boundary = old length on append, new length on truncate (sparse.py:129-133)
+  const int64_t boundary = l_new >= l_old ? l_old : l_new;
+  int64_t first = first_dirty_window(boundary, kernel_size, stride);
+  if (first > count) first = count;
+  if (first > means_count_old) first = means_count_old;  // F18: windows that never existed
+  if (first < 0) first = 0;
+  return cuda_status(launch_compress(k_cache, cap, hkv, d, first, count, l_new, kernel_size, stride,
+                                     means, means_hi, means_lo, means_cap, (cudaStream_t)stream));
+}
+
+size_t infllm2_select_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hq, int32_t hkv,
+                                      int32_t d, int64_t cache_len, int32_t flags) {
+  CallShape cs;
+  if (make_shape(g, n, cache_len - n > 0 ? cache_len - n : 0, hq, hkv, d, cache_len, &cs)) return 0;
+  // The tail rows have the most candidate blocks; size for the whole cache.
+  cs.nb_max = cache_len / g->block_size + 1;
+  size_t ws = select_simt_workspace(n * hkv, cs.nk_total, cs.nb_max);
+  const size_t tc = tc_select_workspace(*g, cs, flags);
+  return ws > tc ? ws : tc;
+}
+
+int infllm2_select(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
+                   int64_t start, int32_t hq, int32_t hkv, int32_t d, const float* fine_means,
+                   const void* means_hi, const void* means_lo, int64_t means_cap, int64_t cache_len,
+                   int32_t* selection, double* sel_scores, void* workspace, size_t workspace_bytes,
+                   int32_t flags, infllm2_stream_t stream) {
+  CallShape cs;
+  int rc = make_shape(g, n, start, hq, hkv, d, cache_len, &cs);
+  if (rc) return rc;
+  if (n == 0) return INFLLM2_OK;
+  if (cs.nk_total > means_cap) return INFLLM2_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_select_supported(*g, cs, means_hi != nullptr)) {
+    return cuda_status(launch_select_tc(*g, cs, q, q_row_stride, fine_means, means_hi, means_lo, means_cap,
+                                        selection, sel_scores, workspace, workspace_bytes, st));
+  }
+  const size_t need = select_simt_workspace(n * hkv, cs.nk_total, cs.nb_max);
+  if (workspace == nullptr || workspace_bytes < need) return INFLLM2_ERR_WORKSPACE;
+  return cuda_status(launch_select_simt(*g, cs, q, q_row_stride, fine_means, means_cap, selection,
+                                        sel_scores, workspace, workspace_bytes, st));
+}
+
+int infllm2_attend(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
+                   int64_t start, int32_t hq, int32_t hkv, int32_t d, const void* k_cache,
+                   const void* v_cache, int64_t cap, int64_t cache_len, const int32_t* selection,
+                   void* out, float* lse, int32_t flags, infllm2_stream_t stream) {
+  CallShape cs;
+  int rc = make_shape(g, n, start, hq, hkv, d, cache_len, &cs);
+  if (rc) return rc;
+  if (cache_len > cap) return INFLLM2_ERR_CAPACITY;
+  if (n == 0) return INFLLM2_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int out_f32 = (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0;
+  if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_attend_supported(*g, cs)) {
+    return cuda_status(launch_attend_tc(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out,
+                                        out_f32, lse, st));
+  }
+  return cuda_status(launch_attend_simt(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out,
+                                        out_f32, lse, st));
+}
+
+int infllm2_forward(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
+                    int64_t start, int32_t hq, int32_t hkv, int32_t d, const void* k_cache,
+                    const void* v_cache, int64_t cap, int64_t cache_len, const float* fine_means,
+                    const void* means_hi, const void* means_lo, int64_t means_cap, int32_t* selection,
+                    double* sel_scores, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                    int32_t flags, infllm2_stream_t stream) {
+  int rc = infllm2_select(g, q, q_row_stride, n, start, hq, hkv, d, fine_means, means_hi, means_lo,
+                          means_cap, cache_len, selection, sel_scores, workspace, workspace_bytes, flags,
+                          stream);
+  if (rc) return rc;
+  return infllm2_attend(g, q, q_row_stride, n, start, hq, hkv, d, k_cache, v_cache, cap, cache_len,
+                        selection, out, lse, flags, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Shared device/host helpers for libinfllm2 (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "infllm2.h"
+
+namespace infllm2 {
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ float bf16_to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float bf16bits_to_f32(uint16_t b) {
+  return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+// Host-side derived geometry for one call.
+struct CallShape {
+  int64_t n, start, cache_len;
+  int32_t hq, hkv, d, group;
+  int32_t max_sel;
+  int64_t nk_total;     // cache_len // s
+  int64_t nb_max;       // candidate blocks of the last row
+};
+
+// First kernel window whose rows change when the cache boundary moves
+// (sparse.py:119-120).
+__host__ __device__ inline int64_t first_dirty_window(int64_t boundary, int64_t p, int64_t s) {
+  return boundary < p ? 0 : (boundary - p) / s + 1;
+}
+
+// Half-open kernel range intersecting block [start, end) (sparse.py:191-198).
+__host__ __device__ inline void kernel_range_for_block(int64_t start, int64_t end, int64_t p,
+                                                       int64_t s, int64_t n_kernels, int64_t* lo,
+                                                       int64_t* hi) {
+  int64_t l = start < p ? 0 : (start - p) / s + 1;
+  int64_t h = (end + s - 1) / s;
+  if (h > n_kernels) h = n_kernels;
+  if (l > n_kernels) l = n_kernels;
+  *lo = l;
+  *hi = h;
+}
+
+}  // namespace infllm2
+
+// Kernel-launch entry points implemented in the .cu files (host side).
+namespace infllm2 {
+cudaError_t launch_append_kv(void* k_cache, void* v_cache, int64_t cap, int hkv, int d,
+                             const void* k_new, const void* v_new, int64_t n_new,
+                             int64_t src_row_stride, int src_is_f32, int64_t l_old,
+                             cudaStream_t stream);
+cudaError_t launch_compress(const void* k_cache, int64_t cap, int hkv, int d, int64_t first,
+                            int64_t count, int64_t length, int p, int s, float* means,
+                            void* hi, void* lo, int64_t means_cap, cudaStream_t stream);
+size_t select_simt_workspace(int64_t items, int64_t nk_total, int64_t nb_max);
+cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                               int64_t q_row_stride, const float* means, int64_t means_cap,
+                               int32_t* selection, double* sel_scores, void* ws, size_t ws_bytes,
+                               cudaStream_t stream);
+cudaError_t launch_attend_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                               int64_t q_row_stride, const void* k_cache, const void* v_cache,
+                               int64_t cap, const int32_t* selection, void* out, int out_f32,
+                               float* lse, cudaStream_t stream);
+}  // namespace infllm2

@@ -1,0 +1,19 @@
+// Tensor-core (tcgen05/TMEM/TMA) kernels for the production geometry and their
+// dispatch predicates.  Implemented in select_tc.cu / attend_tc.cu.
+#pragma once
+
+#include "common.cuh"
+
+namespace infllm2 {
+bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool have_split_means);
+size_t tc_select_workspace(const infllm2_geometry& g, const CallShape& cs, int flags);
+cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                             int64_t q_row_stride, const float* means, const void* means_hi,
+                             const void* means_lo, int64_t means_cap, int32_t* selection,
+                             double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream);
+bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs);
+cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                             int64_t q_row_stride, const void* k_cache, const void* v_cache,
+                             int64_t cap, const int32_t* selection, void* out, int out_f32,
+                             float* lse, cudaStream_t stream);
+}  // namespace infllm2

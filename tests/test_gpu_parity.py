@@ -1,0 +1,208 @@
+"""GPU parity: libinfllm2 (through its C ABI) vs the reference's golden fixtures and the oracle.
+
+Bars:
+* kernel means: bitwise (sha256) equal to the reference's float32 means;
+* block selection: identical ascending ids per (row, KV group), ties included;
+* outputs: float32 out within 1e-5 (CUDA-core path) / 2e-3 abs + 2e-2 rel
+  (tensor-core path, bf16 P) of the reference; LSE within 1e-5 / 1e-4.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import case_inputs, case_names, load
+from inputs import digest, make_qkv
+from oracle import infllm2_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2506_07900_b200 as P  # noqa: E402
+
+
+def _cfg(meta):
+    return P.SparseAttentionConfig(**meta["geometry"])
+
+
+def _layer(meta, k, v, cfg):
+    layer = P.BlockizedLayerCache(meta["hkv"], meta["d"], cfg, capacity=meta["length"])
+    layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    return layer
+
+
+def _means_np(t: torch.Tensor) -> np.ndarray:
+    return t.contiguous().cpu().numpy()
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_kernel_means_bitwise_vs_reference(name):
+    meta, _ = load(name)
+    q, k, v = case_inputs(meta)
+    layer = _layer(meta, k, v, _cfg(meta))
+    torch.cuda.synchronize()
+    assert digest(_means_np(layer.fine_means)) == meta["fine_sha"]
+    assert digest(_means_np(layer.coarse_means)) == meta["coarse_sha"]
+    f, c = layer.rebuild_kernels()
+    assert digest(_means_np(f)) == meta["fine_sha"]
+    assert digest(_means_np(c)) == meta["coarse_sha"]
+
+
+@pytest.mark.parametrize("name", ["inc_small", "inc_b8"])
+def test_incremental_append_truncate_bitwise(name):
+    meta, z = load(name)
+    cfg = P.SparseAttentionConfig(**meta["geometry"])
+    layer = P.BlockizedLayerCache(meta["hkv"], meta["d"], cfg)
+    for step, (op, arg) in enumerate(z["ops"]):
+        if op == 0:
+            kk = make_qkv(meta["seed"] + step, int(arg), 1, 1, meta["hkv"], meta["d"])[1]
+            t = torch.from_numpy(kk).cuda()
+            layer.append(t, t)
+        else:
+            layer.truncate(int(arg))
+        assert layer.length == meta["lengths"][step]
+        assert digest(_means_np(layer.fine_means)) == meta["fine_sha"][step], step
+        assert digest(_means_np(layer.coarse_means)) == meta["coarse_sha"][step], step
+
+
+def _run_case(name, exact):
+    meta, z = load(name)
+    q, k, v = case_inputs(meta)
+    cfg = _cfg(meta)
+    layer = _layer(meta, k, v, cfg)
+    rows = z["rows"]
+    qd = torch.from_numpy(q[rows]).cuda()
+    # rows may be a sample: run each contiguous run of rows as one call
+    sels, outs, lses = [], [], []
+    runs = np.split(np.arange(rows.size), np.flatnonzero(np.diff(rows) != 1) + 1)
+    for run in runs:
+        o, s, l = P.two_stage_attention(qd[run[0]:run[-1] + 1], layer, cfg, meta["start"] + int(rows[run[0]]),
+                                        return_selection=True, return_lse=True,
+                                        out_dtype=torch.float32, exact=exact)
+        sels.append(s)
+        outs.append(o)
+        lses.append(l)
+    sel = torch.cat(sels).cpu().numpy()
+    out = torch.cat(outs).cpu().numpy()
+    lse = torch.cat(lses).cpu().numpy()
+    return meta, z, q, k, v, cfg, sel, out, lse
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["simt", "default"])
+@pytest.mark.parametrize("name", case_names())
+def test_selection_and_outputs_vs_reference(name, exact):
+    meta, z, q, k, v, cfg, sel, out, lse = _run_case(name, exact)
+    bad = np.argwhere((sel != z["selection"]).any(axis=-1))
+    assert bad.size == 0, f"{len(bad)} (row, group) selections differ, first {bad[:4].tolist()}"
+    pos_of = {int(r): j for j, r in enumerate(z["rows"])}
+    idx = [pos_of[int(r)] for r in z["out_rows"]]
+    got = out[idx]
+    want = z["out"]
+    if exact:
+        assert np.max(np.abs(got - want)) <= 1e-5
+    else:
+        assert np.all(np.abs(got - want) <= 2e-3 + 2e-2 * np.abs(want))
+    # LSE vs the oracle restatement over the same (reference) selection
+    geom = O.Geometry(**meta["geometry"])
+    fine = O.window_means(k, geom.kernel_size, geom.kernel_stride)
+    sub = z["out_rows"][:8]
+    ref = O.two_stage_attention(q, k, v, fine, geom, meta["start"], rows=sub)
+    tol = 1e-5 if exact else 1e-4
+    assert np.max(np.abs(lse[[pos_of[int(r)] for r in sub]] - ref.lse[sub])) <= tol
+
+
+def test_touch_stats_and_traces_match_reference_counts():
+    meta, z = load("b8_2k_prefill")
+    q, k, v = case_inputs(meta)
+    cfg = _cfg(meta)
+    layer = _layer(meta, k, v, cfg)
+    stats = P.TouchStats()
+    traces = []
+    P.two_stage_attention(torch.from_numpy(q).cuda(), layer, cfg, 0, stats=stats, traces=traces)
+    assert stats.stage1 == meta["stage1_rows"]
+    assert stats.stage2 == meta["stage2_rows"]
+    assert stats.dense_rows == meta["dense_rows"]
+    assert len(traces) == 2 * 2048
+    t = traces[2 * 1500 + 1]
+    assert t["query_pos"] == 1500 and t["group"] == 1
+    assert t["selected"] == [int(b) for b in z["selection"][1500, 1] if b >= 0]
+    np.testing.assert_allclose(t["scores_topk"], z["scores_topk"][1500, 1, :len(t["selected"])], rtol=1e-5)
+
+
+@pytest.mark.parametrize("length,topk", [(8192, 16), (6000, 8), (4096, 64)])
+def test_random_vs_oracle_sampled_rows(length, topk):
+    """Larger caches than the fixtures: GPU vs oracle (f64 dots) on sampled rows."""
+    geom = O.Geometry(top_k=topk)
+    cfg = P.SparseAttentionConfig(top_k=topk)
+    q, k, v = make_qkv(1234 + length, length, length, 32, 2, 128)
+    layer = P.BlockizedLayerCache(2, 128, cfg, capacity=length)
+    layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    o, s, l = P.two_stage_attention(torch.from_numpy(q).cuda(), layer, cfg, 0, return_selection=True,
+                                    return_lse=True, out_dtype=torch.float32)
+    s, o, l = s.cpu().numpy(), o.cpu().numpy(), l.cpu().numpy()
+    rng = np.random.default_rng(length)
+    rows = np.unique(np.concatenate([[0, 63, 64, length - 1], rng.integers(0, length, 40)]))
+    fine = O.window_means(k, geom.kernel_size, geom.kernel_stride)
+    ref = O.two_stage_attention(q, k, v, fine, geom, 0, rows=rows)
+    mism = [(int(r), g, float(ref.margins[r, g])) for r in rows for g in range(2)
+            if not np.array_equal(s[r, g], ref.selection[r, g])]
+    assert not mism, f"selection mismatches (row, group, oracle margin): {mism[:5]}"
+    assert np.all(np.abs(o[rows] - ref.out[rows]) <= 2e-3 + 2e-2 * np.abs(ref.out[rows]))
+    assert np.max(np.abs(l[rows] - ref.lse[rows])) <= 1e-4
+
+
+def test_decode_steps_match_prefill_rows():
+    """Appending one row at a time (decode) == the same rows in one prefill call
+    when the cache length is the same at call time."""
+    cfg = P.SparseAttentionConfig(top_k=16)
+    q, k, v = make_qkv(77, 3000, 3000, 32, 2, 128)
+    kd, vd, qd = (torch.from_numpy(x).cuda() for x in (k, v, q))
+    layer = P.BlockizedLayerCache(2, 128, cfg)
+    layer.append(kd[:2900], vd[:2900])
+    for t in range(2900, 3000):
+        layer.append(kd[t:t + 1], vd[t:t + 1])
+        o, s = P.two_stage_attention(qd[t:t + 1], layer, cfg, t, return_selection=True,
+                                     out_dtype=torch.float32)
+        ref_layer = P.BlockizedLayerCache(2, 128, cfg)
+        if t % 25 == 0:
+            ref_layer.append(kd[:t + 1], vd[:t + 1])
+            o2, s2 = P.two_stage_attention(qd[t:t + 1], ref_layer, cfg, t, return_selection=True,
+                                           out_dtype=torch.float32)
+            assert torch.equal(s, s2)
+            assert torch.equal(o, o2)
+
+
+def test_validation_errors():
+    cfg = P.SparseAttentionConfig()
+    layer = P.BlockizedLayerCache(2, 128, cfg)
+    k = torch.zeros(100, 2, 128, device="cuda")
+    layer.append(k, k)
+    with pytest.raises(P.ValidationError):
+        P.two_stage_attention(torch.zeros(1, 32, 128, device="cuda"), layer, cfg, 100)
+    with pytest.raises(P.ValidationError):
+        P.two_stage_attention(torch.zeros(1, 31, 128, device="cuda"), layer, cfg, 10)
+    with pytest.raises(P.ValidationError):
+        layer.truncate(101)
+    with pytest.raises(P.ValidationError):
+        layer.append(torch.zeros(3, 3, 128, device="cuda"), torch.zeros(3, 3, 128, device="cuda"))
+
+
+def test_dense_degradation_vs_dense_oracle():
+    """Budget covers every block -> equals dense attention (test_acceptance.py:68-106)."""
+    rng = np.random.default_rng(101)
+    worst = 0.0
+    for trial in range(30):
+        m = int(rng.choice([8, 16, 32, 64]))
+        cfg = P.SparseAttentionConfig(block_size=m, kernel_size=m // 2, kernel_stride=m // 4,
+                                      coarse_stride=m // 2, top_k=int(rng.integers(1, 5)),
+                                      n_init_blocks=int(rng.integers(0, 3)),
+                                      n_local_blocks=int(rng.integers(0, 3)))
+        n_blocks = int(rng.integers(1, cfg.max_selected + 1))
+        length = max(n_blocks * m - int(rng.integers(0, m)), 1)
+        q, k, v = make_qkv(trial, length, 1, 4, 2, 8)
+        layer = P.BlockizedLayerCache(2, 8, cfg)
+        layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+        out = P.two_stage_attention(torch.from_numpy(q).cuda(), layer, cfg, length - 1,
+                                    out_dtype=torch.float32).cpu().numpy()
+        dense, _ = O.dense_attention(q, k, v, length - 1)
+        worst = max(worst, float(np.abs(out - dense).max()))
+    assert worst < 1e-5
