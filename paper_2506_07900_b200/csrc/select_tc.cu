@@ -1,0 +1,526 @@
+// Stage-1 block selection on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Production geometry: GQA group G = 16 heads, D = 128, s = 16, p = 2s, m a
+// multiple of s with (m/s) | 128.  Replaces, for every query row and KV group,
+// kernel_scores + softmax_f64 + group_scores + block_scores + force_blocks +
+// select_topk (sparse.py:163-277, model.py:185-191) as called per row by
+// two_stage_attention (sparse.py:421-451).
+//
+// Work unit = 16 consecutive query positions t0..t0+15 (t0 % 16 == 0) of one
+// KV group: 256 (query, head) rows.  Because 16 | s and 16 | m, all 16 rows
+// see the same kernel count nk_t = min(t0/s + 1, L/s) (sparse.py:426) and the
+// same candidate blocks, so one unit is one dense, masked-at-the-tail GEMM.
+//
+// Kernel means enter as a bf16 hi/lo split (mu = hi + lo to ~2^-17 relative,
+// SURVEY F7): every product is formed twice and accumulated in f32 TMEM.
+//
+//   pass 1  S[row, j]   = Q(256x128) . mu^T        (A = Q rows, B = mu tile)
+//           online max / sum of 2^z per row   ->  lse2[row]     (softmax normaliser)
+//   pass 2  S^T[j, row] = mu(128x128) . Q^T        (A = mu tile, B = Q, N = 256)
+//           p = 2^(z - lse2[row]); group score S_j = mean_h p    (in-thread: a thread
+//           owns one kernel j and all 16 heads of a query -> no shuffles)
+//           block max over each block's kernels (sparse.py:191-215) -> workspace
+//   top-k   per query: forced blocks + budget best non-forced by (-R, id).
+//
+// Warp roles (10 warps): 0 = TMA producer, 1 = TMEM allocator + MMA issuer,
+// 2..9 = epilogue (TMEM -> registers -> softmax math).  TMEM: 512 columns =
+// two 256-column accumulator buffers, so the epilogue of tile c overlaps the
+// MMAs of tile c+1.  Shared memory: Q 64 KB + 2 stages x 64 KB of mu.
+#include <float.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tc_dispatch.cuh"
+
+namespace infllm2 {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kQ = 16;            // query positions per work unit
+constexpr int kG = 16;            // heads per KV group
+constexpr int kRows = kQ * kG;    // 256 (query, head) rows
+constexpr int kD = 128;
+constexpr int kNT = 128;          // kernels per tile
+constexpr int kStages = 2;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (2 + kEpiWarps);
+constexpr int kEpiThreads = 32 * kEpiWarps;
+
+constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
+constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 128 B)
+constexpr uint32_t kMuStageBytes = 4 * kMuHalfBytes;       // hi h0,h1, lo h0,h1 = 64 KB
+constexpr int kSTileLd = kNT + 4;                          // [carry | 128 kernels] + pad
+
+struct SmemLayout {
+  static constexpr uint32_t q = 0;
+  static constexpr uint32_t mu = q + kQBytes;
+  static constexpr uint32_t stile = mu + kStages * kMuStageBytes;          // float [kQ][kSTileLd]
+  static constexpr uint32_t lse2 = stile + kQ * kSTileLd * 4;              // float [kRows]
+  static constexpr uint32_t bars = lse2 + kRows * 4;                       // uint64 [..]
+  static constexpr uint32_t topk = bars + 16 * 8;                          // per warp lists
+  static constexpr uint32_t total = topk + kEpiWarps * 2 * 80 * 12 + 16;
+};
+
+struct Params {
+  int64_t n, start, cache_len, nk_total;
+  int hkv, max_sel;
+  int m, kpb;                     // block size, kernels per block
+  int top_k, n_init, n_local, consume;
+  int64_t units_per_group, n_units;
+  int64_t first_t0;               // aligned position of unit 0
+  int32_t* selection;
+  double* sel_scores;
+  float* rbuf;                    // [grid][kQ][nb_cap]
+  int64_t nb_cap;
+  float zscale;                   // log2(e)/sqrt(D)
+};
+
+// unit index -> (t0, group); heaviest (largest t0) units first
+__device__ __forceinline__ void unit_coords(const Params& p, int64_t u, int64_t* t0, int* grp) {
+  const int64_t tile = p.units_per_group - 1 - u / p.hkv;
+  *grp = (int)(u % p.hkv);
+  *t0 = p.first_t0 + tile * kQ;
+}
+
+__device__ __forceinline__ int64_t unit_nk(const Params& p, int64_t t0) {
+  int64_t nk = t0 / 16 + 1;
+  return nk < p.nk_total ? nk : p.nk_total;
+}
+
+__device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t nk) {
+  const int64_t qb = t0 / p.m;
+  int64_t need = (qb + 1) * p.kpb;
+  if (nk > need) need = nk;
+  return (int)((need + kNT - 1) / kNT);
+}
+
+__device__ __forceinline__ bool better(float ra, int ba, float rb, int bb) {
+  return ra > rb || (ra == rb && ba < bb);   // (score desc, id asc), sparse.py:273
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_hi,
+                 const __grid_constant__ CUtensorMap tm_lo, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem + SmemLayout::q;
+  uint8_t* smu = smem + SmemLayout::mu;
+  float* stile = reinterpret_cast<float*>(smem + SmemLayout::stile);
+  float* lse2 = reinterpret_cast<float*>(smem + SmemLayout::lse2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* mu_full = bars + 2;             // [kStages]
+  uint64_t* mu_empty = bars + 2 + kStages;  // [kStages]
+  uint64_t* acc_full = bars + 2 + 2 * kStages;       // [2]
+  uint64_t* acc_empty = bars + 4 + 2 * kStages;      // [2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * kStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < kStages; ++s) { mbar_init(mu_full + s, 1); mbar_init(mu_empty + s, 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(acc_full + b, 1); mbar_init(acc_empty + b, kEpiWarps); }
+    fence_barrier_init();
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_hi);
+    tma_prefetch(&tm_lo);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0, q_phase = 0;
+      for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        int64_t t0;
+        int grp;
+        unit_coords(p, u, &t0, &grp);
+        const int64_t nk = unit_nk(p, t0);
+        const int tiles = unit_tiles(p, t0, nk);
+        mbar_wait(q_empty, q_phase ^ 1);
+        q_phase ^= 1;
+        mbar_arrive_expect_tx(q_full, kQBytes);
+        const int i0 = (int)(t0 - p.start);
+        tma_load_3d(sq, &tm_q, q_full, 0, grp * kG, i0);
+        tma_load_3d(sq + kQBytes / 2, &tm_q, q_full, 64, grp * kG, i0);
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int c = 0; c < tiles; ++c) {
+            mbar_wait(mu_empty + stage, phase ^ 1);
+            uint8_t* dst = smu + stage * kMuStageBytes;
+            mbar_arrive_expect_tx(mu_full + stage, kMuStageBytes);
+            tma_load_3d(dst, &tm_hi, mu_full + stage, 0, c * kNT, grp);
+            tma_load_3d(dst + kMuHalfBytes, &tm_hi, mu_full + stage, 64, c * kNT, grp);
+            tma_load_3d(dst + 2 * kMuHalfBytes, &tm_lo, mu_full + stage, 0, c * kNT, grp);
+            tma_load_3d(dst + 3 * kMuHalfBytes, &tm_lo, mu_full + stage, 64, c * kNT, grp);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc1 = idesc_bf16_f32(128, 128);
+    const uint32_t idesc2 = idesc_bf16_f32(128, 256);
+    const uint32_t q_addr = smem_u32(sq);
+    const uint32_t mu_addr = smem_u32(smu);
+    int stage = 0, buf = 0;
+    uint32_t phase = 0, q_phase = 0;
+    uint32_t acc_phase[2] = {0, 0};
+    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      int64_t t0;
+      int grp;
+      unit_coords(p, u, &t0, &grp);
+      const int64_t nk = unit_nk(p, t0);
+      const int tiles = unit_tiles(p, t0, nk);
+      mbar_wait(q_full, q_phase);
+      q_phase ^= 1;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int c = 0; c < tiles; ++c) {
+          mbar_wait(mu_full + stage, phase);
+          mbar_wait(acc_empty + buf, acc_phase[buf] ^ 1);
+          acc_phase[buf] ^= 1;
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t mu_s = mu_addr + stage * kMuStageBytes;
+            const uint32_t d0 = tmem + buf * 256;
+            for (int part = 0; part < 2; ++part) {           // hi, then lo
+              const uint32_t mu_p = mu_s + part * 2 * kMuHalfBytes;
+              for (int k = 0; k < kD / 16; ++k) {
+                const uint32_t koff = (k >> 2) * 0 + (k & 3) * 32;
+                const uint32_t mu_k = mu_p + (k >> 2) * kMuHalfBytes + koff;
+                const uint32_t q_k = q_addr + (k >> 2) * (kQBytes / 2) + koff;
+                const uint32_t acc = (part | k) ? 1u : 0u;
+                if (pass == 0) {
+                  umma_f16_ss(d0, sdesc_k_sw128(q_k), sdesc_k_sw128(mu_k), idesc1, acc);
+                  umma_f16_ss(d0 + 128, sdesc_k_sw128(q_k + 128 * 128), sdesc_k_sw128(mu_k), idesc1, acc);
+                } else {
+                  umma_f16_ss(d0, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc2, acc);
+                }
+              }
+            }
+            umma_commit(mu_empty + stage);
+            umma_commit(acc_full + buf);
+            if (pass == 1 && c == tiles - 1) umma_commit(q_empty);
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          buf ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;                 // 0..7
+    const int quad = warp & 3;               // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;                // pass 1: query tile; pass 2: column half
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const int etid = ew * 32 + lane;         // 0..255
+    int buf = 0;
+    uint32_t acc_phase[2] = {0, 0};
+    float* rbuf = p.rbuf + (int64_t)blockIdx.x * kQ * p.nb_cap;
+    uint8_t* topk_base = smem + SmemLayout::topk + ew * 2 * 80 * 12;
+
+    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      int64_t t0;
+      int grp;
+      unit_coords(p, u, &t0, &grp);
+      const int64_t nk = unit_nk(p, t0);
+      const int tiles = unit_tiles(p, t0, nk);
+      const int64_t qb = t0 / p.m;
+      const int64_t n_cand = qb + 1;
+
+      // ---- pass 1: row LSE (log2 domain)
+      {
+        const int row = half * 128 + quad * 32 + lane;
+        float mrun = -INFINITY, srun = 0.f;
+        for (int c = 0; c < tiles; ++c) {
+          mbar_wait(acc_full + buf, acc_phase[buf]);
+          acc_phase[buf] ^= 1;
+          tc_fence_after();
+          const int64_t jbase = (int64_t)c * kNT;
+#pragma unroll 1
+          for (int ch = 0; ch < 4; ++ch) {
+            float v[32];
+            tmem_ld32(tmem + lane_base + buf * 256 + half * 128 + ch * 32, v);
+            tmem_wait_ld();
+            const int64_t j0 = jbase + ch * 32;
+            float cmax = -INFINITY;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              v[x] = (j0 + x < nk) ? v[x] * p.zscale : -INFINITY;
+              cmax = fmaxf(cmax, v[x]);
+            }
+            const float mnew = fmaxf(mrun, cmax);
+            if (mnew != -INFINITY) {
+              float acc = 0.f;
+#pragma unroll
+              for (int x = 0; x < 32; ++x) acc += ex2(v[x] - mnew);
+              srun = srun * ex2(mrun - mnew) + acc;
+              mrun = mnew;
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty + buf);
+          buf ^= 1;
+        }
+        lse2[row] = mrun + log2f(srun);
+      }
+      named_bar_sync(1, kEpiThreads);
+
+      // ---- pass 2: group scores per kernel, block max
+      if (etid < kQ) stile[etid * kSTileLd] = -INFINITY;   // carry (kernel -1)
+      for (int c = 0; c < tiles; ++c) {
+        mbar_wait(acc_full + buf, acc_phase[buf]);
+        acc_phase[buf] ^= 1;
+        tc_fence_after();
+        const int jl = quad * 32 + lane;
+        const bool live = (int64_t)c * kNT + jl < nk;
+#pragma unroll 1
+        for (int qq = 0; qq < 8; ++qq) {
+          const int qi = half * 8 + qq;
+          float v[16];
+          tmem_ld16(tmem + lane_base + buf * 256 + qi * 16, v);
+          tmem_wait_ld();
+          const float* l2 = lse2 + qi * kG;
+          float sacc = 0.f;
+#pragma unroll
+          for (int h = 0; h < kG; ++h) sacc += ex2(v[h] * p.zscale - l2[h]);
+          stile[qi * kSTileLd + 1 + jl] = live ? sacc * (1.0f / kG) : -INFINITY;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + buf);
+        buf ^= 1;
+        named_bar_sync(1, kEpiThreads);
+        // blocks whose last kernel lies in this tile
+        const int bpt = kNT / p.kpb;
+        for (int x = etid; x < kQ * bpt; x += kEpiThreads) {
+          const int qi = x / bpt;
+          const int64_t b = (int64_t)c * bpt + (x - qi * bpt);
+          if (b < n_cand) {
+            const int64_t lo = b * p.kpb - 1 < 0 ? 0 : b * p.kpb - 1;
+            const int64_t hi = (b + 1) * p.kpb;
+            float r = -INFINITY;
+            for (int64_t j = lo; j < hi; ++j) r = fmaxf(r, stile[qi * kSTileLd + 1 + (int)(j - (int64_t)c * kNT)]);
+            rbuf[(int64_t)qi * p.nb_cap + b] = (r == -INFINITY) ? 0.f : r;
+          }
+        }
+        named_bar_sync(1, kEpiThreads);
+        if (etid < kQ) stile[etid * kSTileLd] = stile[etid * kSTileLd + kNT];
+        named_bar_sync(1, kEpiThreads);
+      }
+
+      // ---- top-k per query (warp ew handles queries ew and ew + 8)
+      const int64_t n_init = p.n_init < n_cand ? p.n_init : n_cand;
+      int64_t local_lo = qb + 1;
+      if (p.n_local > 0) {
+        local_lo = qb - p.n_local + 1;
+        if (local_lo < 0) local_lo = 0;
+        if (local_lo < n_init) local_lo = n_init;
+      }
+      const int64_t n_forced = n_init + (qb + 1 - local_lo);
+      int64_t budget = p.top_k;
+      if (p.consume) budget = p.top_k - n_forced > 0 ? p.top_k - n_forced : 0;
+      const int64_t n_free = n_cand - n_forced;
+      for (int sub = 0; sub < 2; ++sub) {
+        const int qi = ew + sub * 8;
+        const int64_t t = t0 + qi;
+        const int64_t i = t - p.start;
+        if (i < 0 || i >= p.n) continue;    // warp-uniform
+        float* rq = rbuf + (int64_t)qi * p.nb_cap;
+        int* ids = reinterpret_cast<int*>(topk_base + sub * 80 * 12);
+        float* scs = reinterpret_cast<float*>(ids + 80);
+        int cnt = 0;
+        if (lane == 0) {
+          for (int64_t b = 0; b < n_init; ++b) { ids[cnt] = (int)b; scs[cnt] = rq[b]; ++cnt; }
+          for (int64_t b = local_lo; b <= qb; ++b) { ids[cnt] = (int)b; scs[cnt] = rq[b]; ++cnt; }
+          if (budget >= n_free)
+            for (int64_t b = n_init; b < local_lo; ++b) { ids[cnt] = (int)b; scs[cnt] = rq[b]; ++cnt; }
+        }
+        if (budget < n_free) {
+          for (int64_t it = 0; it < budget; ++it) {
+            float bv = -1.f;
+            int bb = -1;
+            for (int64_t b = n_init + lane; b < local_lo; b += 32) {
+              const float r = rq[b];
+              if (r >= 0.f && (bb < 0 || better(r, (int)b, bv, bb))) { bv = r; bb = (int)b; }
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+              const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+              const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
+              if (ob >= 0 && (bb < 0 || better(ov, ob, bv, bb))) { bv = ov; bb = ob; }
+            }
+            if (lane == 0) {
+              ids[cnt] = bb;
+              scs[cnt] = bv;
+              ++cnt;
+              rq[bb] = -1.f;
+            }
+            __syncwarp();
+          }
+        }
+        if (lane == 0) {
+          for (int x = 1; x < cnt; ++x) {
+            const int key = ids[x];
+            const float sv = scs[x];
+            int y = x - 1;
+            while (y >= 0 && ids[y] > key) { ids[y + 1] = ids[y]; scs[y + 1] = scs[y]; --y; }
+            ids[y + 1] = key;
+            scs[y + 1] = sv;
+          }
+          const int64_t item = i * p.hkv + grp;
+          int32_t* out = p.selection + item * p.max_sel;
+          for (int x = 0; x < p.max_sel; ++x) out[x] = x < cnt ? ids[x] : -1;
+          if (p.sel_scores) {
+            double* osc = p.sel_scores + item * p.max_sel;
+            for (int x = 0; x < p.max_sel; ++x) osc[x] = x < cnt ? (double)scs[x] : 0.0;
+          }
+        }
+        __syncwarp();
+      }
+      named_bar_sync(1, kEpiThreads);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------------ host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(ptr);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+bool encode_tmap_3d_bf16(CUtensorMap* map, const void* base, const uint64_t dims[3],
+                         const uint64_t strides_bytes[2], const uint32_t box[3]) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t gd[3] = {dims[0], dims[1], dims[2]};
+  cuuint64_t gs[2] = {strides_bytes[0], strides_bytes[1]};
+  cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gd, gs, bx, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int tc_grid(int64_t n_units) {
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (int)(n_units < sms ? n_units : sms);
+}
+
+bool tc_kernels_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("INFLLM2_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool have_split_means) {
+  if (!have_split_means || !tc_kernels_enabled()) return false;
+  if (cs.group != kG || cs.d != kD) return false;
+  if (g.kernel_stride != 16 || g.kernel_size != 32) return false;
+  if (g.block_size % 16 != 0 || kNT % (g.block_size / 16) != 0) return false;
+  if (g.top_k + g.n_init_blocks + g.n_local_blocks > 80) return false;
+  if (cs.nk_total < 1) return false;
+  return true;
+}
+
+size_t tc_select_workspace(const infllm2_geometry& g, const CallShape& cs, int) {
+  if (cs.group != kG || cs.d != kD) return 0;
+  const int64_t nb_cap = cs.cache_len / g.block_size + 2;
+  return (size_t)kNumSMs * kQ * nb_cap * sizeof(float);
+}
+
+cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                             int64_t q_row_stride, const float* /*means*/, const void* means_hi,
+                             const void* means_lo, int64_t means_cap, int32_t* selection,
+                             double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  Params p;
+  p.n = cs.n;
+  p.start = cs.start;
+  p.cache_len = cs.cache_len;
+  p.nk_total = cs.nk_total;
+  p.hkv = cs.hkv;
+  p.max_sel = cs.max_sel;
+  p.m = g.block_size;
+  p.kpb = g.block_size / g.kernel_stride;
+  p.top_k = g.top_k;
+  p.n_init = g.n_init_blocks;
+  p.n_local = g.n_local_blocks;
+  p.consume = g.forced_consume_budget;
+  p.first_t0 = cs.start / kQ * kQ;
+  const int64_t last = cs.start + cs.n - 1;
+  p.units_per_group = (last - p.first_t0) / kQ + 1;
+  p.n_units = p.units_per_group * cs.hkv;
+  p.selection = selection;
+  p.sel_scores = sel_scores;
+  p.nb_cap = cs.cache_len / g.block_size + 2;
+  p.zscale = 1.4426950408889634f / sqrtf((float)kD);
+  const int grid = tc_grid(p.n_units);
+  if ((size_t)grid * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
+  p.rbuf = static_cast<float*>(ws);
+
+  CUtensorMap tq, thi, tlo;
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)cs.n};
+    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)q_row_stride * 2};
+    const uint32_t box[3] = {64, (uint32_t)kG, (uint32_t)kQ};
+    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)means_cap, (uint64_t)cs.hkv};
+    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)means_cap * kD * 2};
+    const uint32_t box[3] = {64, (uint32_t)kNT, 1};
+    if (!encode_tmap_3d_bf16(&thi, means_hi, dims, strides, box)) return cudaErrorInvalidValue;
+    if (!encode_tmap_3d_bf16(&tlo, means_lo, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  const size_t smem = SmemLayout::total + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  select_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, thi, tlo, p);
+  return cudaGetLastError();
+}
+
+// Stage-2 tensor-core kernel not yet wired: every attend call uses the CUDA-core kernel.
+bool tc_attend_supported(const infllm2_geometry&, const CallShape&) { return false; }
+cudaError_t launch_attend_tc(const infllm2_geometry&, const CallShape&, const void*, int64_t, const void*,
+                             const void*, int64_t, const int32_t*, void*, int, float*, cudaStream_t) {
+  return cudaErrorNotSupported;
+}
+
+}  // namespace infllm2
