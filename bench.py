@@ -1,0 +1,515 @@
+#!/usr/bin/env python3
+"""InfLLM v2 prefill benchmark (BASELINE.json configs[2]): 32-layer MiniCPM4-8B-shaped
+sparse-attention stack (32 q heads / 2 KV heads / d 128, m=64, p=32, s=16, k=16,
+init 1, local 2), 128K-token prefill, query-sequence sharded over N GPUs.
+
+One step = for every layer: the layer's K/V rows enter the blockized cache
+(NCCL all-gather of the per-rank token shards when N > 1, append, kernel-mean
+compression), then two_stage_attention over this rank's query rows (stage-1
+tcgen05 selection + stage-2 attention).  Inputs (synthetic bf16, N(0,1), per
+layer) are resident in HBM before the timed region; the cache working set
+(128 MiB K/V per layer) exceeds nothing in L2's favour across layers (32 layers x
+1.2 GiB of inputs > 126 MB L2), stated in config.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N > 1 under torchrun.
+`--impl reference` times the CPU oracle port (oracle/, the reference's algorithm
+restated in numpy) on the host cores for the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEQ = 131072
+LAYERS = 32
+HQ, HKV, D = 32, 2, 128
+GEOM = dict(block_size=64, kernel_size=32, kernel_stride=16, coarse_stride=128, top_k=16,
+            n_init_blocks=1, n_local_blocks=2)
+METRIC = "InfLLM v2 prefill tok/s @128K (32-layer 8B-shaped sparse attention stack)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seq", type=int, default=SEQ)
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- workload
+
+
+def zigzag_chunks(seq: int, world: int, rank: int):
+    """Rank r owns chunks r and 2N-1-r of 2N equal chunks: stage-1 cost grows
+    linearly with position, so the pair sums to the same work on every rank."""
+    nch = 2 * world
+    size = seq // nch
+    bounds = [(c * size, (c + 1) * size if c < nch - 1 else seq) for c in range(nch)]
+    return [bounds[rank], bounds[nch - 1 - rank]]
+
+
+def algorithmic_work(seq: int, rows_list):
+    """Per layer, for the given query rows: stage-1 FLOPs (one QK pass,
+    2*D*HQ*sum nk_t) and stage-2 FLOPs (4*D*G*sum rows(t,g)) — SURVEY §8(d)."""
+    import numpy as np
+    s, m, k = GEOM["kernel_stride"], GEOM["block_size"], GEOM["top_k"]
+    nk_total = seq // s
+    f1 = f2 = 0.0
+    rows2 = 0
+    for lo, hi in rows_list:
+        t = np.arange(lo, hi, dtype=np.int64)
+        nk = np.minimum(t // s + 1, nk_total)
+        f1 += 2.0 * D * HQ * float(nk.sum())
+        n_cand = t // m + 1
+        n_forced = np.minimum(1, n_cand) + np.minimum(2, n_cand)  # init 1 + local 2 (disjoint once qb >= 2)
+        n_forced = np.where(t // m >= 2, 3, n_cand)
+        dense = (n_cand - n_forced) <= k
+        sparse_rows = (n_forced + k - 1) * m + (t % m) + 1
+        r = np.where(dense, t + 1, sparse_rows)
+        rows2 += int(r.sum()) * HKV
+        f2 += 4.0 * D * (HQ // HKV) * float(r.sum()) * HKV
+    return f1, f2, rows2
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2506_07900_b200 as P
+    from paper_2506_07900_b200 import _lib
+
+    lib = _lib.load()
+    seq, layers = args.seq, args.layers
+    cfg = P.SparseAttentionConfig(**GEOM)
+    chunks = zigzag_chunks(seq, world, rank)
+    my_rows = sum(hi - lo for lo, hi in chunks)
+
+    # ---- synthetic per-layer inputs, resident in HBM (each rank holds its own
+    # token shard of K/V and its own query rows)
+    gen = torch.Generator(device=dev)
+    q_in, k_in, v_in = [], [], []
+    for layer in range(layers):
+        gen.manual_seed(1_000_003 * layer + 17)
+        qs = [torch.randn((hi - lo, HQ, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+              for lo, hi in chunks]
+        ks = [torch.randn((hi - lo, HKV, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+              for lo, hi in chunks]
+        vs = [torch.randn((hi - lo, HKV, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+              for lo, hi in chunks]
+        q_in.append(qs)
+        k_in.append(ks)
+        v_in.append(vs)
+    caches = [P.BlockizedLayerCache(HKV, D, cfg, capacity=seq, device=dev) for _ in range(layers)]
+    size = seq // (2 * world)
+    gath_k = [torch.empty((world, size, HKV, D), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    gath_v = [torch.empty_like(g) for g in gath_k]
+
+    stream = torch.cuda.current_stream(dev)
+    ev_sel = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(layers * 2)]
+    ev_att = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(layers * 2)]
+
+    def fill_cache(layer):
+        """All-gather the token shards of K/V (the real exchange step), then
+        append in natural order and compress."""
+        cache = caches[layer]
+        cache.truncate(0)
+        if world == 1:
+            for (lo, hi), kk, vv in zip(chunks, k_in[layer], v_in[layer]):
+                cache.append(kk, vv)
+            return
+        for h in range(2):
+            dist.all_gather_into_tensor(gath_k[h], k_in[layer][h])
+            dist.all_gather_into_tensor(gath_v[h], v_in[layer][h])
+        # natural chunk c: first half c -> gath[0][c]; second half -> gath[1][2N-1-c]
+        ks, vs = [], []
+        for c in range(2 * world):
+            if c < world:
+                ks.append(gath_k[0][c]); vs.append(gath_v[0][c])
+            else:
+                ks.append(gath_k[1][2 * world - 1 - c]); vs.append(gath_v[1][2 * world - 1 - c])
+        cache.append(torch.cat(ks), torch.cat(vs))
+
+    def attend(layer, timed=False, outs=None):
+        cache = caches[layer]
+        for h, (lo, hi) in enumerate(chunks):
+            q = q_in[layer][h]
+            if timed:
+                ev = ev_sel[2 * layer + h]
+                ev[0].record(stream)
+            o = P.two_stage_attention(q, cache, cfg, lo)
+            if timed:
+                ev[1].record(stream)
+            if outs is not None:
+                outs.append(o)
+
+    def step(timed=False):
+        for layer in range(layers):
+            fill_cache(layer)
+            attend(layer, timed)
+
+    # ---- per-kernel split (stage-1 select vs stage-2 attend) measured live via
+    # the C ABI on this stream, one extra untimed pass after the timed region
+    def split_pass():
+        geom = cfg.geometry()
+        import ctypes
+        t_sel = t_att = 0.0
+        for layer in range(layers):
+            fill_cache(layer)
+            cache = caches[layer]
+            kc, vc, cap, fine, hi, lo, mcap = cache._device_args()
+            for h, (rlo, rhi) in enumerate(chunks):
+                q = q_in[layer][h]
+                n = rhi - rlo
+                sel = torch.empty((n, HKV, cfg.max_selected), dtype=torch.int32, device=dev)
+                out = torch.empty((n, HQ, D), dtype=torch.bfloat16, device=dev)
+                wsb = lib.infllm2_select_workspace_bytes(ctypes.byref(geom), n, HQ, HKV, D, cache.length, 0)
+                ws = P.sparse._workspace(dev, wsb)
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream)
+                _lib.check(lib.infllm2_select(ctypes.byref(geom), q.data_ptr(), q.stride(0), n, rlo, HQ, HKV, D,
+                                              fine.data_ptr(), hi.data_ptr(), lo.data_ptr(), mcap, cache.length,
+                                              sel.data_ptr(), None, ws.data_ptr(), ws.numel(), 0,
+                                              stream.cuda_stream), "select")
+                e1.record(stream)
+                _lib.check(lib.infllm2_attend(ctypes.byref(geom), q.data_ptr(), q.stride(0), n, rlo, HQ, HKV, D,
+                                              kc.data_ptr(), vc.data_ptr(), cap, cache.length, sel.data_ptr(),
+                                              out.data_ptr(), None, 0, stream.cuda_stream), "attend")
+                e2.record(stream)
+                e2.synchronize()
+                t_sel += e0.elapsed_time(e1)
+                t_att += e1.elapsed_time(e2)
+        return t_sel, t_att
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = lib.infllm2_launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1)
+    launches = lib.infllm2_launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = seq / (ms_per_step / 1e3)       # whole-job tokens/s (each token through 32 layers)
+
+    # ---- dominant-kernel roofline (stage-1 select vs stage-2 attend)
+    t_sel, t_att = split_pass()
+    f1, f2, rows2 = algorithmic_work(seq, chunks)
+    f1 *= layers
+    f2 *= layers
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+    peak_t = peaks.get("bf16_tflops_sustained", 1383.3)
+    sel_tflops = f1 / (t_sel / 1e3) / 1e12
+    att_tflops = f2 / (t_att / 1e3) / 1e12
+    if t_sel >= t_att:
+        roof = {"kernel": "select_tc_kernel (stage-1)", "bound": "tensor", "achieved": round(sel_tflops, 2),
+                "peak": peak_t, "unit": "TFLOP/s", "frac": round(sel_tflops / peak_t, 4), "traffic": None,
+                "share_of_step": round(t_sel / (t_sel + t_att), 3)}
+    else:
+        roof = {"kernel": "attend (stage-2)", "bound": "tensor", "achieved": round(att_tflops, 2), "peak": peak_t,
+                "unit": "TFLOP/s", "frac": round(att_tflops / peak_t, 4), "traffic": None,
+                "share_of_step": round(t_att / (t_sel + t_att), 3)}
+    roof["stage1_ms_per_step"] = round(t_sel, 3)
+    roof["stage2_ms_per_step"] = round(t_att, 3)
+    roof["stage1_tflops"] = round(sel_tflops, 2)
+    roof["stage2_tflops"] = round(att_tflops, 2)
+    roof["stage2_gather_GBps"] = round(rows2 * layers * D * 2 * 2 / (t_att / 1e3) / 1e9, 1)
+
+    # ---- e2e through the public API with host buffers (pinned), H2D of every
+    # layer's q/k/v shard and D2H of the last layer's output inside the region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) bf16 q/k/v per layer (post-RoPE), torch.Generator seeded per layer",
+            "config": {"workload": f"configs[2]: {layers}-layer InfLLM v2 stack, {seq}-token prefill, "
+                                   f"32q/2kv/d128, m64 p32 s16 k16 init1 local2, query rows zig-zag sharded",
+                       "seq_len": seq, "layers": layers, "parallelism": f"query-shard x{world} (NCCL all-gather K/V)",
+                       "l2": "inputs 1.2 GiB/layer x 32 layers >> 126 MB L2 (no flush needed)"},
+            "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dist):
+    """Same metric through two_stage_attention with HOST inputs: per layer the
+    pinned q/k/v shards are copied H2D on a copy stream (overlapped with the
+    previous layer's compute), and the last layer's output is read back."""
+    import torch
+
+    layers = args.layers
+    nbuf = 2
+    host = []
+    for b in range(nbuf):
+        g = torch.Generator().manual_seed(99 + b)
+        host.append([[torch.randn((hi - lo, HQ, D), generator=g).to(torch.bfloat16).pin_memory() for lo, hi in chunks],
+                     [torch.randn((hi - lo, HKV, D), generator=g).to(torch.bfloat16).pin_memory() for lo, hi in chunks],
+                     [torch.randn((hi - lo, HKV, D), generator=g).to(torch.bfloat16).pin_memory() for lo, hi in chunks]])
+    dbuf = [[[torch.empty(t.shape, dtype=t.dtype, device=dev) for t in grp] for grp in hb] for hb in host]
+    out_host = torch.empty((chunks[0][1] - chunks[0][0], HQ, D), dtype=torch.bfloat16).pin_memory()
+    copy_stream = torch.cuda.Stream(dev)
+    h2d_bytes = sum(t.numel() * t.element_size() for grp in host[0] for t in grp) * layers
+    size = args.seq // (2 * world)
+    gk = [torch.empty((world, size, HKV, D), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    gv = [torch.empty_like(x) for x in gk]
+
+    def step():
+        ready = [torch.cuda.Event() for _ in range(layers)]
+        done = [torch.cuda.Event() for _ in range(layers)]
+        def issue_copy(layer):
+            b = layer % nbuf
+            with torch.cuda.stream(copy_stream):
+                if layer >= nbuf:
+                    copy_stream.wait_event(done[layer - nbuf])
+                for grp_h, grp_d in zip(host[b], dbuf[b]):
+                    for th, td in zip(grp_h, grp_d):
+                        td.copy_(th, non_blocking=True)
+                ready[layer].record(copy_stream)
+        issue_copy(0)
+        out = None
+        for layer in range(layers):
+            if layer + 1 < layers:
+                issue_copy(layer + 1)
+            stream.wait_event(ready[layer])
+            qd, kd, vd = dbuf[layer % nbuf]
+            cache = caches[layer]
+            cache.truncate(0)
+            if world == 1:
+                for kk, vv in zip(kd, vd):
+                    cache.append(kk, vv)
+            else:
+                for h in range(2):
+                    dist.all_gather_into_tensor(gk[h], kd[h])
+                    dist.all_gather_into_tensor(gv[h], vd[h])
+                ks = [gk[0][c] if c < world else gk[1][2 * world - 1 - c] for c in range(2 * world)]
+                vs = [gv[0][c] if c < world else gv[1][2 * world - 1 - c] for c in range(2 * world)]
+                cache.append(torch.cat(ks), torch.cat(vs))
+            for h, (lo, hi) in enumerate(chunks):
+                o = P.two_stage_attention(qd[h], cache, cfg, lo)
+                if layer == layers - 1 and h == 0:
+                    out = o
+            done[layer].record(stream)
+        out_host.copy_(out, non_blocking=True)
+        return out_host.numel() * out_host.element_size()
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    d2h = 0
+    for _ in range(args.steps):
+        d2h = step()
+    t1.record(stream)
+    barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(args.seq / (ms / args.steps / 1e3), 1), "unit": "tok/s",
+            "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
+            "note": "pinned host q/k/v per layer, H2D overlapped with compute on a copy stream"}
+
+
+# ----------------------------------------------------------------------------- CPU baseline (oracle)
+
+
+def _cpu_worker(payload):
+    rows, seed = payload
+    import numpy as np
+    from oracle import infllm2_oracle as O
+    st = _CPU_STATE
+    t0 = time.perf_counter()
+    O.two_stage_attention(st["q"], st["k"], st["v"], st["fine"], st["geom"], 0, rows=np.asarray(rows))
+    return time.perf_counter() - t0, len(rows)
+
+
+_CPU_STATE = {}
+
+
+def cpu_baseline(args, seconds=None, cores=None):
+    """Time the oracle port (the reference's algorithm in numpy) on sampled
+    query rows of a 128K cache, one process per host core.  Returns tok/s for
+    the 32-layer stack: rows/s / layers."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from oracle import infllm2_oracle as O
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    seconds = seconds or args.cpu_seconds
+    seq = args.seq
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((seq, HKV, D), dtype=np.float32)
+    v = rng.standard_normal((seq, HKV, D), dtype=np.float32)
+    geom = O.Geometry(**GEOM)
+    _CPU_STATE.update(k=k, v=v, fine=O.window_means(k, 32, 16), geom=geom)
+    cores = cores or os.cpu_count() or 1
+    # rows sampled uniformly over positions (cost grows with position)
+    n_rows = max(cores * 2, 16)
+    rows = np.sort(rng.choice(seq, size=n_rows * 64, replace=False))
+    q = np.zeros((seq, HQ, D), np.float32)
+    q[rows] = rng.standard_normal((rows.size, HQ, D), dtype=np.float32)
+    _CPU_STATE["q"] = q
+    ctx = mp.get_context("fork")
+    done_rows = 0
+    busy = 0.0
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        batches = [(rows[i::rows.size // 2][:2].tolist(), i) for i in range(rows.size // 2)]
+        it = pool.imap_unordered(_cpu_worker, batches)
+        for dt, n in it:
+            done_rows += n
+            busy += dt
+            if time.perf_counter() - t0 > seconds:
+                pool.terminate()
+                break
+    wall = time.perf_counter() - t0
+    rows_per_s = done_rows / wall
+    return {"value": round(rows_per_s / args.layers, 3), "unit": "tok/s", "cores": cores, "kind": "port",
+            "sample": f"{done_rows} query rows (both KV groups, uniform positions) of one {seq}-row layer in "
+                      f"{wall:.1f}s; tok/s = rows/s / {args.layers} layers",
+            "rows_per_s_one_layer": round(rows_per_s, 3)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        pass  # the oracle has nothing to warm beyond imports
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        c = cpu_baseline(args, seconds=max(5.0, args.cpu_seconds / max(1, args.steps)))
+        vals.append(c)
+    wall = time.perf_counter() - t0
+    value = sum(c["value"] for c in vals) / len(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * args.seq / value, 1) if value else None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (numpy)",
+            "data": "synthetic N(0,1)", "config": {"workload": "configs[2] sampled rows, CPU oracle port",
+                                                   "seq_len": args.seq, "layers": args.layers},
+            "cpu_baseline": {"value": round(value, 3), "unit": "tok/s", "cores": vals[0]["cores"], "kind": "port",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": round(value, 3), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": round(wall, 1)}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

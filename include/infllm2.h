@@ -82,6 +82,9 @@ const char* infllm2_strerror(int code);
 int infllm2_version(void);            /* major*10000 + minor*100 + patch */
 int infllm2_validate_geometry(const infllm2_geometry* g);  /* sparse.py:42-51 */
 int32_t infllm2_max_selected(const infllm2_geometry* g);
+/* Number of kernel launches this library has enqueued since load (host counter;
+ * lets callers report how many of the library's kernels ran in a region). */
+uint64_t infllm2_launch_count(void);
 
 /* Append n_new rows to the blockized cache at rows [l_old, l_old+n_new).
  * k_new/v_new are (n_new, HKV, D), rows `src_row_stride` elements apart,

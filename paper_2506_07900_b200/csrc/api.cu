@@ -9,7 +9,14 @@
 #include "common.cuh"
 #include "tc_dispatch.cuh"
 
+#include <atomic>
+
 using namespace infllm2;
+
+namespace infllm2 {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace infllm2
 
 namespace {
 
@@ -60,6 +67,8 @@ const char* infllm2_strerror(int code) {
 }
 
 int infllm2_version(void) { return 100; }
+
+uint64_t infllm2_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int infllm2_validate_geometry(const infllm2_geometry* g) {
   if (!g) return INFLLM2_ERR_CONFIG;

@@ -182,6 +182,7 @@ cudaError_t launch_attend_simt(const infllm2_geometry& g, const CallShape& cs, c
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
+  count_launch();
   attend_simt_kernel<<<grid, kThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }

@@ -49,6 +49,7 @@ __host__ __device__ inline void kernel_range_for_block(int64_t start, int64_t en
 
 // Kernel-launch entry points implemented in the .cu files (host side).
 namespace infllm2 {
+void count_launch();  // host-side counter behind infllm2_launch_count()
 cudaError_t launch_append_kv(void* k_cache, void* v_cache, int64_t cap, int hkv, int d,
                              const void* k_new, const void* v_new, int64_t n_new,
                              int64_t src_row_stride, int src_is_f32, int64_t l_old,

@@ -80,9 +80,11 @@ cudaError_t launch_append_kv(void* k_cache, void* v_cache, int64_t cap, int hkv,
   auto* kc = static_cast<__nv_bfloat16*>(k_cache);
   auto* vc = static_cast<__nv_bfloat16*>(v_cache);
   if (src_is_f32)
+    count_launch();
     append_kv_kernel<true><<<grid, 256, 0, stream>>>(kc, vc, cap, hkv, d, k_new, v_new, n_new,
                                                       src_row_stride, l_old);
   else
+    count_launch();
     append_kv_kernel<false><<<grid, 256, 0, stream>>>(kc, vc, cap, hkv, d, k_new, v_new, n_new,
                                                        src_row_stride, l_old);
   return cudaGetLastError();
@@ -93,6 +95,7 @@ cudaError_t launch_compress(const void* k_cache, int64_t cap, int hkv, int d, in
                             void* lo, int64_t means_cap, cudaStream_t stream) {
   if (count <= first) return cudaSuccess;
   const int grid = grid_for((count - first) * hkv * d, 256);
+  count_launch();
   compress_kernel<<<grid, 256, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(k_cache), cap, hkv, d, first, count, length, p, s, means,
       static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo), means_cap);

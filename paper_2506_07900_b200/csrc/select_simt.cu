@@ -269,6 +269,7 @@ cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, c
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
+  count_launch();
   select_simt_kernel<<<grid, kThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }

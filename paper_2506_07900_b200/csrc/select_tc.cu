@@ -512,6 +512,7 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  count_launch();
   select_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, thi, tlo, p);
   return cudaGetLastError();
 }
