@@ -79,12 +79,11 @@ cudaError_t launch_append_kv(void* k_cache, void* v_cache, int64_t cap, int hkv,
   const int grid = grid_for(n_new * hkv * d, 256);
   auto* kc = static_cast<__nv_bfloat16*>(k_cache);
   auto* vc = static_cast<__nv_bfloat16*>(v_cache);
+  count_launch();
   if (src_is_f32)
-    count_launch();
     append_kv_kernel<true><<<grid, 256, 0, stream>>>(kc, vc, cap, hkv, d, k_new, v_new, n_new,
                                                       src_row_stride, l_old);
   else
-    count_launch();
     append_kv_kernel<false><<<grid, 256, 0, stream>>>(kc, vc, cap, hkv, d, k_new, v_new, n_new,
                                                        src_row_stride, l_old);
   return cudaGetLastError();
