@@ -25,7 +25,7 @@ LIB = os.path.join(PKG, "libinfllm2.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SKIP = {"tc_stub.cu"}
+SKIP: set = set()
 
 
 def nvcc() -> str:

@@ -1,0 +1,470 @@
+// Stage-2 block-sparse attention on the tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces sparse_attend (sparse.py:347-384) for the production geometry
+// (G = 16 heads per KV group, D = 128, m = 64).  One work item is one
+// (query row, KV group); its selected blocks (ascending, from stage 1) are
+// gathered by TMA two at a time into 128-row K/V tiles:
+//
+//   S^T[128 rows x 16 heads] = K_tile (128x128, K-major) . Q^T      (TMEM)
+//   softmax warps: thread = row; mask rows beyond the query position
+//     (causal clip, sparse.py:370-372) and the empty half of a 1-block tile;
+//     P = 2^(z - M_h) -> bf16 -> smem (MN-major, no swizzle)
+//   O^T[128 d x 16 heads] += V_tile^T (MN-major, 128-B swizzle) . P^T (TMEM)
+//
+// Every K/V byte feeds only the 16 heads of its group, so the kernel is bound
+// by the gather bandwidth (L2 -> SMEM), not by the tensor pipe:
+// three 64 KB K/V stages keep ~128 KB in flight per SM.  The running max M_h
+// is the exact max of the first tile (which always holds the forced init
+// block); later tiles only trigger a rescale of O (TMEM ld/scale/st) when a
+// score exceeds M_h + 8 (log2 units), so P stays <= 256 and the rescale is rare.
+//
+// Warp roles (10 warps): 0 = TMA producer, 1 = TMEM alloc + MMA issuer,
+// 2..5 = softmax (128 threads = tile rows), 6..9 = epilogue (thread = d lane
+// of O^T: normalise, store bf16/f32 output and the natural-log LSE).
+#include <float.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tc_dispatch.cuh"
+
+namespace infllm2 {
+
+bool tc_kernels_enabled();
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kG = 16;
+constexpr int kD = 128;
+constexpr int kM = 64;                 // block size
+constexpr int kRowsT = 128;            // rows per tile (two blocks)
+constexpr int kStages = 3;
+constexpr int kThreads = 320;
+constexpr int kMaxSel = 80;
+
+constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
+constexpr uint32_t kTileBytes = 2 * kHalfBytes;         // 32 KB per K or V tile
+constexpr uint32_t kStageBytes = 2 * kTileBytes;        // K + V = 64 KB
+constexpr uint32_t kQBytes = 2 * kG * 128;              // 4 KB (two 64-d halves of 16 rows)
+constexpr uint32_t kPBytes = kRowsT * kG * 2;           // 4 KB
+
+struct Smem {
+  static constexpr uint32_t kv = 0;
+  static constexpr uint32_t q = kv + kStages * kStageBytes;     // 2 buffers
+  static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
+  static constexpr uint32_t stats = p + 2 * kPBytes;            // [2][4 warps][16] l + [2][16] M
+  static constexpr uint32_t red = stats + 2 * 5 * 16 * 4;       // [4 warps][16] reduction scratch
+  static constexpr uint32_t bars = red + 4 * 16 * 4;
+  static constexpr uint32_t total = bars + 32 * 8;
+};
+
+struct Params {
+  int64_t n, start;
+  int hq, hkv, max_sel, out_f32;
+  const int32_t* sel;
+  void* out;
+  float* lse;
+};
+
+__device__ __forceinline__ int item_blocks(const Params& p, int64_t item, int64_t pos, const int32_t*& s) {
+  s = p.sel + item * p.max_sel;
+  int nb = 0;
+  while (nb < p.max_sel && s[nb] >= 0 && (int64_t)s[nb] * kM <= pos) ++nb;
+  return nb;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                 const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
+  uint64_t* kv_full = bars;               // [3]
+  uint64_t* kv_empty = bars + 3;          // [3]
+  uint64_t* q_full = bars + 6;            // [2]
+  uint64_t* q_empty = bars + 8;           // [2]
+  uint64_t* s_full = bars + 10;           // [2]
+  uint64_t* s_empty = bars + 12;          // [2]
+  uint64_t* p_full = bars + 14;           // [2]
+  uint64_t* p_empty = bars + 16;          // [2]
+  uint64_t* o_full = bars + 18;           // [2]
+  uint64_t* o_empty = bars + 20;          // [2]
+  uint64_t* st_full = bars + 22;          // [2]
+  uint64_t* st_empty = bars + 24;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  float* stats = reinterpret_cast<float*>(smem + Smem::stats);
+  float* red = reinterpret_cast<float*>(smem + Smem::red);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 4);
+      mbar_init(p_full + i, 4);
+      mbar_init(p_empty + i, 1);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_empty + i, 4);
+      mbar_init(st_full + i, 4);
+      mbar_init(st_empty + i, 4);
+    }
+    fence_barrier_init();
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+  }
+  if (warp == 1) tmem_alloc<64>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;       // cols [0,32): S slots, [32,64): O slots
+  const int64_t items = p.n * p.hkv;
+
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int64_t i = item / p.hkv;
+        const int grp = (int)(item - i * p.hkv);
+        const int64_t pos = p.start + i;
+        const int32_t* s;
+        const int nb = item_blocks(p, item, pos, s);
+        const int qb = it & 1;
+        mbar_wait(q_empty + qb, ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full + qb, kQBytes);
+        uint8_t* qd = smem + Smem::q + qb * kQBytes;
+        tma_load_3d(qd, &tm_q, q_full + qb, 0, grp * kG, (int)i);
+        tma_load_3d(qd + kQBytes / 2, &tm_q, q_full + qb, 64, grp * kG, (int)i);
+        for (int c = 0; c * 2 < nb; ++c) {
+          const int nt = (nb - 2 * c) >= 2 ? 2 : 1;
+          mbar_wait(kv_empty + stage, phase ^ 1);
+          mbar_arrive_expect_tx(kv_full + stage, nt * 4 * (kM * 128));
+          uint8_t* kd = smem + Smem::kv + stage * kStageBytes;
+          uint8_t* vd = kd + kTileBytes;
+          for (int x = 0; x < nt; ++x) {
+            const int row0 = s[2 * c + x] * kM;
+            const uint32_t off = x * kM * 128;
+            tma_load_3d(kd + off, &tm_k, kv_full + stage, 0, row0, grp);
+            tma_load_3d(kd + kHalfBytes + off, &tm_k, kv_full + stage, 64, row0, grp);
+            tma_load_3d(vd + off, &tm_v, kv_full + stage, 0, row0, grp);
+            tma_load_3d(vd + kHalfBytes + off, &tm_v, kv_full + stage, 64, row0, grp);
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- MMA issuer
+    const uint32_t idesc_qk = idesc_bf16_f32(128, kG);
+    const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    int sslot = 0, pbuf = 0;
+    uint32_t s_ph[2] = {0, 0}, p_ph[2] = {0, 0};
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int64_t i = item / p.hkv;
+      const int64_t pos = p.start + i;
+      const int32_t* s;
+      const int nb = item_blocks(p, item, pos, s);
+      const int tiles = (nb + 1) / 2;
+      const int qb = it & 1, ob = it & 1;
+      mbar_wait(q_full + qb, (it >> 1) & 1);
+      const uint32_t q_addr = smem_u32(smem + Smem::q + qb * kQBytes);
+      int stage_c = stage;
+      uint32_t phase_c = phase;
+      auto issue_qk = [&](int st, int slot) {
+        const uint32_t k_addr = smem_u32(smem + Smem::kv + st * kStageBytes);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
+            const uint32_t qoff = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+            umma_f16_ss(tmem + slot * kG, sdesc_k_sw128(k_addr + off), sdesc_k_sw128(q_addr + qoff), idesc_qk,
+                        k > 0 ? 1u : 0u);
+          }
+          umma_commit(s_full + slot);
+        }
+        __syncwarp();
+      };
+      // prologue: QK of tile 0
+      mbar_wait(kv_full + stage_c, phase_c);
+      mbar_wait(s_empty + sslot, s_ph[sslot] ^ 1);
+      s_ph[sslot] ^= 1;
+      issue_qk(stage_c, sslot);
+      for (int c = 0; c < tiles; ++c) {
+        const int cur_stage = stage_c, cur_slot = sslot;
+        if (++stage_c == kStages) { stage_c = 0; phase_c ^= 1; }
+        sslot ^= 1;
+        if (c + 1 < tiles) {
+          mbar_wait(kv_full + stage_c, phase_c);
+          mbar_wait(s_empty + sslot, s_ph[sslot] ^ 1);
+          s_ph[sslot] ^= 1;
+          issue_qk(stage_c, sslot);
+        }
+        if (c == tiles - 1) {
+          if (elect_one()) umma_commit(q_empty + qb);
+          __syncwarp();
+        }
+        // PV of tile c once its P is in shared memory
+        mbar_wait(p_full + pbuf, p_ph[pbuf]);
+        p_ph[pbuf] ^= 1;
+        if (c == 0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
+        if (elect_one()) {
+          const uint32_t v_addr = smem_u32(smem + Smem::kv + cur_stage * kStageBytes + kTileBytes);
+          const uint32_t p_addr = smem_u32(smem + Smem::p + pbuf * kPBytes);
+          for (int k = 0; k < ksteps; ++k) {
+            umma_f16_ss(tmem + 32 + ob * kG, sdesc_mn_sw128(v_addr + k * 2048, kHalfBytes, 1024),
+                        sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv, (c > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(kv_empty + cur_stage);
+          umma_commit(p_empty + pbuf);
+          if (c == tiles - 1) umma_commit(o_full + ob);
+        }
+        __syncwarp();
+        pbuf ^= 1;
+        (void)cur_slot;
+      }
+      stage = stage_c;
+      phase = phase_c;
+    }
+  } else if (warp < 6) {
+    // -------------------------------------------------------------- softmax
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;                  // tile row == TMEM lane
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const float c2 = 1.4426950408889634f / sqrtf((float)kD);
+    int sslot = 0, pbuf = 0;
+    uint32_t s_ph[2] = {0, 0}, p_ph[2] = {0, 0};
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int64_t i = item / p.hkv;
+      const int64_t pos = p.start + i;
+      const int32_t* s;
+      const int nb = item_blocks(p, item, pos, s);
+      const int tiles = (nb + 1) / 2;
+      const int ob = it & 1;
+      float mrun[kG], lsum[kG];
+#pragma unroll
+      for (int h = 0; h < kG; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; }
+      for (int c = 0; c < tiles; ++c) {
+        mbar_wait(s_full + sslot, s_ph[sslot]);
+        s_ph[sslot] ^= 1;
+        tc_fence_after();
+        float z[kG];
+        tmem_ld16(tmem + lane_base + sslot * kG, z);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + sslot);
+        sslot ^= 1;
+        const int x = row >> 6;
+        bool valid = (2 * c + x) < nb;
+        if (valid) valid = (int64_t)s[2 * c + x] * kM + (row & 63) <= pos;
+#pragma unroll
+        for (int h = 0; h < kG; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
+        // running max: exact on the first tile, rescale later only if z > M + 8
+        bool need = (c == 0);
+        if (c > 0) {
+          bool over = false;
+#pragma unroll
+          for (int h = 0; h < kG; ++h) over |= z[h] > mrun[h] + 8.f;
+          const unsigned any = __ballot_sync(0xffffffffu, over);
+          if (lane == 0) red[quad * 16] = any ? 1.f : 0.f;
+          named_bar_sync(2, 128);
+          need = (red[0] + red[16] + red[32] + red[48]) > 0.f;
+          named_bar_sync(2, 128);
+        }
+        if (need) {
+          float tmax[kG];
+#pragma unroll
+          for (int h = 0; h < kG; ++h) {
+            float v = z[h];
+            for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+            tmax[h] = v;
+          }
+          if (lane < kG) {
+            float mine = tmax[0];
+#pragma unroll
+            for (int h = 1; h < kG; ++h) mine = (lane == h) ? tmax[h] : mine;
+            red[quad * 16 + lane] = mine;
+          }
+          named_bar_sync(2, 128);
+          float corr[kG];
+          bool any_corr = false;
+#pragma unroll
+          for (int h = 0; h < kG; ++h) {
+            const float tm = fmaxf(fmaxf(red[h], red[16 + h]), fmaxf(red[32 + h], red[48 + h]));
+            const float mnew = fmaxf(mrun[h], tm);
+            corr[h] = (mrun[h] == -INFINITY) ? 1.f : ex2(mrun[h] - mnew);
+            any_corr |= (c > 0) && (corr[h] != 1.f);
+            lsum[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
+            mrun[h] = mnew;
+          }
+          named_bar_sync(2, 128);
+          if (c > 0 && any_corr) {
+            // rescale O^T (this thread owns d lane == row): wait for PV(c-1),
+            // whose completion is the next phase of p_empty[buffer of c-1]
+            mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
+            tc_fence_after();
+            float o[kG];
+            tmem_ld16(tmem + lane_base + 32 + ob * kG, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int h = 0; h < kG; ++h) o[h] *= corr[h];
+            tmem_st16(tmem + lane_base + 32 + ob * kG, o);
+            tmem_wait_st();
+            tc_fence_before();
+          }
+        }
+        // P = 2^(z - M) as bf16 into the MN-major interleaved buffer
+        mbar_wait(p_empty + pbuf, p_ph[pbuf] ^ 1);
+        p_ph[pbuf] ^= 1;
+        uint32_t packed[kG / 2];
+#pragma unroll
+        for (int h = 0; h < kG; h += 2) {
+          const float a = ex2(z[h] - mrun[h]);
+          const float b = ex2(z[h + 1] - mrun[h + 1]);
+          const __nv_bfloat162 pr = __floats2bfloat162_rn(a, b);
+          lsum[h] += __low2float(pr);
+          lsum[h + 1] += __high2float(pr);
+          packed[h / 2] = *reinterpret_cast<const uint32_t*>(&pr);
+        }
+        uint8_t* pb = smem + Smem::p + pbuf * kPBytes;
+        const uint32_t base = (row >> 3) * 256 + (row & 7) * 16;
+        *reinterpret_cast<uint4*>(pb + base) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        *reinterpret_cast<uint4*>(pb + base + 128) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full + pbuf);
+        pbuf ^= 1;
+      }
+      // per-head row sums -> stats for the epilogue
+      mbar_wait(st_empty + ob, ((it >> 1) & 1) ^ 1);
+      float* st = stats + ob * 5 * 16;
+#pragma unroll
+      for (int h = 0; h < kG; ++h) {
+        float v = lsum[h];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) st[quad * 16 + h] = v;
+      }
+      if (quad == 0 && lane < kG) {
+        float mine = mrun[0];
+#pragma unroll
+        for (int h = 1; h < kG; ++h) mine = (lane == h) ? mrun[h] : mine;
+        st[64 + lane] = mine;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(st_full + ob);
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int quad = warp & 3;
+    const int d = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int64_t i = item / p.hkv;
+      const int grp = (int)(item - i * p.hkv);
+      const int ob = it & 1;
+      const uint32_t par = (it >> 1) & 1;
+      mbar_wait(o_full + ob, par);
+      mbar_wait(st_full + ob, par);
+      tc_fence_after();
+      float o[kG];
+      tmem_ld16(tmem + lane_base + 32 + ob * kG, o);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty + ob);
+      const float* st = stats + ob * 5 * 16;
+      float l[kG];
+#pragma unroll
+      for (int h = 0; h < kG; ++h) l[h] = st[h] + st[16 + h] + st[32 + h] + st[48 + h];
+      const int64_t obase = (i * p.hq + (int64_t)grp * kG) * kD + d;
+      if (p.out_f32) {
+        float* out = static_cast<float*>(p.out);
+#pragma unroll
+        for (int h = 0; h < kG; ++h) out[obase + h * kD] = o[h] / l[h];
+      } else {
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+#pragma unroll
+        for (int h = 0; h < kG; ++h) out[obase + h * kD] = __float2bfloat16_rn(o[h] / l[h]);
+      }
+      if (p.lse && quad == 0 && lane < kG) {
+        float lh = l[0];
+#pragma unroll
+        for (int h = 1; h < kG; ++h) lh = (lane == h) ? l[h] : lh;
+        p.lse[i * p.hq + grp * kG + lane] = (st[64 + lane] + log2f(lh)) * 0.6931471805599453f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(st_empty + ob);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<64>(tmem);
+}
+
+}  // namespace
+
+bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
+  if (!tc_kernels_enabled()) return false;
+  if (cs.group != kG || cs.d != kD || g.block_size != kM) return false;
+  if (cs.max_sel > kMaxSel) return false;
+  return cs.n > 0;
+}
+
+cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q, int64_t q_row_stride,
+                             const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
+                             void* out, int out_f32, float* lse, cudaStream_t stream) {
+  Params p;
+  p.n = cs.n;
+  p.start = cs.start;
+  p.hq = cs.hq;
+  p.hkv = cs.hkv;
+  p.max_sel = cs.max_sel;
+  p.out_f32 = out_f32;
+  p.sel = selection;
+  p.out = out;
+  p.lse = lse;
+  CUtensorMap tq, tk, tv;
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)cs.n};
+    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)q_row_stride * 2};
+    const uint32_t box[3] = {64, (uint32_t)kG, 1};
+    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.cache_len, (uint64_t)cs.hkv};
+    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)cap * kD * 2};
+    const uint32_t box[3] = {64, (uint32_t)kM, 1};
+    if (!encode_tmap_3d_bf16(&tk, k_cache, dims, strides, box)) return cudaErrorInvalidValue;
+    if (!encode_tmap_3d_bf16(&tv, v_cache, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  const size_t smem = Smem::total + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = cs.n * cs.hkv;
+  const int grid = (int)(items < sms ? items : sms);
+  count_launch();
+  attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace infllm2

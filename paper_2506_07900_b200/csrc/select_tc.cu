@@ -517,11 +517,4 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
   return cudaGetLastError();
 }
 
-// Stage-2 tensor-core kernel not yet wired: every attend call uses the CUDA-core kernel.
-bool tc_attend_supported(const infllm2_geometry&, const CallShape&) { return false; }
-cudaError_t launch_attend_tc(const infllm2_geometry&, const CallShape&, const void*, int64_t, const void*,
-                             const void*, int64_t, const int32_t*, void*, int, float*, cudaStream_t) {
-  return cudaErrorNotSupported;
-}
-
 }  // namespace infllm2
