@@ -47,7 +47,8 @@ constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 
 constexpr uint32_t kTileBytes = 2 * kHalfBytes;         // 32 KB per K or V tile
 constexpr uint32_t kStageBytes = 2 * kTileBytes;        // K + V = 64 KB
 constexpr uint32_t kQBytes = 2 * kG * 128;              // 4 KB (two 64-d halves of 16 rows)
-constexpr uint32_t kPBytes = kRowsT * kG * 2;           // 4 KB
+constexpr uint32_t kPBytes = 2 * kRowsT * kG * 2;       // 8 KB: P_hi and P_lo (bf16 each)
+constexpr uint32_t kPHalf = kRowsT * kG * 2;            // 4 KB
 
 struct Smem {
   static constexpr uint32_t kv = 0;
@@ -222,8 +223,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           const uint32_t v_addr = smem_u32(smem + Smem::kv + cur_stage * kStageBytes + kTileBytes);
           const uint32_t p_addr = smem_u32(smem + Smem::p + pbuf * kPBytes);
           for (int k = 0; k < ksteps; ++k) {
-            umma_f16_ss(tmem + 32 + ob * kG, sdesc_mn_sw128(v_addr + k * 2048, kHalfBytes, 1024),
-                        sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv, (c > 0 || k > 0) ? 1u : 0u);
+            const uint64_t vdesc = sdesc_mn_sw128(v_addr + k * 2048, kHalfBytes, 1024);
+            umma_f16_ss(tmem + 32 + ob * kG, vdesc, sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv,
+                        (c > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ss(tmem + 32 + ob * kG, vdesc, sdesc_interleave(p_addr + kPHalf + k * 512, 256, 128),
+                        idesc_pv, 1u);
           }
           umma_commit(kv_empty + cur_stage);
           umma_commit(p_empty + pbuf);
@@ -328,20 +332,26 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         // P = 2^(z - M) as bf16 into the MN-major interleaved buffer
         mbar_wait(p_empty + pbuf, p_ph[pbuf] ^ 1);
         p_ph[pbuf] ^= 1;
-        uint32_t packed[kG / 2];
+        // P split into bf16 hi + lo (two PV MMAs): ~16-bit P, so the output
+        // is not limited by bf16 rounding of the softmax weights.
+        uint32_t phi[kG / 2], plo[kG / 2];
 #pragma unroll
         for (int h = 0; h < kG; h += 2) {
           const float a = ex2(z[h] - mrun[h]);
           const float b = ex2(z[h + 1] - mrun[h + 1]);
-          const __nv_bfloat162 pr = __floats2bfloat162_rn(a, b);
-          lsum[h] += __low2float(pr);
-          lsum[h + 1] += __high2float(pr);
-          packed[h / 2] = *reinterpret_cast<const uint32_t*>(&pr);
+          lsum[h] += a;
+          lsum[h + 1] += b;
+          const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
+          const __nv_bfloat162 lo2 = __floats2bfloat162_rn(a - __low2float(hi2), b - __high2float(hi2));
+          phi[h / 2] = *reinterpret_cast<const uint32_t*>(&hi2);
+          plo[h / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
         }
         uint8_t* pb = smem + Smem::p + pbuf * kPBytes;
         const uint32_t base = (row >> 3) * 256 + (row & 7) * 16;
-        *reinterpret_cast<uint4*>(pb + base) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        *reinterpret_cast<uint4*>(pb + base + 128) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
+        *reinterpret_cast<uint4*>(pb + base + 128) = make_uint4(phi[4], phi[5], phi[6], phi[7]);
+        *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
+        *reinterpret_cast<uint4*>(pb + kPHalf + base + 128) = make_uint4(plo[4], plo[5], plo[6], plo[7]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + pbuf);
