@@ -68,11 +68,27 @@ struct Params {
   float* lse;
 };
 
-__device__ __forceinline__ int item_blocks(const Params& p, int64_t item, int64_t pos, const int32_t*& s) {
-  s = p.sel + item * p.max_sel;
-  int nb = 0;
-  while (nb < p.max_sel && s[nb] >= 0 && (int64_t)s[nb] * kM <= pos) ++nb;
-  return nb;
+// The item's selection row, read once per warp with lane-parallel loads
+// (entries lane, lane+32, lane+64); nb = blocks that start at or before pos.
+struct SelRow {
+  int r0, r1, r2;
+  int nb;
+  __device__ __forceinline__ int get(int j) const {
+    const int v = j < 32 ? r0 : (j < 64 ? r1 : r2);
+    return __shfl_sync(0xffffffffu, v, j & 31);
+  }
+};
+
+__device__ __forceinline__ SelRow load_sel(const Params& p, int64_t item, int64_t pos, int lane) {
+  const int32_t* s = p.sel + item * p.max_sel;
+  SelRow r;
+  r.r0 = lane < p.max_sel ? s[lane] : -1;
+  r.r1 = lane + 32 < p.max_sel ? s[lane + 32] : -1;
+  r.r2 = lane + 64 < p.max_sel ? s[lane + 64] : -1;
+  auto ok = [&](int b) { return b >= 0 && (int64_t)b * kM <= pos; };
+  r.nb = __popc(__ballot_sync(0xffffffffu, ok(r.r0))) + __popc(__ballot_sync(0xffffffffu, ok(r.r1))) +
+         __popc(__ballot_sync(0xffffffffu, ok(r.r2)));
+  return r;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -126,38 +142,43 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
-    if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        const int64_t i = item / p.hkv;
-        const int grp = (int)(item - i * p.hkv);
-        const int64_t pos = p.start + i;
-        const int32_t* s;
-        const int nb = item_blocks(p, item, pos, s);
-        const int qb = it & 1;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int64_t i = item / p.hkv;
+      const int grp = (int)(item - i * p.hkv);
+      const int64_t pos = p.start + i;
+      const SelRow sr = load_sel(p, item, pos, lane);
+      const int nb = sr.nb;
+      const int qb = it & 1;
+      if (lane == 0) {
         mbar_wait(q_empty + qb, ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(q_full + qb, kQBytes);
         uint8_t* qd = smem + Smem::q + qb * kQBytes;
         tma_load_3d(qd, &tm_q, q_full + qb, 0, grp * kG, (int)i);
         tma_load_3d(qd + kQBytes / 2, &tm_q, q_full + qb, 64, grp * kG, (int)i);
-        for (int c = 0; c * 2 < nb; ++c) {
-          const int nt = (nb - 2 * c) >= 2 ? 2 : 1;
+      }
+      for (int c = 0; c * 2 < nb; ++c) {
+        const int nt = (nb - 2 * c) >= 2 ? 2 : 1;
+        const int b0 = sr.get(2 * c);
+        const int b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
+        if (lane == 0) {
           mbar_wait(kv_empty + stage, phase ^ 1);
           mbar_arrive_expect_tx(kv_full + stage, nt * 4 * (kM * 128));
           uint8_t* kd = smem + Smem::kv + stage * kStageBytes;
           uint8_t* vd = kd + kTileBytes;
           for (int x = 0; x < nt; ++x) {
-            const int row0 = s[2 * c + x] * kM;
+            const int row0 = (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
             tma_load_3d(kd + off, &tm_k, kv_full + stage, 0, row0, grp);
             tma_load_3d(kd + kHalfBytes + off, &tm_k, kv_full + stage, 64, row0, grp);
             tma_load_3d(vd + off, &tm_v, kv_full + stage, 0, row0, grp);
             tma_load_3d(vd + kHalfBytes + off, &tm_v, kv_full + stage, 64, row0, grp);
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -172,8 +193,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int64_t i = item / p.hkv;
       const int64_t pos = p.start + i;
-      const int32_t* s;
-      const int nb = item_blocks(p, item, pos, s);
+      const SelRow sr = load_sel(p, item, pos, lane);
+      const int nb = sr.nb;
       const int tiles = (nb + 1) / 2;
       const int qb = it & 1, ob = it & 1;
       mbar_wait(q_full + qb, (it >> 1) & 1);
@@ -252,8 +273,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int64_t i = item / p.hkv;
       const int64_t pos = p.start + i;
-      const int32_t* s;
-      const int nb = item_blocks(p, item, pos, s);
+      const SelRow sr = load_sel(p, item, pos, lane);
+      const int nb = sr.nb;
       const int tiles = (nb + 1) / 2;
       const int ob = it & 1;
       float mrun[kG], lsum[kG];
@@ -271,8 +292,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (lane == 0) mbar_arrive(s_empty + sslot);
         sslot ^= 1;
         const int x = row >> 6;
+        const int b0 = sr.get(2 * c), b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         bool valid = (2 * c + x) < nb;
-        if (valid) valid = (int64_t)s[2 * c + x] * kM + (row & 63) <= pos;
+        if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
 #pragma unroll
         for (int h = 0; h < kG; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
         // running max: exact on the first tile, rescale later only if z > M + 8

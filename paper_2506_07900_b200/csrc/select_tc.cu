@@ -240,7 +240,9 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int64_t qb = t0 / p.m;
       const int64_t n_cand = qb + 1;
 
-      // ---- pass 1: row LSE (log2 domain)
+      // ---- pass 1: row LSE (log2 domain).  Two 32-column TMEM loads per
+      // wait, max on the raw accumulator (zscale > 0), FFMA+ex2 with four
+      // independent partial sums; masking only on the tail tile.
       {
         const int row = half * 128 + quad * 32 + lane;
         float mrun = -INFINITY, srun = 0.f;
@@ -249,24 +251,29 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           acc_phase[buf] ^= 1;
           tc_fence_after();
           const int64_t jbase = (int64_t)c * kNT;
+          const bool tail = jbase + kNT > nk;
 #pragma unroll 1
-          for (int ch = 0; ch < 4; ++ch) {
-            float v[32];
-            tmem_ld32(tmem + lane_base + buf * 256 + half * 128 + ch * 32, v);
+          for (int ch = 0; ch < 4; ch += 2) {
+            float v[64];
+            tmem_ld32(tmem + lane_base + buf * 256 + half * 128 + ch * 32, *reinterpret_cast<float(*)[32]>(v));
+            tmem_ld32(tmem + lane_base + buf * 256 + half * 128 + ch * 32 + 32,
+                      *reinterpret_cast<float(*)[32]>(v + 32));
             tmem_wait_ld();
-            const int64_t j0 = jbase + ch * 32;
-            float cmax = -INFINITY;
+            if (tail) {
+              const int64_t j0 = jbase + ch * 32;
 #pragma unroll
-            for (int x = 0; x < 32; ++x) {
-              v[x] = (j0 + x < nk) ? v[x] * p.zscale : -INFINITY;
-              cmax = fmaxf(cmax, v[x]);
+              for (int x = 0; x < 64; ++x) v[x] = (j0 + x < nk) ? v[x] : -INFINITY;
             }
+            float m4[4] = {v[0], v[1], v[2], v[3]};
+#pragma unroll
+            for (int x = 4; x < 64; ++x) m4[x & 3] = fmaxf(m4[x & 3], v[x]);
+            const float cmax = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * p.zscale;
             const float mnew = fmaxf(mrun, cmax);
             if (mnew != -INFINITY) {
-              float acc = 0.f;
+              float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-              for (int x = 0; x < 32; ++x) acc += ex2(v[x] - mnew);
-              srun = srun * ex2(mrun - mnew) + acc;
+              for (int x = 0; x < 64; ++x) a4[x & 3] += ex2(fmaf(v[x], p.zscale, -mnew));
+              srun = srun * ex2(mrun - mnew) + ((a4[0] + a4[1]) + (a4[2] + a4[3]));
               mrun = mnew;
             }
           }
@@ -288,16 +295,24 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int jl = quad * 32 + lane;
         const bool live = (int64_t)c * kNT + jl < nk;
 #pragma unroll 1
-        for (int qq = 0; qq < 8; ++qq) {
-          const int qi = half * 8 + qq;
-          float v[16];
-          tmem_ld16(tmem + lane_base + buf * 256 + qi * 16, v);
+        for (int qq = 0; qq < 8; qq += 4) {
+          float v[64];
+          const uint32_t col = tmem + lane_base + buf * 256 + (half * 8 + qq) * 16;
+          tmem_ld32(col, *reinterpret_cast<float(*)[32]>(v));
+          tmem_ld32(col + 32, *reinterpret_cast<float(*)[32]>(v + 32));
           tmem_wait_ld();
-          const float* l2 = lse2 + qi * kG;
-          float sacc = 0.f;
 #pragma unroll
-          for (int h = 0; h < kG; ++h) sacc += ex2(v[h] * p.zscale - l2[h]);
-          stile[qi * kSTileLd + 1 + jl] = live ? sacc * (1.0f / kG) : -INFINITY;
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int qi = half * 8 + qq + u4;
+            const float* l2 = lse2 + qi * kG;
+            float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+            for (int h = 0; h < kG; h += 2) {
+              a0 += ex2(fmaf(v[u4 * 16 + h], p.zscale, -l2[h]));
+              a1 += ex2(fmaf(v[u4 * 16 + h + 1], p.zscale, -l2[h + 1]));
+            }
+            stile[qi * kSTileLd + 1 + jl] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
+          }
         }
         tc_fence_before();
         __syncwarp();
