@@ -27,6 +27,7 @@
 // two 256-column accumulator buffers, so the epilogue of tile c overlaps the
 // MMAs of tile c+1.  Shared memory: Q 64 KB + 2 stages x 64 KB of mu.
 #include <float.h>
+#include <limits.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -46,8 +47,11 @@ constexpr int kD = 128;
 constexpr int kNT = 128;          // kernels per tile
 constexpr int kStages = 2;
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 32 * (2 + kEpiWarps);
+constexpr int kTopkWarps = 2;     // dedicated selection warps (8 queries each)
+constexpr int kThreads = 32 * (2 + kEpiWarps + kTopkWarps);
 constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kListCap = 256;     // per-warp threshold-compaction list
+constexpr int kOutCap = 96;
 
 constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
 constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 128 B)
@@ -60,8 +64,9 @@ struct SmemLayout {
   static constexpr uint32_t stile = mu + kStages * kMuStageBytes;          // float [kQ][kSTileLd]
   static constexpr uint32_t lse2 = stile + kQ * kSTileLd * 4;              // float [kRows]
   static constexpr uint32_t bars = lse2 + kRows * 4;                       // uint64 [..]
-  static constexpr uint32_t topk = bars + 16 * 8;                          // per warp lists
-  static constexpr uint32_t total = topk + kEpiWarps * 2 * 80 * 12 + 16;
+  static constexpr uint32_t topk = bars + 24 * 8;                          // per top-k warp lists
+  static constexpr uint32_t topk_per_warp = kListCap * 8;
+  static constexpr uint32_t total = topk + kTopkWarps * topk_per_warp + 16;
 };
 
 struct Params {
@@ -73,7 +78,7 @@ struct Params {
   int64_t first_t0;               // aligned position of unit 0
   int32_t* selection;
   double* sel_scores;
-  float* rbuf;                    // [grid][kQ][nb_cap]
+  float* rbuf;                    // [grid][2][kQ][nb_cap]  block scores, double-buffered per unit
   int64_t nb_cap;
   float zscale;                   // log2(e)/sqrt(D)
 };
@@ -101,6 +106,168 @@ __device__ __forceinline__ bool better(float ra, int ba, float rb, int bb) {
   return ra > rb || (ra == rb && ba < bb);   // (score desc, id asc), sparse.py:273
 }
 
+// Forced set / budget of a unit (all 16 rows share it): force_blocks
+// (sparse.py:218-227) and the budget rule of select_topk (sparse.py:268).
+struct UnitSel {
+  int64_t qb, n_cand, n_init, local_lo, budget, n_free;
+};
+__device__ __forceinline__ UnitSel unit_sel(const Params& p, int64_t t0) {
+  UnitSel u;
+  u.qb = t0 / p.m;
+  u.n_cand = u.qb + 1;
+  u.n_init = p.n_init < u.n_cand ? p.n_init : u.n_cand;
+  u.local_lo = u.qb + 1;
+  if (p.n_local > 0) {
+    u.local_lo = u.qb - p.n_local + 1;
+    if (u.local_lo < 0) u.local_lo = 0;
+    if (u.local_lo < u.n_init) u.local_lo = u.n_init;
+  }
+  const int64_t n_forced = u.n_init + (u.qb + 1 - u.local_lo);
+  u.budget = p.top_k;
+  if (p.consume) u.budget = p.top_k - n_forced > 0 ? p.top_k - n_forced : 0;
+  u.n_free = u.n_cand - n_forced;
+  return u;
+}
+
+// Warp bitonic sort of one value per lane: descending floats / ascending ints.
+__device__ __forceinline__ float warp_sort_desc(float x, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const float y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool keep_max = (((lane & k) == 0) == ((lane & j) == 0));
+      x = keep_max ? fmaxf(x, y) : fminf(x, y);
+    }
+  return x;
+}
+__device__ __forceinline__ int warp_sort_asc(int x, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool keep_min = (((lane & k) == 0) == ((lane & j) == 0));
+      x = keep_min ? min(x, y) : max(x, y);
+    }
+  return x;
+}
+
+// Warp argmax over (score desc, id asc) strictly after (prev_v, prev_b) in that order.
+__device__ __forceinline__ void warp_best_after(float& bv, int& bb) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
+    if (ob >= 0 && (bb < 0 || better(ov, ob, bv, bb))) { bv = ov; bb = ob; }
+  }
+}
+
+// One query's selection by one warp: forced init blocks, the `budget` best
+// candidates of rq[n_init, local_lo) by (score desc, id asc), forced local
+// blocks; written ascending with -1 padding (select_topk, sparse.py:247-277).
+// Fast path (budget <= 32): threshold T0 = budget-th largest lane maximum
+// (at least `budget` candidates reach it, so the answer lies in {r >= T0}),
+// compact that set in id order, pick `budget` from it, bitonic-sort the ids.
+__device__ void warp_select(const float* rq, const UnitSel& u, int lane, float* lkey, int* lid, int32_t* out,
+                            double* osc, int max_sel) {
+  const int lo = (int)u.n_init, hi = (int)u.local_lo;
+  const int budget = (int)u.budget;
+  int chosen = INT_MAX;          // lane x < budget holds the x-th chosen id
+  if (budget >= u.n_free) {
+    // dense regime: every candidate is selected (assembled below)
+  } else if (budget > 0 && budget <= 32) {
+    float m = -1.f;
+    for (int b = lo + lane; b < hi; b += 32) m = fmaxf(m, rq[b]);
+    const float t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m, lane), budget - 1);
+    int cnt = 0;
+    bool overflow = false;
+    for (int base = lo; base < hi; base += 32) {
+      const int b = base + lane;
+      const float r = b < hi ? rq[b] : -2.f;
+      const bool f = r >= t0;
+      const unsigned mask = __ballot_sync(0xffffffffu, f);
+      const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
+      if (f && pos < kListCap) { lkey[pos] = r; lid[pos] = b; }
+      cnt += __popc(mask);
+    }
+    overflow = cnt > kListCap;
+    __syncwarp();
+    float pv = INFINITY;
+    int pb = -1;
+    for (int it = 0; it < budget; ++it) {
+      float bv = -1.f;
+      int bb = -1;
+      if (!overflow) {
+        for (int x = lane; x < cnt; x += 32) {
+          const float r = lkey[x];
+          const int b = lid[x];
+          if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
+        }
+      } else {
+        for (int b = lo + lane; b < hi; b += 32) {
+          const float r = rq[b];
+          if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
+        }
+      }
+      warp_best_after(bv, bb);
+      if (lane == it) chosen = bb;
+      pv = bv;
+      pb = bb;
+    }
+    chosen = warp_sort_asc(chosen, lane);
+  } else if (budget > 32) {
+    // rare large budgets: iterative order-statistics over the whole range
+    float pv = INFINITY;
+    int pb = -1;
+    for (int it = 0; it < budget; ++it) {
+      float bv = -1.f;
+      int bb = -1;
+      for (int b = lo + lane; b < hi; b += 32) {
+        const float r = rq[b];
+        if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
+      }
+      warp_best_after(bv, bb);
+      if (lane == 0) lid[it] = bb;  // staged in smem, sorted below
+      pv = bv;
+      pb = bb;
+    }
+    __syncwarp();
+    // insertion-free ascending order: ids are distinct, rank = #smaller
+    for (int x = lane; x < budget; x += 32) {
+      const int me = lid[x];
+      int rank = 0;
+      for (int y = 0; y < budget; ++y) rank += lid[y] < me;
+      lkey[rank] = __int_as_float(me);
+    }
+    __syncwarp();
+  }
+  // assemble: [0, lo) + chosen + [local_lo, qb]
+  const int n_ch = budget >= u.n_free ? (int)u.n_free : budget;
+  const int n_loc = (int)(u.qb + 1 - u.local_lo);
+  for (int x = lane; x < max_sel; x += 32) {
+    int id = -1;
+    if (x < lo) id = x;
+    else if (x < lo + n_ch) {
+      const int c = x - lo;
+      if (budget >= u.n_free) id = lo + c;
+      else if (budget <= 32) id = -2;  // filled from registers below
+      else id = __float_as_int(lkey[c]);
+    } else if (x < lo + n_ch + n_loc) id = (int)u.local_lo + (x - lo - n_ch);
+    if (id != -2) {
+      out[x] = id;
+      if (osc) osc[x] = id >= 0 ? (double)rq[id] : 0.0;
+    }
+  }
+  if (budget < u.n_free && budget > 0 && budget <= 32) {
+    // lane c holds the c-th smallest chosen id
+    if (lane < budget) {
+      out[lo + lane] = chosen;
+      if (osc) osc[lo + lane] = (double)rq[chosen];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_hi,
                  const __grid_constant__ CUtensorMap tm_lo, const Params p) {
@@ -117,7 +284,9 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   uint64_t* mu_empty = bars + 2 + kStages;  // [kStages]
   uint64_t* acc_full = bars + 2 + 2 * kStages;       // [2]
   uint64_t* acc_empty = bars + 4 + 2 * kStages;      // [2]
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * kStages);
+  uint64_t* rb_full = bars + 6 + 2 * kStages;        // [2] block scores of a unit ready
+  uint64_t* rb_empty = bars + 8 + 2 * kStages;       // [2] top-k warps done with them
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -125,7 +294,12 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int s = 0; s < kStages; ++s) { mbar_init(mu_full + s, 1); mbar_init(mu_empty + s, 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(acc_full + b, 1); mbar_init(acc_empty + b, kEpiWarps); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, kEpiWarps);
+      mbar_init(rb_full + b, kEpiWarps);
+      mbar_init(rb_empty + b, kTopkWarps);
+    }
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_hi);
@@ -219,7 +393,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         }
       }
     }
-  } else {
+  } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;                 // 0..7
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
@@ -228,10 +402,9 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     const int etid = ew * 32 + lane;         // 0..255
     int buf = 0;
     uint32_t acc_phase[2] = {0, 0};
-    float* rbuf = p.rbuf + (int64_t)blockIdx.x * kQ * p.nb_cap;
-    uint8_t* topk_base = smem + SmemLayout::topk + ew * 2 * 80 * 12;
-
-    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    int ucount = 0;
+    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++ucount) {
+      float* rbuf = p.rbuf + ((int64_t)blockIdx.x * 2 + (ucount & 1)) * kQ * p.nb_cap;
       int64_t t0;
       int grp;
       unit_coords(p, u, &t0, &grp);
@@ -287,6 +460,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       named_bar_sync(1, kEpiThreads);
 
       // ---- pass 2: group scores per kernel, block max
+      mbar_wait(rb_empty + (ucount & 1), ((ucount >> 1) & 1) ^ 1);
       if (etid < kQ) stile[etid * kSTileLd] = -INFINITY;   // carry (kernel -1)
       for (int c = 0; c < tiles; ++c) {
         mbar_wait(acc_full + buf, acc_phase[buf]);
@@ -337,75 +511,34 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         named_bar_sync(1, kEpiThreads);
       }
 
-      // ---- top-k per query (warp ew handles queries ew and ew + 8)
-      const int64_t n_init = p.n_init < n_cand ? p.n_init : n_cand;
-      int64_t local_lo = qb + 1;
-      if (p.n_local > 0) {
-        local_lo = qb - p.n_local + 1;
-        if (local_lo < 0) local_lo = 0;
-        if (local_lo < n_init) local_lo = n_init;
-      }
-      const int64_t n_forced = n_init + (qb + 1 - local_lo);
-      int64_t budget = p.top_k;
-      if (p.consume) budget = p.top_k - n_forced > 0 ? p.top_k - n_forced : 0;
-      const int64_t n_free = n_cand - n_forced;
-      for (int sub = 0; sub < 2; ++sub) {
-        const int qi = ew + sub * 8;
-        const int64_t t = t0 + qi;
-        const int64_t i = t - p.start;
-        if (i < 0 || i >= p.n) continue;    // warp-uniform
-        float* rq = rbuf + (int64_t)qi * p.nb_cap;
-        int* ids = reinterpret_cast<int*>(topk_base + sub * 80 * 12);
-        float* scs = reinterpret_cast<float*>(ids + 80);
-        int cnt = 0;
-        if (lane == 0) {
-          for (int64_t b = 0; b < n_init; ++b) { ids[cnt] = (int)b; scs[cnt] = rq[b]; ++cnt; }
-          for (int64_t b = local_lo; b <= qb; ++b) { ids[cnt] = (int)b; scs[cnt] = rq[b]; ++cnt; }
-          if (budget >= n_free)
-            for (int64_t b = n_init; b < local_lo; ++b) { ids[cnt] = (int)b; scs[cnt] = rq[b]; ++cnt; }
-        }
-        if (budget < n_free) {
-          for (int64_t it = 0; it < budget; ++it) {
-            float bv = -1.f;
-            int bb = -1;
-            for (int64_t b = n_init + lane; b < local_lo; b += 32) {
-              const float r = rq[b];
-              if (r >= 0.f && (bb < 0 || better(r, (int)b, bv, bb))) { bv = r; bb = (int)b; }
-            }
-            for (int off = 16; off > 0; off >>= 1) {
-              const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-              const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
-              if (ob >= 0 && (bb < 0 || better(ov, ob, bv, bb))) { bv = ov; bb = ob; }
-            }
-            if (lane == 0) {
-              ids[cnt] = bb;
-              scs[cnt] = bv;
-              ++cnt;
-              rq[bb] = -1.f;
-            }
-            __syncwarp();
-          }
-        }
-        if (lane == 0) {
-          for (int x = 1; x < cnt; ++x) {
-            const int key = ids[x];
-            const float sv = scs[x];
-            int y = x - 1;
-            while (y >= 0 && ids[y] > key) { ids[y + 1] = ids[y]; scs[y + 1] = scs[y]; --y; }
-            ids[y + 1] = key;
-            scs[y + 1] = sv;
-          }
-          const int64_t item = i * p.hkv + grp;
-          int32_t* out = p.selection + item * p.max_sel;
-          for (int x = 0; x < p.max_sel; ++x) out[x] = x < cnt ? ids[x] : -1;
-          if (p.sel_scores) {
-            double* osc = p.sel_scores + item * p.max_sel;
-            for (int x = 0; x < p.max_sel; ++x) osc[x] = x < cnt ? (double)scs[x] : 0.0;
-          }
-        }
+      // hand the unit's block scores to the top-k warps
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(rb_full + (ucount & 1));
+    }
+  } else {
+    // ------------------------------------------------------------ top-k warps
+    const int tw = warp - 2 - kEpiWarps;     // 0..kTopkWarps-1
+    float* lkey = reinterpret_cast<float*>(smem + SmemLayout::topk + tw * SmemLayout::topk_per_warp);
+    int* lid = reinterpret_cast<int*>(lkey + kListCap);
+    int ucount = 0;
+    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++ucount) {
+      int64_t t0;
+      int grp;
+      unit_coords(p, u, &t0, &grp);
+      const UnitSel us = unit_sel(p, t0);
+      const float* rbuf = p.rbuf + ((int64_t)blockIdx.x * 2 + (ucount & 1)) * kQ * p.nb_cap;
+      mbar_wait(rb_full + (ucount & 1), (ucount >> 1) & 1);
+      for (int qi = tw; qi < kQ; qi += kTopkWarps) {
+        const int64_t i = t0 + qi - p.start;
+        if (i < 0 || i >= p.n) continue;     // warp-uniform
+        const int64_t item = i * p.hkv + grp;
+        warp_select(rbuf + (int64_t)qi * p.nb_cap, us, lane, lkey, lid, p.selection + item * p.max_sel,
+                    p.sel_scores ? p.sel_scores + item * p.max_sel : nullptr, p.max_sel);
         __syncwarp();
       }
-      named_bar_sync(1, kEpiThreads);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(rb_empty + (ucount & 1));
     }
   }
 
@@ -474,7 +607,7 @@ bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool ha
 size_t tc_select_workspace(const infllm2_geometry& g, const CallShape& cs, int) {
   if (cs.group != kG || cs.d != kD) return 0;
   const int64_t nb_cap = cs.cache_len / g.block_size + 2;
-  return (size_t)kNumSMs * kQ * nb_cap * sizeof(float);
+  return (size_t)kNumSMs * 2 * kQ * nb_cap * sizeof(float);
 }
 
 cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
@@ -503,7 +636,7 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.nb_cap = cs.cache_len / g.block_size + 2;
   p.zscale = 1.4426950408889634f / sqrtf((float)kD);
   const int grid = tc_grid(p.n_units);
-  if ((size_t)grid * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
+  if ((size_t)grid * 2 * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
   p.rbuf = static_cast<float*>(ws);
 
   CUtensorMap tq, thi, tlo;

@@ -128,7 +128,7 @@ def test_touch_stats_and_traces_match_reference_counts():
     np.testing.assert_allclose(t["scores_topk"], z["scores_topk"][1500, 1, :len(t["selected"])], rtol=1e-5)
 
 
-@pytest.mark.parametrize("length,topk", [(8192, 16), (6000, 8), (4096, 64)])
+@pytest.mark.parametrize("length,topk", [(8192, 16), (6000, 64), (4096, 8), (5000, 32)])
 def test_random_vs_oracle_sampled_rows(length, topk):
     """Larger caches than the fixtures: GPU vs oracle (f64 dots) on sampled rows."""
     geom = O.Geometry(top_k=topk)
