@@ -47,10 +47,10 @@ constexpr int kD = 128;
 constexpr int kNT = 128;          // kernels per tile
 constexpr int kStages = 2;
 constexpr int kEpiWarps = 8;
-constexpr int kTopkWarps = 2;     // dedicated selection warps (8 queries each)
+constexpr int kTopkWarps = 4;     // dedicated selection warps (4 queries each)
 constexpr int kThreads = 32 * (2 + kEpiWarps + kTopkWarps);
 constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kListCap = 256;     // per-warp threshold-compaction list
+constexpr int kListCap = 352;     // per-warp threshold-compaction list (+ staging tail)
 constexpr int kOutCap = 96;
 
 constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
@@ -188,34 +188,51 @@ __device__ void warp_select(const float* rq, const UnitSel& u, int lane, float* 
       const bool f = r >= t0;
       const unsigned mask = __ballot_sync(0xffffffffu, f);
       const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
-      if (f && pos < kListCap) { lkey[pos] = r; lid[pos] = b; }
+      if (f && pos < kListCap - kOutCap) { lkey[pos] = r; lid[pos] = b; }
       cnt += __popc(mask);
     }
-    overflow = cnt > kListCap;
+    overflow = cnt > kListCap - kOutCap;
     __syncwarp();
-    float pv = INFINITY;
-    int pb = -1;
-    for (int it = 0; it < budget; ++it) {
-      float bv = -1.f;
-      int bb = -1;
-      if (!overflow) {
-        for (int x = lane; x < cnt; x += 32) {
-          const float r = lkey[x];
-          const int b = lid[x];
-          if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
+    if (!overflow) {
+      // rank every listed candidate against the whole list (no dependent
+      // chains), keep rank < budget; the list is in id order, so a ballot
+      // compaction emits the chosen ids already ascending.
+      int taken = 0;
+      for (int base = 0; base < cnt; base += 32) {
+        const int x = base + lane;
+        bool keep = false;
+        if (x < cnt) {
+          const float rk = lkey[x];
+          const int bk = lid[x];
+          int rank = 0;
+          for (int f = 0; f < cnt; ++f) rank += better(lkey[f], lid[f], rk, bk) ? 1 : 0;
+          keep = rank < budget;
         }
-      } else {
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        const int pos = taken + __popc(mask & ((1u << lane) - 1u));
+        if (keep) lid[kListCap - kOutCap + pos] = lid[x];   // staging area at the list tail
+        taken += __popc(mask);
+      }
+      __syncwarp();
+      chosen = lane < budget ? lid[kListCap - kOutCap + lane] : INT_MAX;
+      __syncwarp();
+    } else {
+      float pv = INFINITY;
+      int pb = -1;
+      for (int it = 0; it < budget; ++it) {
+        float bv = -1.f;
+        int bb = -1;
         for (int b = lo + lane; b < hi; b += 32) {
           const float r = rq[b];
           if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
         }
+        warp_best_after(bv, bb);
+        if (lane == it) chosen = bb;
+        pv = bv;
+        pb = bb;
       }
-      warp_best_after(bv, bb);
-      if (lane == it) chosen = bb;
-      pv = bv;
-      pb = bb;
+      chosen = warp_sort_asc(chosen, lane);
     }
-    chosen = warp_sort_asc(chosen, lane);
   } else if (budget > 32) {
     // rare large budgets: iterative order-statistics over the whole range
     float pv = INFINITY;
