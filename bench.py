@@ -105,15 +105,6 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workload
 
 
-def zigzag_chunks(seq: int, world: int, rank: int):
-    """Rank r owns chunks r and 2N-1-r of 2N equal chunks: stage-1 cost grows
-    linearly with position, so the pair sums to the same work on every rank."""
-    nch = 2 * world
-    size = seq // nch
-    bounds = [(c * size, (c + 1) * size if c < nch - 1 else seq) for c in range(nch)]
-    return [bounds[rank], bounds[nch - 1 - rank]]
-
-
 def algorithmic_work(seq: int, rows_list):
     """Per layer, for the given query rows: stage-1 FLOPs (one QK pass,
     2*D*HQ*sum nk_t) and stage-2 FLOPs (4*D*G*sum rows(t,g)) — SURVEY §8(d)."""
@@ -155,11 +146,12 @@ def run_ours(args):
 
     import paper_2506_07900_b200 as P
     from paper_2506_07900_b200 import _lib
+    from paper_2506_07900_b200 import sharding as S
 
     lib = _lib.load()
     seq, layers = args.seq, args.layers
     cfg = P.SparseAttentionConfig(**GEOM)
-    chunks = zigzag_chunks(seq, world, rank)
+    chunks = S.zigzag_chunks(seq, world, rank)
     my_rows = sum(hi - lo for lo, hi in chunks)
 
     # ---- synthetic per-layer inputs, resident in HBM (each rank holds its own
@@ -178,9 +170,6 @@ def run_ours(args):
         k_in.append(ks)
         v_in.append(vs)
     caches = [P.BlockizedLayerCache(HKV, D, cfg, capacity=seq, device=dev) for _ in range(layers)]
-    size = seq // (2 * world)
-    gath_k = [torch.empty((world, size, HKV, D), dtype=torch.bfloat16, device=dev) for _ in range(2)]
-    gath_v = [torch.empty_like(g) for g in gath_k]
 
     stream = torch.cuda.current_stream(dev)
     ev_sel = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(layers * 2)]
@@ -188,24 +177,8 @@ def run_ours(args):
 
     def fill_cache(layer):
         """All-gather the token shards of K/V (the real exchange step), then
-        append in natural order and compress."""
-        cache = caches[layer]
-        cache.truncate(0)
-        if world == 1:
-            for (lo, hi), kk, vv in zip(chunks, k_in[layer], v_in[layer]):
-                cache.append(kk, vv)
-            return
-        for h in range(2):
-            dist.all_gather_into_tensor(gath_k[h], k_in[layer][h])
-            dist.all_gather_into_tensor(gath_v[h], v_in[layer][h])
-        # natural chunk c: first half c -> gath[0][c]; second half -> gath[1][2N-1-c]
-        ks, vs = [], []
-        for c in range(2 * world):
-            if c < world:
-                ks.append(gath_k[0][c]); vs.append(gath_v[0][c])
-            else:
-                ks.append(gath_k[1][2 * world - 1 - c]); vs.append(gath_v[1][2 * world - 1 - c])
-        cache.append(torch.cat(ks), torch.cat(vs))
+        append in natural order and compress (paper_2506_07900_b200.sharding)."""
+        S.fill_layer_cache(caches[layer], k_in[layer], v_in[layer], world)
 
     def attend(layer, timed=False, outs=None):
         cache = caches[layer]
@@ -338,6 +311,7 @@ def run_ours(args):
 
 
 def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dist):
+    from paper_2506_07900_b200 import sharding as S
     """Same metric through two_stage_attention with HOST inputs: per layer the
     pinned q/k/v shards are copied H2D on a copy stream (overlapped with the
     previous layer's compute), and the last layer's output is read back."""
@@ -355,9 +329,6 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
     out_host = torch.empty((chunks[0][1] - chunks[0][0], HQ, D), dtype=torch.bfloat16).pin_memory()
     copy_stream = torch.cuda.Stream(dev)
     h2d_bytes = sum(t.numel() * t.element_size() for grp in host[0] for t in grp) * layers
-    size = args.seq // (2 * world)
-    gk = [torch.empty((world, size, HKV, D), dtype=torch.bfloat16, device=dev) for _ in range(2)]
-    gv = [torch.empty_like(x) for x in gk]
 
     def step():
         ready = [torch.cuda.Event() for _ in range(layers)]
@@ -379,17 +350,7 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
             stream.wait_event(ready[layer])
             qd, kd, vd = dbuf[layer % nbuf]
             cache = caches[layer]
-            cache.truncate(0)
-            if world == 1:
-                for kk, vv in zip(kd, vd):
-                    cache.append(kk, vv)
-            else:
-                for h in range(2):
-                    dist.all_gather_into_tensor(gk[h], kd[h])
-                    dist.all_gather_into_tensor(gv[h], vd[h])
-                ks = [gk[0][c] if c < world else gk[1][2 * world - 1 - c] for c in range(2 * world)]
-                vs = [gv[0][c] if c < world else gv[1][2 * world - 1 - c] for c in range(2 * world)]
-                cache.append(torch.cat(ks), torch.cat(vs))
+            S.fill_layer_cache(cache, kd, vd, world)
             for h, (lo, hi) in enumerate(chunks):
                 o = P.two_stage_attention(qd[h], cache, cfg, lo)
                 if layer == layers - 1 and h == 0:

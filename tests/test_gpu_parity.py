@@ -206,3 +206,34 @@ def test_dense_degradation_vs_dense_oracle():
         dense, _ = O.dense_attention(q, k, v, length - 1)
         worst = max(worst, float(np.abs(out - dense).max()))
     assert worst < 1e-5
+
+
+class _RefLikeLayer:
+    """Stand-in for deskinfer's LayerCache surface (keys/values/length/heads)."""
+
+    def __init__(self, k, v):
+        self.keys, self.values = k, v
+        self.length = k.shape[0]
+        self.n_kv_heads, self.head_dim = k.shape[1], k.shape[2]
+
+
+@pytest.mark.parametrize("name", ["small_prefill", "b8_3k_chunk"])
+def test_numpy_compat_adapter_matches_reference(name):
+    """compat.two_stage_attention_numpy (the reference-signature switch in
+    INTEGRATION.md) reproduces the reference's outputs and traces."""
+    from paper_2506_07900_b200.compat import two_stage_attention_numpy
+    meta, z = load(name)
+    q, k, v = case_inputs(meta)
+    cfg = _cfg(meta)
+    layer = _RefLikeLayer(k, v)
+    rows = z["out_rows"]
+    traces = []
+    for r in rows[:6]:
+        out = two_stage_attention_numpy(q[r:r + 1], layer, cfg, meta["start"] + int(r), traces=traces)
+        j = int(np.flatnonzero(z["out_rows"] == r)[0])
+        assert out.dtype == np.float32
+        assert np.all(np.abs(out[0] - z["out"][j]) <= 2e-3 + 2e-2 * np.abs(z["out"][j]))
+    pos_of = {int(r): j for j, r in enumerate(z["rows"])}
+    for t in traces:
+        j = pos_of[t["query_pos"] - meta["start"]]
+        assert t["selected"] == [int(b) for b in z["selection"][j, t["group"]] if b >= 0]
