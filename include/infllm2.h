@@ -151,6 +151,42 @@ int infllm2_forward(const infllm2_geometry* g,
                     void* workspace, size_t workspace_bytes, int32_t flags,
                     infllm2_stream_t stream);
 
+/* ---------------------------------------------------------------- batched decode
+ * S sequences (each its own blockized cache of one layer) append one token and
+ * attend one query row: BASELINE configs[3].  The reference's decode is the same
+ * per-row procedure with n = 1 (model.py:442-444, specdec.py:717-718). */
+typedef struct infllm2_seq_desc {
+  void* k_cache;            /* bf16 [HKV][cap][D] */
+  void* v_cache;
+  int64_t cap;
+  float* fine_means;        /* f32 [HKV][means_cap][D] (stride 16) */
+  void* means_hi;           /* bf16 split of fine_means */
+  void* means_lo;
+  int64_t means_cap;
+  float* coarse_means;      /* f32 [HKV][coarse_cap][D] */
+  int64_t coarse_cap;
+} infllm2_seq_desc;
+
+/* Device table (descriptors, TMA tensor maps, device-resident lengths). */
+size_t infllm2_decode_table_bytes(int32_t n_seq);
+/* Build it from HOST descriptors and lengths into `table` (device memory of
+ * infllm2_decode_table_bytes bytes).  Synchronises `stream`; rebuild only when a
+ * cache is reallocated or its length changes outside infllm2_decode_step. */
+int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq,
+                               int32_t hkv, int32_t d, void* table, infllm2_stream_t stream);
+size_t infllm2_decode_workspace_bytes(const infllm2_geometry* g, int32_t n_seq, int32_t hkv,
+                                      int64_t max_cache_len);
+/* One decode step for all sequences: append k_new/v_new ((S, HKV, D) bf16) at
+ * each sequence's length (the device length is incremented), re-sync the kernel
+ * means, select and attend q ((S, HQ, D) bf16).  max_len_after bounds every
+ * sequence's length after the append (sizes the split-K grid).  Caches must have
+ * room for one more row.  selection (S, HKV, max_sel), out (S, HQ, D), lse (S, HQ). */
+int infllm2_decode_step(const infllm2_geometry* g, void* table, int32_t n_seq, int64_t max_len_after,
+                        int32_t hq, int32_t hkv, int32_t d, const void* q, const void* k_new,
+                        const void* v_new, int32_t* selection, void* out, float* lse,
+                        void* workspace, size_t workspace_bytes, int32_t flags,
+                        infllm2_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

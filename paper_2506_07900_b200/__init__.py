@@ -6,13 +6,14 @@ Drop-in for the reference's sparse-attention surface (``deskinfer.sparse``):
 hand-written sm_100a kernels in ``libinfllm2.so`` (C ABI: ``include/infllm2.h``).
 """
 
+from .decode import DecodeBatch
 from .errors import NumericError, ValidationError
 from .sparse import (BlockizedLayerCache, KVCache, SparseAttentionConfig, TouchStats,
                      blockized_cache, build_kernels, force_blocks, kernel_range_for_block,
                      partition_blocks, two_stage_attention)
 
 __all__ = [
-    "BlockizedLayerCache", "KVCache", "NumericError", "SparseAttentionConfig", "TouchStats",
+    "DecodeBatch", "BlockizedLayerCache", "KVCache", "NumericError", "SparseAttentionConfig", "TouchStats",
     "ValidationError", "blockized_cache", "build_kernels", "force_blocks",
     "kernel_range_for_block", "partition_blocks", "two_stage_attention",
 ]

@@ -57,6 +57,22 @@ SIGNATURES = {
                                        c_vp, c_vp, c_vp, c_sz, c_i32, c_vp]),
 }
 
+class SeqDesc(ctypes.Structure):
+    """``infllm2_seq_desc`` — one sequence's blockized cache (batched decode)."""
+
+    _fields_ = [("k_cache", c_vp), ("v_cache", c_vp), ("cap", c_i64), ("fine_means", c_vp), ("means_hi", c_vp),
+                ("means_lo", c_vp), ("means_cap", c_i64), ("coarse_means", c_vp), ("coarse_cap", c_i64)]
+
+
+SIGNATURES.update({
+    "infllm2_decode_table_bytes": (c_sz, [c_i32]),
+    "infllm2_decode_table_build": (ctypes.c_int, [ctypes.POINTER(SeqDesc), ctypes.POINTER(c_i64), c_i32, c_i32,
+                                                  c_i32, c_vp, c_vp]),
+    "infllm2_decode_workspace_bytes": (c_sz, [ctypes.POINTER(Geometry), c_i32, c_i32, c_i64]),
+    "infllm2_decode_step": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp,
+                                           c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_i32, c_vp]),
+})
+
 _lib = None
 _lock = threading.Lock()
 

@@ -180,4 +180,31 @@ int infllm2_forward(const infllm2_geometry* g, const void* q, int64_t q_row_stri
                         selection, out, lse, flags, stream);
 }
 
+size_t infllm2_decode_table_bytes(int32_t n_seq) { return n_seq > 0 ? decode_table_bytes(n_seq) : 0; }
+
+int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq, int32_t hkv,
+                               int32_t d, void* table, infllm2_stream_t stream) {
+  if (n_seq <= 0 || !seqs || !lens || !table) return INFLLM2_ERR_SHAPE;
+  for (int s = 0; s < n_seq; ++s)
+    if (lens[s] < 0 || lens[s] > seqs[s].cap) return INFLLM2_ERR_CAPACITY;
+  return decode_table_build(seqs, lens, n_seq, hkv, d, table, (cudaStream_t)stream);
+}
+
+size_t infllm2_decode_workspace_bytes(const infllm2_geometry* g, int32_t n_seq, int32_t hkv, int64_t max_cache_len) {
+  if (infllm2_validate_geometry(g) || n_seq <= 0) return 0;
+  return decode_workspace_bytes(*g, n_seq, hkv, max_cache_len);
+}
+
+int infllm2_decode_step(const infllm2_geometry* g, void* table, int32_t n_seq, int64_t max_len_after, int32_t hq,
+                        int32_t hkv, int32_t d, const void* q, const void* k_new, const void* v_new,
+                        int32_t* selection, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                        int32_t flags, infllm2_stream_t stream) {
+  int rc = infllm2_validate_geometry(g);
+  if (rc) return rc;
+  if (n_seq <= 0 || hq <= 0 || hkv <= 0 || hq % hkv || max_len_after < 1) return INFLLM2_ERR_SHAPE;
+  if (!decode_supported(*g, hq, hkv, d)) return INFLLM2_ERR_UNSUPPORTED;
+  return decode_step(*g, table, n_seq, max_len_after, hq, hkv, d, q, k_new, v_new, selection, out,
+                     (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0, lse, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 }  // extern "C"

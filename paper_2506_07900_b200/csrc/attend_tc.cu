@@ -66,7 +66,17 @@ struct Params {
   const int32_t* sel;
   void* out;
   float* lse;
+  // batched decode: row i is sequence i with its own cache; its K/V tensor maps
+  // are kv_maps[map_stride*i + 0/1] (device memory) and its query position is
+  // seq_len[i] - 1.  Both null for prefill (one cache, pos = start + i).
+  const CUtensorMap* kv_maps;
+  int map_stride;
+  const int64_t* seq_len;
 };
+
+__device__ __forceinline__ int64_t item_pos(const Params& p, int64_t i) {
+  return p.seq_len ? p.seq_len[i] - 1 : p.start + i;
+}
 
 // The item's selection row, read once per warp with lane-parallel loads
 // (entries lane, lane+32, lane+64); nb = blocks that start at or before pos.
@@ -148,7 +158,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int64_t i = item / p.hkv;
       const int grp = (int)(item - i * p.hkv);
-      const int64_t pos = p.start + i;
+      const int64_t pos = item_pos(p, i);
+      const CUtensorMap* mk = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i : &tm_k;
+      const CUtensorMap* mv = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i + 1 : &tm_v;
       const SelRow sr = load_sel(p, item, pos, lane);
       const int nb = sr.nb;
       const int qb = it & 1;
@@ -171,10 +183,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           for (int x = 0; x < nt; ++x) {
             const int row0 = (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
-            tma_load_3d(kd + off, &tm_k, kv_full + stage, 0, row0, grp);
-            tma_load_3d(kd + kHalfBytes + off, &tm_k, kv_full + stage, 64, row0, grp);
-            tma_load_3d(vd + off, &tm_v, kv_full + stage, 0, row0, grp);
-            tma_load_3d(vd + kHalfBytes + off, &tm_v, kv_full + stage, 64, row0, grp);
+            tma_load_3d(kd + off, mk, kv_full + stage, 0, row0, grp);
+            tma_load_3d(kd + kHalfBytes + off, mk, kv_full + stage, 64, row0, grp);
+            tma_load_3d(vd + off, mv, kv_full + stage, 0, row0, grp);
+            tma_load_3d(vd + kHalfBytes + off, mv, kv_full + stage, 64, row0, grp);
           }
         }
         __syncwarp();
@@ -192,7 +204,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     int it = 0;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int64_t i = item / p.hkv;
-      const int64_t pos = p.start + i;
+      const int64_t pos = item_pos(p, i);
       const SelRow sr = load_sel(p, item, pos, lane);
       const int nb = sr.nb;
       const int tiles = (nb + 1) / 2;
@@ -272,7 +284,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     int it = 0;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int64_t i = item / p.hkv;
-      const int64_t pos = p.start + i;
+      const int64_t pos = item_pos(p, i);
       const SelRow sr = load_sel(p, item, pos, lane);
       const int nb = sr.nb;
       const int tiles = (nb + 1) / 2;
@@ -449,6 +461,42 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
 }  // namespace
 
+// Batched decode: one query row per sequence, per-sequence K/V tensor maps in
+// device memory (maps[stride*s + 0] = K, + 1 = V), positions seq_len[s] - 1.
+cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
+                                    const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
+                                    const int32_t* selection, void* out, int out_f32, float* lse,
+                                    cudaStream_t stream) {
+  Params p;
+  p.n = n_seq;
+  p.start = 0;
+  p.hq = hq;
+  p.hkv = hkv;
+  p.max_sel = max_sel;
+  p.out_f32 = out_f32;
+  p.sel = selection;
+  p.out = out;
+  p.lse = lse;
+  p.kv_maps = kv_maps;
+  p.map_stride = map_stride;
+  p.seq_len = seq_len;
+  CUtensorMap tq;
+  const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
+  const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
+  const uint32_t box[3] = {64, (uint32_t)kG, 1};
+  if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
+  const size_t smem = Smem::total + 1024;
+  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t items = n_seq * hkv;
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(items < sms ? items : sms);
+  count_launch();
+  attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tq, tq, p);
+  return cudaGetLastError();
+}
+
 bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
   if (!tc_kernels_enabled()) return false;
   if (cs.group != kG || cs.d != kD || g.block_size != kM) return false;
@@ -469,6 +517,9 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.sel = selection;
   p.out = out;
   p.lse = lse;
+  p.kv_maps = nullptr;
+  p.map_stride = 0;
+  p.seq_len = nullptr;
   CUtensorMap tq, tk, tv;
   {
     const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)cs.n};

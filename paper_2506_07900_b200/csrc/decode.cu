@@ -1,0 +1,617 @@
+// Batched single-token decode (BASELINE configs[3]): S sequences, each with its
+// own blockized cache, append one token and attend one query row per layer.
+//
+// Per layer-step, five launches, all batched over sequences:
+//   1. decode_append_compress_kernel  new K/V row + the <= 3 kernel windows it
+//      touches (fine, hi/lo split, coarse), bitwise as build_kernels
+//      (sparse.py:70-91, 111-133); bumps the device-side length.
+//   2. decode_stage1_kernel (tcgen05)  split-K over 256-kernel chunks of every
+//      (sequence, group): z = mu . q for the 16 heads (M = 128 kernels, N = 16
+//      heads, bf16 hi+lo), written to an L2-resident z buffer, plus per-chunk
+//      (max, sum 2^z) partials.  HBM-bound on the means (8.4 MB per 128K seq-layer).
+//   3. decode_scores_kernel  combine partials -> exact per-head LSE; group
+//      score S_j = mean_h 2^(z - lse) (sparse.py:163-188); block max over each
+//      block's kernels (sparse.py:191-215) for a range of 64 blocks.
+//   4. decode_topk_kernel  one warp per (sequence, group): forced + top-k
+//      (sparse.py:218-277) via topk::warp_select.
+//   5. attend_tc_kernel with per-sequence K/V tensor maps (stage 2).
+#include <float.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tc_dispatch.cuh"
+#include "topk.cuh"
+
+namespace infllm2 {
+
+cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
+                                    const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
+                                    const int32_t* selection, void* out, int out_f32, float* lse,
+                                    cudaStream_t stream);
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kG = 16;
+constexpr int kD = 128;
+constexpr int kS = 16;             // fine stride
+constexpr int kP = 32;             // kernel size
+constexpr int kTile = 128;         // kernels per MMA tile
+constexpr int kChunk = 256;        // kernels per stage-1 work item
+constexpr int kBlkChunk = 64;      // blocks per scores work item
+constexpr int kMaps = 4;           // per sequence: K, V, hi, lo
+
+// Device-side table: [n_seq] descriptors, [n_seq][4] tensor maps, [n_seq] lengths.
+struct SeqDesc {
+  __nv_bfloat16* k;
+  __nv_bfloat16* v;
+  int64_t cap;
+  float* fine;
+  __nv_bfloat16* hi;
+  __nv_bfloat16* lo;
+  int64_t means_cap;
+  float* coarse;
+  int64_t coarse_cap;
+};
+
+struct TableView {
+  const SeqDesc* desc;
+  const CUtensorMap* maps;
+  int64_t* len;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline TableView table_view(void* base, int n_seq) {
+  uint8_t* b = static_cast<uint8_t*>(base);
+  TableView t;
+  const size_t maps_off = align_up(sizeof(SeqDesc) * n_seq, 128);
+  const size_t len_off = maps_off + sizeof(CUtensorMap) * kMaps * n_seq;
+  t.desc = reinterpret_cast<const SeqDesc*>(b);
+  t.maps = reinterpret_cast<const CUtensorMap*>(b + maps_off);
+  t.len = reinterpret_cast<int64_t*>(b + len_off);
+  return t;
+}
+
+size_t table_bytes(int n_seq) {
+  return align_up(sizeof(SeqDesc) * n_seq, 128) + sizeof(CUtensorMap) * kMaps * n_seq + sizeof(int64_t) * n_seq;
+}
+
+// ------------------------------------------------------------------ 1. append + compress
+
+__device__ void window_mean(const __nv_bfloat16* kg, int64_t cap, int d, int64_t j, int stride, int64_t length,
+                            int e, float* out_mean) {
+  const int64_t r0 = j * stride;
+  int64_t r1 = r0 + kP;
+  if (r1 > length) r1 = length;
+  const __nv_bfloat16* src = kg + r0 * d + e;
+  double acc = (double)__bfloat162float(src[0]);
+  for (int64_t r = 1; r < r1 - r0; ++r) acc += (double)__bfloat162float(src[r * d]);
+  *out_mean = __double2float_rn(acc / (double)(r1 - r0));
+}
+
+__global__ void __launch_bounds__(256) decode_append_compress_kernel(void* table, int n_seq, int hkv, int d,
+                                                                     const __nv_bfloat16* __restrict__ k_new,
+                                                                     const __nv_bfloat16* __restrict__ v_new,
+                                                                     int coarse_stride) {
+  const int s = blockIdx.x;
+  TableView tv = table_view(table, n_seq);
+  const SeqDesc ds = tv.desc[s];
+  const int64_t l_old = tv.len[s];
+  const int64_t l_new = l_old + 1;
+  for (int idx = threadIdx.x; idx < hkv * d; idx += blockDim.x) {
+    const int g = idx / d, e = idx - g * d;
+    ds.k[((int64_t)g * ds.cap + l_old) * d + e] = k_new[(int64_t)s * hkv * d + idx];
+    ds.v[((int64_t)g * ds.cap + l_old) * d + e] = v_new[(int64_t)s * hkv * d + idx];
+  }
+  __syncthreads();
+  // fine windows (stride 16): first dirty window clipped to those that existed (F18)
+  {
+    int64_t first = l_old < kP ? 0 : (l_old - kP) / kS + 1;
+    const int64_t count_old = l_old / kS, count = l_new / kS;
+    if (first > count_old) first = count_old;
+    const int64_t nwin = count - first;
+    for (int64_t idx = threadIdx.x; idx < nwin * hkv * d; idx += blockDim.x) {
+      const int64_t j = first + idx / (hkv * d);
+      const int rem = (int)(idx % (hkv * d));
+      const int g = rem / d, e = rem - g * d;
+      float mu;
+      window_mean(ds.k + (int64_t)g * ds.cap * d, ds.cap, d, j, kS, l_new, e, &mu);
+      const int64_t dst = ((int64_t)g * ds.means_cap + j) * d + e;
+      ds.fine[dst] = mu;
+      const __nv_bfloat16 h = __float2bfloat16_rn(mu);
+      ds.hi[dst] = h;
+      ds.lo[dst] = __float2bfloat16_rn(mu - __bfloat162float(h));
+    }
+  }
+  {
+    int64_t first = l_old < kP ? 0 : (l_old - kP) / coarse_stride + 1;
+    const int64_t count_old = l_old / coarse_stride, count = l_new / coarse_stride;
+    if (first > count_old) first = count_old;
+    const int64_t nwin = count - first;
+    for (int64_t idx = threadIdx.x; idx < nwin * hkv * d; idx += blockDim.x) {
+      const int64_t j = first + idx / (hkv * d);
+      const int rem = (int)(idx % (hkv * d));
+      const int g = rem / d, e = rem - g * d;
+      float mu;
+      window_mean(ds.k + (int64_t)g * ds.cap * d, ds.cap, d, j, coarse_stride, l_new, e, &mu);
+      ds.coarse[((int64_t)g * ds.coarse_cap + j) * d + e] = mu;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tv.len[s] = l_new;
+}
+
+// ------------------------------------------------------------------ 2. stage-1 (tcgen05, split-K)
+
+constexpr int kS1Stages = 3;
+constexpr uint32_t kMuHalf = kTile * 128;          // 16 KB
+constexpr uint32_t kMuStage = 4 * kMuHalf;         // hi h0,h1, lo h0,h1
+constexpr uint32_t kQB = 2 * kG * 128;             // 4 KB
+constexpr int kS1Threads = 192;                     // 0 TMA, 1 MMA, 2..5 epilogue
+
+struct S1Smem {
+  static constexpr uint32_t mu = 0;
+  static constexpr uint32_t q = mu + kS1Stages * kMuStage;
+  static constexpr uint32_t red = q + 2 * kQB;                    // [128][16] m, [128][16] s
+  static constexpr uint32_t bars = red + 2 * 128 * kG * 4;
+  static constexpr uint32_t total = bars + 32 * 8;
+};
+
+struct S1Params {
+  void* table;
+  int n_seq, hkv;
+  int64_t nchunk;            // chunks per (seq, group)
+  int64_t zstride;           // floats per (seq, group) in zbuf
+  float* zbuf;               // [seq][g][kernel][16] log2-domain scores
+  float* pstat;              // [seq][g][chunk][16][2]
+  float zscale;
+};
+
+__device__ __forceinline__ void s1_item(const S1Params& p, const TableView& tv, int64_t item, int* s, int* g,
+                                        int64_t* j0, int64_t* j1) {
+  const int64_t sg = item / p.nchunk;
+  const int64_t c = item - sg * p.nchunk;
+  *s = (int)(sg / p.hkv);
+  *g = (int)(sg - (int64_t)(*s) * p.hkv);
+  const int64_t nk = tv.len[*s] / kS;
+  *j0 = c * kChunk;
+  int64_t e = *j0 + kChunk;
+  *j1 = e < nk ? e : nk;
+}
+
+__global__ void __launch_bounds__(kS1Threads, 1)
+decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S1Smem::bars);
+  uint64_t* mu_full = bars;          // [3]
+  uint64_t* mu_empty = bars + 3;     // [3]
+  uint64_t* q_full = bars + 6;       // [2]
+  uint64_t* q_empty = bars + 8;      // [2]
+  uint64_t* s_full = bars + 10;      // [2]
+  uint64_t* s_empty = bars + 12;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  float* red_m = reinterpret_cast<float*>(smem + S1Smem::red);
+  float* red_s = red_m + 128 * kG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TableView tv = table_view(p.table, p.n_seq);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kS1Stages; ++i) { mbar_init(mu_full + i, 1); mbar_init(mu_empty + i, 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 4);
+    }
+    fence_barrier_init();
+    tma_prefetch(&tm_q);
+  }
+  if (warp == 1) tmem_alloc<32>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t items = (int64_t)p.n_seq * p.hkv * p.nchunk;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        int s, g;
+        int64_t j0, j1;
+        s1_item(p, tv, item, &s, &g, &j0, &j1);
+        if (j0 >= j1) continue;
+        const int qb = it & 1;
+        mbar_wait(q_empty + qb, ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full + qb, kQB);
+        uint8_t* qd = smem + S1Smem::q + qb * kQB;
+        tma_load_3d(qd, &tm_q, q_full + qb, 0, g * kG, s);
+        tma_load_3d(qd + kQB / 2, &tm_q, q_full + qb, 64, g * kG, s);
+        const CUtensorMap* mhi = tv.maps + (int64_t)kMaps * s + 2;
+        const CUtensorMap* mlo = tv.maps + (int64_t)kMaps * s + 3;
+        for (int64_t t0 = j0; t0 < j1; t0 += kTile) {
+          mbar_wait(mu_empty + stage, phase ^ 1);
+          mbar_arrive_expect_tx(mu_full + stage, kMuStage);
+          uint8_t* dst = smem + S1Smem::mu + stage * kMuStage;
+          tma_load_3d(dst, mhi, mu_full + stage, 0, (int)t0, g);
+          tma_load_3d(dst + kMuHalf, mhi, mu_full + stage, 64, (int)t0, g);
+          tma_load_3d(dst + 2 * kMuHalf, mlo, mu_full + stage, 0, (int)t0, g);
+          tma_load_3d(dst + 3 * kMuHalf, mlo, mu_full + stage, 64, (int)t0, g);
+          if (++stage == kS1Stages) { stage = 0; phase ^= 1; }
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(128, kG);
+    int stage = 0, slot = 0;
+    uint32_t phase = 0;
+    uint32_t s_ph[2] = {0, 0};
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+      int s, g;
+      int64_t j0, j1;
+      s1_item(p, tv, item, &s, &g, &j0, &j1);
+      if (j0 >= j1) continue;
+      const int qb = it & 1;
+      mbar_wait(q_full + qb, (it >> 1) & 1);
+      const uint32_t q_addr = smem_u32(smem + S1Smem::q + qb * kQB);
+      for (int64_t t0 = j0; t0 < j1; t0 += kTile) {
+        mbar_wait(mu_full + stage, phase);
+        mbar_wait(s_empty + slot, s_ph[slot] ^ 1);
+        s_ph[slot] ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t mu_s = smem_u32(smem + S1Smem::mu + stage * kMuStage);
+          for (int part = 0; part < 2; ++part) {
+            for (int k = 0; k < kD / 16; ++k) {
+              const uint32_t koff = (k & 3) * 32;
+              const uint32_t mu_k = mu_s + part * 2 * kMuHalf + (k >> 2) * kMuHalf + koff;
+              const uint32_t q_k = q_addr + (k >> 2) * (kQB / 2) + koff;
+              umma_f16_ss(tmem + slot * kG, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc, (part | k) ? 1u : 0u);
+            }
+          }
+          umma_commit(mu_empty + stage);
+          umma_commit(s_full + slot);
+          if (t0 + kTile >= j1) umma_commit(q_empty + qb);
+        }
+        __syncwarp();
+        if (++stage == kS1Stages) { stage = 0; phase ^= 1; }
+        slot ^= 1;
+      }
+      ++it;
+    }
+  } else {
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const int etid = (warp - 2) * 32 + lane;
+    int slot = 0;
+    uint32_t s_ph[2] = {0, 0};
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+      int s, g;
+      int64_t j0, j1;
+      s1_item(p, tv, item, &s, &g, &j0, &j1);
+      float* ps = p.pstat + item * (2 * kG);
+      if (j0 >= j1) {
+        if (etid < kG) { ps[2 * etid] = -INFINITY; ps[2 * etid + 1] = 0.f; }
+        continue;
+      }
+      float m[kG], sm[kG];
+#pragma unroll
+      for (int h = 0; h < kG; ++h) { m[h] = -INFINITY; sm[h] = 0.f; }
+      float* zg = p.zbuf + ((int64_t)s * p.hkv + g) * p.zstride;
+      for (int64_t t0 = j0; t0 < j1; t0 += kTile) {
+        mbar_wait(s_full + slot, s_ph[slot]);
+        s_ph[slot] ^= 1;
+        tc_fence_after();
+        float v[kG];
+        tmem_ld16(tmem + lane_base + slot * kG, v);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + slot);
+        slot ^= 1;
+        const int64_t j = t0 + row;
+        if (j < j1) {
+#pragma unroll
+          for (int h = 0; h < kG; ++h) v[h] *= p.zscale;
+          float4* dst = reinterpret_cast<float4*>(zg + j * kG);
+#pragma unroll
+          for (int x = 0; x < 4; ++x) dst[x] = make_float4(v[4 * x], v[4 * x + 1], v[4 * x + 2], v[4 * x + 3]);
+#pragma unroll
+          for (int h = 0; h < kG; ++h) {
+            if (v[h] > m[h]) {
+              sm[h] = sm[h] * ex2(m[h] - v[h]) + 1.f;
+              m[h] = v[h];
+            } else {
+              sm[h] += ex2(v[h] - m[h]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < kG; ++h) { red_m[h * 128 + etid] = m[h]; red_s[h * 128 + etid] = sm[h]; }
+      named_bar_sync(1, 128);
+      if (etid < kG) {
+        float M = -INFINITY;
+        for (int x = 0; x < 128; ++x) M = fmaxf(M, red_m[etid * 128 + x]);
+        float S = 0.f;
+        for (int x = 0; x < 128; ++x) {
+          const float mm = red_m[etid * 128 + x];
+          if (mm != -INFINITY) S += red_s[etid * 128 + x] * ex2(mm - M);
+        }
+        ps[2 * etid] = M;
+        ps[2 * etid + 1] = S;
+      }
+      named_bar_sync(1, 128);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<32>(tmem);
+}
+
+// ------------------------------------------------------------------ 3. block scores
+
+struct ScoreParams {
+  void* table;
+  int n_seq, hkv, m, kpb;
+  int64_t nchunk, nbchunk, zstride, nb_cap;
+  const float* zbuf;
+  const float* pstat;
+  float* rbuf;               // [seq][g][nb_cap]
+};
+
+__global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p) {
+  __shared__ float lse2[kG];
+  __shared__ float sk[kBlkChunk * 8 + 8];   // kernels of this block range (kpb <= 8)
+  const TableView tv = table_view(p.table, p.n_seq);
+  const int64_t item = blockIdx.x;
+  const int64_t sg = item / p.nbchunk;
+  const int64_t bc = item - sg * p.nbchunk;
+  const int s = (int)(sg / p.hkv);
+  const int g = (int)(sg - (int64_t)s * p.hkv);
+  const int64_t L = tv.len[s];
+  const int64_t pos = L - 1;
+  int64_t nk_t = pos / kS + 1;
+  if (nk_t > L / kS) nk_t = L / kS;
+  const int64_t n_cand = pos / p.m + 1;
+  const int64_t b0 = bc * kBlkChunk;
+  if (b0 >= n_cand) return;
+  const int64_t b1 = b0 + kBlkChunk < n_cand ? b0 + kBlkChunk : n_cand;
+  if (threadIdx.x < kG) {
+    const float* ps = p.pstat + sg * p.nchunk * (2 * kG);
+    float M = -INFINITY;
+    for (int64_t c = 0; c < p.nchunk; ++c) M = fmaxf(M, ps[c * 2 * kG + 2 * threadIdx.x]);
+    float S = 0.f;
+    for (int64_t c = 0; c < p.nchunk; ++c) {
+      const float mm = ps[c * 2 * kG + 2 * threadIdx.x];
+      if (mm != -INFINITY) S += ps[c * 2 * kG + 2 * threadIdx.x + 1] * ex2(mm - M);
+    }
+    lse2[threadIdx.x] = M + log2f(S);
+  }
+  __syncthreads();
+  // kernel range covering blocks [b0, b1): lo of b0 .. hi of b1-1
+  int64_t jlo, jhi, tmp;
+  kernel_range_for_block(b0 * p.m, b0 * p.m + p.m, kP, kS, nk_t, &jlo, &tmp);
+  jhi = b1 * p.kpb < nk_t ? b1 * p.kpb : nk_t;
+  const float* zg = p.zbuf + sg * p.zstride;
+  for (int64_t j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
+    const float4* z4 = reinterpret_cast<const float4*>(zg + j * kG);
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const float4 z = z4[x];
+      a0 += ex2(z.x - lse2[4 * x]) + ex2(z.z - lse2[4 * x + 2]);
+      a1 += ex2(z.y - lse2[4 * x + 1]) + ex2(z.w - lse2[4 * x + 3]);
+    }
+    sk[j - jlo] = (a0 + a1) * (1.0f / kG);
+  }
+  __syncthreads();
+  for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    int64_t end = (b + 1) * p.m;
+    if (end > pos + 1) end = pos + 1;
+    int64_t lo, hi;
+    kernel_range_for_block(b * p.m, end, kP, kS, nk_t, &lo, &hi);
+    float r = 0.f;
+    if (hi > lo) {
+      r = sk[lo - jlo];
+      for (int64_t j = lo + 1; j < hi; ++j) r = fmaxf(r, sk[j - jlo]);
+    }
+    p.rbuf[sg * p.nb_cap + b] = r;
+  }
+}
+
+// ------------------------------------------------------------------ 4. top-k
+
+struct TopkParams {
+  void* table;
+  int n_seq, hkv, m, top_k, n_init, n_local, consume, max_sel;
+  int64_t nb_cap;
+  const float* rbuf;
+  int32_t* selection;
+};
+
+__global__ void __launch_bounds__(32) decode_topk_kernel(const TopkParams p) {
+  __shared__ float lkey[topk::kListCap];
+  __shared__ int lid[topk::kListCap];
+  const TableView tv = table_view(p.table, p.n_seq);
+  const int64_t sg = blockIdx.x;
+  const int s = (int)(sg / p.hkv);
+  const int64_t pos = tv.len[s] - 1;
+  const topk::UnitSel us = topk::unit_sel(pos, p.m, p.top_k, p.n_init, p.n_local, p.consume);
+  topk::warp_select(p.rbuf + sg * p.nb_cap, us, threadIdx.x, lkey, lid, p.selection + sg * p.max_sel, nullptr,
+                    p.max_sel);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host API
+
+size_t decode_table_bytes(int n_seq) { return table_bytes(n_seq); }
+
+int decode_table_build(const infllm2_seq_desc* host, const int64_t* lens, int n_seq, int hkv, int d,
+                       void* table_dev, cudaStream_t stream) {
+  const size_t bytes = table_bytes(n_seq);
+  uint8_t* staging = static_cast<uint8_t*>(malloc(bytes));
+  if (!staging) return INFLLM2_ERR_CUDA;
+  memset(staging, 0, bytes);
+  TableView tv = table_view(staging, n_seq);
+  SeqDesc* desc = const_cast<SeqDesc*>(tv.desc);
+  CUtensorMap* maps = const_cast<CUtensorMap*>(tv.maps);
+  int rc = INFLLM2_OK;
+  for (int s = 0; s < n_seq && rc == INFLLM2_OK; ++s) {
+    const infllm2_seq_desc& h = host[s];
+    desc[s].k = static_cast<__nv_bfloat16*>(h.k_cache);
+    desc[s].v = static_cast<__nv_bfloat16*>(h.v_cache);
+    desc[s].cap = h.cap;
+    desc[s].fine = h.fine_means;
+    desc[s].hi = static_cast<__nv_bfloat16*>(h.means_hi);
+    desc[s].lo = static_cast<__nv_bfloat16*>(h.means_lo);
+    desc[s].means_cap = h.means_cap;
+    desc[s].coarse = h.coarse_means;
+    desc[s].coarse_cap = h.coarse_cap;
+    tv.len[s] = lens[s];
+    const uint64_t kdims[3] = {(uint64_t)d, (uint64_t)h.cap, (uint64_t)hkv};
+    const uint64_t kstr[2] = {(uint64_t)d * 2, (uint64_t)h.cap * d * 2};
+    const uint32_t kbox[3] = {64, 64, 1};
+    const uint64_t mdims[3] = {(uint64_t)d, (uint64_t)h.means_cap, (uint64_t)hkv};
+    const uint64_t mstr[2] = {(uint64_t)d * 2, (uint64_t)h.means_cap * d * 2};
+    const uint32_t mbox[3] = {64, (uint32_t)kTile, 1};
+    if (!encode_tmap_3d_bf16(&maps[kMaps * s + 0], h.k_cache, kdims, kstr, kbox) ||
+        !encode_tmap_3d_bf16(&maps[kMaps * s + 1], h.v_cache, kdims, kstr, kbox) ||
+        !encode_tmap_3d_bf16(&maps[kMaps * s + 2], h.means_hi, mdims, mstr, mbox) ||
+        !encode_tmap_3d_bf16(&maps[kMaps * s + 3], h.means_lo, mdims, mstr, mbox))
+      rc = INFLLM2_ERR_SHAPE;
+  }
+  if (rc == INFLLM2_OK) {
+    // pageable source: the copy completes (staged) before cudaMemcpyAsync returns
+    if (cudaMemcpyAsync(table_dev, staging, bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+      rc = INFLLM2_ERR_CUDA;
+    else if (cudaStreamSynchronize(stream) != cudaSuccess)
+      rc = INFLLM2_ERR_CUDA;
+  }
+  free(staging);
+  return rc;
+}
+
+struct DecodeWs {
+  float* zbuf;
+  float* pstat;
+  float* rbuf;
+  int64_t nchunk, nbchunk, zstride, nb_cap;
+  size_t bytes;
+};
+
+static DecodeWs decode_ws_layout(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len, void* base) {
+  DecodeWs w;
+  const int64_t nk = max_len / kS + 1;
+  w.nchunk = (nk + kChunk - 1) / kChunk;
+  w.zstride = w.nchunk * kChunk * kG;
+  w.nb_cap = max_len / g.block_size + 2;
+  w.nbchunk = (w.nb_cap + kBlkChunk - 1) / kBlkChunk;
+  uint8_t* b = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  w.zbuf = reinterpret_cast<float*>(b + off);
+  off += align_up(sizeof(float) * n_seq * hkv * w.zstride, 256);
+  w.pstat = reinterpret_cast<float*>(b + off);
+  off += align_up(sizeof(float) * n_seq * hkv * w.nchunk * 2 * kG, 256);
+  w.rbuf = reinterpret_cast<float*>(b + off);
+  off += align_up(sizeof(float) * n_seq * hkv * w.nb_cap, 256);
+  w.bytes = off;
+  return w;
+}
+
+bool decode_supported(const infllm2_geometry& g, int hq, int hkv, int d) {
+  return hq / hkv == kG && hq % hkv == 0 && d == kD && g.kernel_stride == kS && g.kernel_size == kP &&
+         g.block_size == 64 && g.coarse_stride % kS == 0 && infllm2_max_selected(&g) <= 80;
+}
+
+size_t decode_workspace_bytes(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len) {
+  return decode_ws_layout(g, n_seq, hkv, max_len, nullptr).bytes;
+}
+
+int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv, int d,
+                const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32,
+                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  DecodeWs w = decode_ws_layout(g, n_seq, hkv, max_len_after, ws);
+  if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
+  const int max_sel = infllm2_max_selected(&g);
+  const TableView tvd = table_view(table, n_seq);
+  // 1. append + compress
+  count_launch();
+  decode_append_compress_kernel<<<n_seq, 256, 0, stream>>>(table, n_seq, hkv, d,
+                                                            static_cast<const __nv_bfloat16*>(k_new),
+                                                            static_cast<const __nv_bfloat16*>(v_new), g.coarse_stride);
+  // 2. stage-1 split-K
+  S1Params sp;
+  sp.table = table;
+  sp.n_seq = n_seq;
+  sp.hkv = hkv;
+  sp.nchunk = w.nchunk;
+  sp.zstride = w.zstride;
+  sp.zbuf = w.zbuf;
+  sp.pstat = w.pstat;
+  sp.zscale = 1.4426950408889634f / sqrtf((float)kD);
+  CUtensorMap tq;
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
+    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
+    const uint32_t box[3] = {64, (uint32_t)kG, 1};
+    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
+  }
+  const size_t smem1 = S1Smem::total + 1024;
+  if (cudaFuncSetAttribute(decode_stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) !=
+      cudaSuccess)
+    return INFLLM2_ERR_CUDA;
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items1 = (int64_t)n_seq * hkv * w.nchunk;
+  count_launch();
+  decode_stage1_kernel<<<(int)(items1 < sms ? items1 : sms), kS1Threads, smem1, stream>>>(tq, sp);
+  // 3. block scores
+  ScoreParams scp;
+  scp.table = table;
+  scp.n_seq = n_seq;
+  scp.hkv = hkv;
+  scp.m = g.block_size;
+  scp.kpb = g.block_size / kS;
+  scp.nchunk = w.nchunk;
+  scp.nbchunk = w.nbchunk;
+  scp.zstride = w.zstride;
+  scp.nb_cap = w.nb_cap;
+  scp.zbuf = w.zbuf;
+  scp.pstat = w.pstat;
+  scp.rbuf = w.rbuf;
+  count_launch();
+  decode_scores_kernel<<<(int)(n_seq * hkv * w.nbchunk), 256, 0, stream>>>(scp);
+  // 4. top-k
+  TopkParams tp;
+  tp.table = table;
+  tp.n_seq = n_seq;
+  tp.hkv = hkv;
+  tp.m = g.block_size;
+  tp.top_k = g.top_k;
+  tp.n_init = g.n_init_blocks;
+  tp.n_local = g.n_local_blocks;
+  tp.consume = g.forced_consume_budget;
+  tp.max_sel = max_sel;
+  tp.nb_cap = w.nb_cap;
+  tp.rbuf = w.rbuf;
+  tp.selection = selection;
+  count_launch();
+  decode_topk_kernel<<<n_seq * hkv, 32, 0, stream>>>(tp);
+  // 5. stage 2
+  cudaError_t e = launch_attend_tc_decode(hq, hkv, max_sel, n_seq, q, tvd.maps, kMaps, tvd.len, selection, out,
+                                          out_f32, lse, stream);
+  if (e != cudaSuccess) return INFLLM2_ERR_CUDA;
+  return cudaGetLastError() == cudaSuccess ? INFLLM2_OK : INFLLM2_ERR_CUDA;
+}
+
+}  // namespace infllm2

@@ -33,6 +33,7 @@
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tc_dispatch.cuh"
+#include "topk.cuh"
 
 namespace infllm2 {
 
@@ -50,8 +51,11 @@ constexpr int kEpiWarps = 8;
 constexpr int kTopkWarps = 4;     // dedicated selection warps (4 queries each)
 constexpr int kThreads = 32 * (2 + kEpiWarps + kTopkWarps);
 constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kListCap = 352;     // per-warp threshold-compaction list (+ staging tail)
-constexpr int kOutCap = 96;
+using topk::kListCap;
+using topk::kOutCap;
+using topk::UnitSel;
+using topk::unit_sel;
+using topk::warp_select;
 
 constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
 constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 128 B)
@@ -100,189 +104,6 @@ __device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t n
   int64_t need = (qb + 1) * p.kpb;
   if (nk > need) need = nk;
   return (int)((need + kNT - 1) / kNT);
-}
-
-__device__ __forceinline__ bool better(float ra, int ba, float rb, int bb) {
-  return ra > rb || (ra == rb && ba < bb);   // (score desc, id asc), sparse.py:273
-}
-
-// Forced set / budget of a unit (all 16 rows share it): force_blocks
-// (sparse.py:218-227) and the budget rule of select_topk (sparse.py:268).
-struct UnitSel {
-  int64_t qb, n_cand, n_init, local_lo, budget, n_free;
-};
-__device__ __forceinline__ UnitSel unit_sel(const Params& p, int64_t t0) {
-  UnitSel u;
-  u.qb = t0 / p.m;
-  u.n_cand = u.qb + 1;
-  u.n_init = p.n_init < u.n_cand ? p.n_init : u.n_cand;
-  u.local_lo = u.qb + 1;
-  if (p.n_local > 0) {
-    u.local_lo = u.qb - p.n_local + 1;
-    if (u.local_lo < 0) u.local_lo = 0;
-    if (u.local_lo < u.n_init) u.local_lo = u.n_init;
-  }
-  const int64_t n_forced = u.n_init + (u.qb + 1 - u.local_lo);
-  u.budget = p.top_k;
-  if (p.consume) u.budget = p.top_k - n_forced > 0 ? p.top_k - n_forced : 0;
-  u.n_free = u.n_cand - n_forced;
-  return u;
-}
-
-// Warp bitonic sort of one value per lane: descending floats / ascending ints.
-__device__ __forceinline__ float warp_sort_desc(float x, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const float y = __shfl_xor_sync(0xffffffffu, x, j);
-      const bool keep_max = (((lane & k) == 0) == ((lane & j) == 0));
-      x = keep_max ? fmaxf(x, y) : fminf(x, y);
-    }
-  return x;
-}
-__device__ __forceinline__ int warp_sort_asc(int x, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int y = __shfl_xor_sync(0xffffffffu, x, j);
-      const bool keep_min = (((lane & k) == 0) == ((lane & j) == 0));
-      x = keep_min ? min(x, y) : max(x, y);
-    }
-  return x;
-}
-
-// Warp argmax over (score desc, id asc) strictly after (prev_v, prev_b) in that order.
-__device__ __forceinline__ void warp_best_after(float& bv, int& bb) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-    const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
-    if (ob >= 0 && (bb < 0 || better(ov, ob, bv, bb))) { bv = ov; bb = ob; }
-  }
-}
-
-// One query's selection by one warp: forced init blocks, the `budget` best
-// candidates of rq[n_init, local_lo) by (score desc, id asc), forced local
-// blocks; written ascending with -1 padding (select_topk, sparse.py:247-277).
-// Fast path (budget <= 32): threshold T0 = budget-th largest lane maximum
-// (at least `budget` candidates reach it, so the answer lies in {r >= T0}),
-// compact that set in id order, pick `budget` from it, bitonic-sort the ids.
-__device__ void warp_select(const float* rq, const UnitSel& u, int lane, float* lkey, int* lid, int32_t* out,
-                            double* osc, int max_sel) {
-  const int lo = (int)u.n_init, hi = (int)u.local_lo;
-  const int budget = (int)u.budget;
-  int chosen = INT_MAX;          // lane x < budget holds the x-th chosen id
-  if (budget >= u.n_free) {
-    // dense regime: every candidate is selected (assembled below)
-  } else if (budget > 0 && budget <= 32) {
-    float m = -1.f;
-    for (int b = lo + lane; b < hi; b += 32) m = fmaxf(m, rq[b]);
-    const float t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m, lane), budget - 1);
-    int cnt = 0;
-    bool overflow = false;
-    for (int base = lo; base < hi; base += 32) {
-      const int b = base + lane;
-      const float r = b < hi ? rq[b] : -2.f;
-      const bool f = r >= t0;
-      const unsigned mask = __ballot_sync(0xffffffffu, f);
-      const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
-      if (f && pos < kListCap - kOutCap) { lkey[pos] = r; lid[pos] = b; }
-      cnt += __popc(mask);
-    }
-    overflow = cnt > kListCap - kOutCap;
-    __syncwarp();
-    if (!overflow) {
-      // rank every listed candidate against the whole list (no dependent
-      // chains), keep rank < budget; the list is in id order, so a ballot
-      // compaction emits the chosen ids already ascending.
-      int taken = 0;
-      for (int base = 0; base < cnt; base += 32) {
-        const int x = base + lane;
-        bool keep = false;
-        if (x < cnt) {
-          const float rk = lkey[x];
-          const int bk = lid[x];
-          int rank = 0;
-          for (int f = 0; f < cnt; ++f) rank += better(lkey[f], lid[f], rk, bk) ? 1 : 0;
-          keep = rank < budget;
-        }
-        const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        const int pos = taken + __popc(mask & ((1u << lane) - 1u));
-        if (keep) lid[kListCap - kOutCap + pos] = lid[x];   // staging area at the list tail
-        taken += __popc(mask);
-      }
-      __syncwarp();
-      chosen = lane < budget ? lid[kListCap - kOutCap + lane] : INT_MAX;
-      __syncwarp();
-    } else {
-      float pv = INFINITY;
-      int pb = -1;
-      for (int it = 0; it < budget; ++it) {
-        float bv = -1.f;
-        int bb = -1;
-        for (int b = lo + lane; b < hi; b += 32) {
-          const float r = rq[b];
-          if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
-        }
-        warp_best_after(bv, bb);
-        if (lane == it) chosen = bb;
-        pv = bv;
-        pb = bb;
-      }
-      chosen = warp_sort_asc(chosen, lane);
-    }
-  } else if (budget > 32) {
-    // rare large budgets: iterative order-statistics over the whole range
-    float pv = INFINITY;
-    int pb = -1;
-    for (int it = 0; it < budget; ++it) {
-      float bv = -1.f;
-      int bb = -1;
-      for (int b = lo + lane; b < hi; b += 32) {
-        const float r = rq[b];
-        if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
-      }
-      warp_best_after(bv, bb);
-      if (lane == 0) lid[it] = bb;  // staged in smem, sorted below
-      pv = bv;
-      pb = bb;
-    }
-    __syncwarp();
-    // insertion-free ascending order: ids are distinct, rank = #smaller
-    for (int x = lane; x < budget; x += 32) {
-      const int me = lid[x];
-      int rank = 0;
-      for (int y = 0; y < budget; ++y) rank += lid[y] < me;
-      lkey[rank] = __int_as_float(me);
-    }
-    __syncwarp();
-  }
-  // assemble: [0, lo) + chosen + [local_lo, qb]
-  const int n_ch = budget >= u.n_free ? (int)u.n_free : budget;
-  const int n_loc = (int)(u.qb + 1 - u.local_lo);
-  for (int x = lane; x < max_sel; x += 32) {
-    int id = -1;
-    if (x < lo) id = x;
-    else if (x < lo + n_ch) {
-      const int c = x - lo;
-      if (budget >= u.n_free) id = lo + c;
-      else if (budget <= 32) id = -2;  // filled from registers below
-      else id = __float_as_int(lkey[c]);
-    } else if (x < lo + n_ch + n_loc) id = (int)u.local_lo + (x - lo - n_ch);
-    if (id != -2) {
-      out[x] = id;
-      if (osc) osc[x] = id >= 0 ? (double)rq[id] : 0.0;
-    }
-  }
-  if (budget < u.n_free && budget > 0 && budget <= 32) {
-    // lane c holds the c-th smallest chosen id
-    if (lane < budget) {
-      out[lo + lane] = chosen;
-      if (osc) osc[lo + lane] = (double)rq[chosen];
-    }
-  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -543,7 +364,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       int64_t t0;
       int grp;
       unit_coords(p, u, &t0, &grp);
-      const UnitSel us = unit_sel(p, t0);
+      const UnitSel us = unit_sel(t0, p.m, p.top_k, p.n_init, p.n_local, p.consume);
       const float* rbuf = p.rbuf + ((int64_t)blockIdx.x * 2 + (ucount & 1)) * kQ * p.nb_cap;
       mbar_wait(rb_full + (ucount & 1), (ucount >> 1) & 1);
       for (int qi = tw; qi < kQ; qi += kTopkWarps) {

@@ -1,0 +1,108 @@
+"""Batched single-token decode over S sequences (BASELINE configs[3]).
+
+The reference decodes one sequence at a time by calling two_stage_attention with
+n = 1 after appending the new token (model.py:434-444; specdec.py:717-718).  On
+the B200 a decode step of S sequences for one layer is one batched call
+(`infllm2_decode_step`): append + incremental kernel-mean re-sync, split-K
+stage-1 on the tensor cores, block scores, top-k, stage-2 — five launches for
+all sequences, no host synchronisation.  Sequences stay independent (each has
+its own cache); a multi-GPU deployment partitions sequences across ranks with
+no collective.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from .errors import ValidationError
+from .sparse import BlockizedLayerCache, SparseAttentionConfig, _ptr, _stream
+
+
+class DecodeBatch:
+    """One layer's caches of S sequences, stepped together."""
+
+    def __init__(self, layers: Sequence[BlockizedLayerCache], config: SparseAttentionConfig):
+        if not layers:
+            raise ValidationError("empty decode batch")
+        l0 = layers[0]
+        for l in layers:
+            if (l.n_kv_heads, l.head_dim, l.device) != (l0.n_kv_heads, l0.head_dim, l0.device):
+                raise ValidationError("decode batch caches must share head geometry and device")
+        self.layers = list(layers)
+        self.config = config
+        self.device = l0.device
+        self._table: Optional[torch.Tensor] = None
+        self._sig = None
+        self._lib = _lib.load()
+
+    def _signature(self):
+        return tuple((l._k.data_ptr(), l._v.data_ptr(), l._cap, l._fine.data_ptr(), l._coarse.data_ptr(), l.length)
+                     for l in self.layers)
+
+    def _ensure(self) -> None:
+        for l in self.layers:
+            l._reserve(l.length + 1)
+        sig = self._signature()
+        if sig == self._sig:
+            return
+        n = len(self.layers)
+        descs = (_lib.SeqDesc * n)()
+        lens = (ctypes.c_int64 * n)()
+        for i, l in enumerate(self.layers):
+            descs[i] = _lib.SeqDesc(l._k.data_ptr(), l._v.data_ptr(), l._cap, l._fine.data_ptr(), l._fine_hi.data_ptr(),
+                                    l._fine_lo.data_ptr(), l._fine.shape[1], l._coarse.data_ptr(), l._coarse.shape[1])
+            lens[i] = l.length
+        nbytes = self._lib.infllm2_decode_table_bytes(n)
+        if self._table is None or self._table.numel() < nbytes:
+            self._table = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        _lib.check(self._lib.infllm2_decode_table_build(descs, lens, n, self.layers[0].n_kv_heads,
+                                                        self.layers[0].head_dim, self._table.data_ptr(),
+                                                        _stream(self.device)), "decode table")
+        self._sig = sig
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, *, return_selection: bool = False,
+             return_lse: bool = False, out_dtype: Optional[torch.dtype] = None):
+        """Append (S, HKV, D) k_new/v_new and attend (S, HQ, D) q for every sequence."""
+        n = len(self.layers)
+        l0 = self.layers[0]
+        hq, d = q.shape[1], q.shape[2]
+        if q.shape[0] != n or k_new.shape != (n, l0.n_kv_heads, l0.head_dim) or v_new.shape != k_new.shape:
+            raise ValidationError("decode step shapes must be q (S, HQ, D), k/v (S, HKV, D)")
+        if hq % l0.n_kv_heads:
+            raise ValidationError("query heads not divisible by KV heads")
+        self._ensure()
+        dev = self.device
+        qb = q.to(device=dev, dtype=torch.bfloat16).contiguous()
+        kb = k_new.to(device=dev, dtype=torch.bfloat16).contiguous()
+        vb = v_new.to(device=dev, dtype=torch.bfloat16).contiguous()
+        out_dtype = out_dtype or (q.dtype if q.dtype in (torch.float32, torch.bfloat16) else torch.bfloat16)
+        geom = self.config.geometry()
+        smax = self.config.max_selected
+        sel = torch.empty((n, l0.n_kv_heads, smax), dtype=torch.int32, device=dev)
+        out = torch.empty((n, hq, d), dtype=out_dtype, device=dev)
+        lse = torch.empty((n, hq), dtype=torch.float32, device=dev) if return_lse else None
+        max_len = max(l.length for l in self.layers) + 1
+        ws_bytes = self._lib.infllm2_decode_workspace_bytes(ctypes.byref(geom), n, l0.n_kv_heads, max_len)
+        from .sparse import _workspace
+        ws = _workspace(dev, ws_bytes)
+        flags = _lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0
+        _lib.check(self._lib.infllm2_decode_step(
+            ctypes.byref(geom), self._table.data_ptr(), n, max_len, hq, l0.n_kv_heads, d, _ptr(qb), _ptr(kb),
+            _ptr(vb), _ptr(sel), _ptr(out), _ptr(lse), _ptr(ws), ws.numel(), flags, _stream(dev)), "decode step")
+        for l in self.layers:           # the device advanced every length by one
+            l.length += 1
+            l._nk_valid = l.length // self.config.kernel_stride
+            l._nc_valid = l.length // self.config.coarse_stride
+        self._sig = self._signature()
+        if return_selection or return_lse:
+            res = (out,)
+            if return_selection:
+                res += (sel,)
+            if return_lse:
+                res += (lse,)
+            return res
+        return out

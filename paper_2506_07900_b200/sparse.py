@@ -204,8 +204,10 @@ class BlockizedLayerCache:
         cap = max(need, 2 * self._cap, 64)
         h, d, dev = self.n_kv_heads, self.head_dim, self.device
         s, sc = self.config.kernel_stride, self.config.coarse_stride
-        k = torch.empty((h, cap, d), dtype=torch.bfloat16, device=dev)
-        v = torch.empty_like(k)
+        # zero-filled: rows past the length are read (P = 0) by the decode
+        # stage-2 tiles, so they must be finite
+        k = torch.zeros((h, cap, d), dtype=torch.bfloat16, device=dev)
+        v = torch.zeros_like(k)
         fine = torch.empty((h, cap // s + 1, d), dtype=torch.float32, device=dev)
         hi = torch.empty((h, cap // s + 1, d), dtype=torch.bfloat16, device=dev)
         lo = torch.empty_like(hi)
