@@ -64,9 +64,32 @@ class DecodeBatch:
                                                         _stream(self.device)), "decode table")
         self._sig = sig
 
+    def reserve(self, extra_tokens: int) -> None:
+        """Preallocate room for `extra_tokens` more decode steps (no reallocation,
+        hence no table rebuild, while they run — required for graph capture)."""
+        for l in self.layers:
+            l._reserve(l.length + extra_tokens)
+        self._ensure()
+
+    def advance(self, n: int = 1) -> None:
+        """Host bookkeeping for `n` steps replayed from a captured graph."""
+        for l in self.layers:
+            l.length += n
+            l._nk_valid = l.length // self.config.kernel_stride
+            l._nc_valid = l.length // self.config.coarse_stride
+        self._sig = self._signature()
+
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, *, return_selection: bool = False,
-             return_lse: bool = False, out_dtype: Optional[torch.dtype] = None):
-        """Append (S, HKV, D) k_new/v_new and attend (S, HQ, D) q for every sequence."""
+             return_lse: bool = False, out_dtype: Optional[torch.dtype] = None, max_len: Optional[int] = None,
+             bookkeep: bool = True):
+        """Append (S, HKV, D) k_new/v_new and attend (S, HQ, D) q for every sequence.
+
+        `max_len` fixes the length bound that sizes the split-K grid and the
+        workspace (default: current max + 1).  Passing a fixed bound (e.g. the
+        reserved capacity) makes the launches identical from step to step, so
+        a whole multi-layer decode step can be captured in a CUDA graph and
+        replayed (`bookkeep=False` inside the capture, then `advance()`).
+        """
         n = len(self.layers)
         l0 = self.layers[0]
         hq, d = q.shape[1], q.shape[2]
@@ -85,7 +108,10 @@ class DecodeBatch:
         sel = torch.empty((n, l0.n_kv_heads, smax), dtype=torch.int32, device=dev)
         out = torch.empty((n, hq, d), dtype=out_dtype, device=dev)
         lse = torch.empty((n, hq), dtype=torch.float32, device=dev) if return_lse else None
-        max_len = max(l.length for l in self.layers) + 1
+        cur = max(l.length for l in self.layers) + 1
+        max_len = cur if max_len is None else int(max_len)
+        if max_len < cur:
+            raise ValidationError("max_len below the longest sequence")
         ws_bytes = self._lib.infllm2_decode_workspace_bytes(ctypes.byref(geom), n, l0.n_kv_heads, max_len)
         from .sparse import _workspace
         ws = _workspace(dev, ws_bytes)
@@ -93,11 +119,8 @@ class DecodeBatch:
         _lib.check(self._lib.infllm2_decode_step(
             ctypes.byref(geom), self._table.data_ptr(), n, max_len, hq, l0.n_kv_heads, d, _ptr(qb), _ptr(kb),
             _ptr(vb), _ptr(sel), _ptr(out), _ptr(lse), _ptr(ws), ws.numel(), flags, _stream(dev)), "decode step")
-        for l in self.layers:           # the device advanced every length by one
-            l.length += 1
-            l._nk_valid = l.length // self.config.kernel_stride
-            l._nc_valid = l.length // self.config.coarse_stride
-        self._sig = self._signature()
+        if bookkeep:                    # the device advanced every length by one
+            self.advance(1)
         if return_selection or return_lse:
             res = (out,)
             if return_selection:
