@@ -72,7 +72,21 @@ struct Params {
   const CUtensorMap* kv_maps;
   int map_stride;
   const int64_t* seq_len;
+  // split-K (decode): each work unit is (item, part) covering tiles
+  // [part*split, (part+1)*split); partial O^T (unnormalised), max and row sum go
+  // to part_o / part_ml and attend_combine_kernel merges them.  split == 0: off.
+  int split;
+  int64_t parts;
+  float* part_o;      // [item][part][16][128]
+  float* part_ml;     // [item][part][16][2]
 };
+
+__device__ __forceinline__ void tile_range(const Params& p, int64_t part, int tiles, int* c0, int* c1) {
+  if (p.split == 0) { *c0 = 0; *c1 = tiles; return; }
+  const int64_t a = part * p.split, b = a + p.split;
+  *c0 = (int)(a < tiles ? a : tiles);
+  *c1 = (int)(b < tiles ? b : tiles);
+}
 
 __device__ __forceinline__ int64_t item_pos(const Params& p, int64_t i) {
   return p.seq_len ? p.seq_len[i] - 1 : p.start + i;
@@ -148,14 +162,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;       // cols [0,32): S slots, [32,64): O slots
-  const int64_t items = p.n * p.hkv;
+  const int64_t items = p.n * p.hkv * p.parts;   // work units (item, part)
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      const int64_t item = w / p.parts, part = w - item * p.parts;
       const int64_t i = item / p.hkv;
       const int grp = (int)(item - i * p.hkv);
       const int64_t pos = item_pos(p, i);
@@ -163,7 +178,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const CUtensorMap* mv = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i + 1 : &tm_v;
       const SelRow sr = load_sel(p, item, pos, lane);
       const int nb = sr.nb;
+      int c0, c1;
+      tile_range(p, part, (nb + 1) / 2, &c0, &c1);
+      if (c0 >= c1) continue;
       const int qb = it & 1;
+      ++it;
       if (lane == 0) {
         mbar_wait(q_empty + qb, ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(q_full + qb, kQBytes);
@@ -171,7 +190,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         tma_load_3d(qd, &tm_q, q_full + qb, 0, grp * kG, (int)i);
         tma_load_3d(qd + kQBytes / 2, &tm_q, q_full + qb, 64, grp * kG, (int)i);
       }
-      for (int c = 0; c * 2 < nb; ++c) {
+      for (int c = c0; c < c1; ++c) {
         const int nt = (nb - 2 * c) >= 2 ? 2 : 1;
         const int b0 = sr.get(2 * c);
         const int b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
@@ -202,12 +221,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     int sslot = 0, pbuf = 0;
     uint32_t s_ph[2] = {0, 0}, p_ph[2] = {0, 0};
     int it = 0;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      const int64_t item = w / p.parts, part = w - item * p.parts;
       const int64_t i = item / p.hkv;
       const int64_t pos = item_pos(p, i);
       const SelRow sr = load_sel(p, item, pos, lane);
       const int nb = sr.nb;
-      const int tiles = (nb + 1) / 2;
+      int c0, c1;
+      tile_range(p, part, (nb + 1) / 2, &c0, &c1);
+      if (c0 >= c1) continue;
       const int qb = it & 1, ob = it & 1;
       mbar_wait(q_full + qb, (it >> 1) & 1);
       const uint32_t q_addr = smem_u32(smem + Smem::q + qb * kQBytes);
@@ -232,24 +254,24 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(s_empty + sslot, s_ph[sslot] ^ 1);
       s_ph[sslot] ^= 1;
       issue_qk(stage_c, sslot);
-      for (int c = 0; c < tiles; ++c) {
+      for (int c = c0; c < c1; ++c) {
         const int cur_stage = stage_c, cur_slot = sslot;
         if (++stage_c == kStages) { stage_c = 0; phase_c ^= 1; }
         sslot ^= 1;
-        if (c + 1 < tiles) {
+        if (c + 1 < c1) {
           mbar_wait(kv_full + stage_c, phase_c);
           mbar_wait(s_empty + sslot, s_ph[sslot] ^ 1);
           s_ph[sslot] ^= 1;
           issue_qk(stage_c, sslot);
         }
-        if (c == tiles - 1) {
+        if (c == c1 - 1) {
           if (elect_one()) umma_commit(q_empty + qb);
           __syncwarp();
         }
         // PV of tile c once its P is in shared memory
         mbar_wait(p_full + pbuf, p_ph[pbuf]);
         p_ph[pbuf] ^= 1;
-        if (c == 0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
+        if (c == c0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
         if (elect_one()) {
@@ -258,13 +280,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           for (int k = 0; k < ksteps; ++k) {
             const uint64_t vdesc = sdesc_mn_sw128(v_addr + k * 2048, kHalfBytes, 1024);
             umma_f16_ss(tmem + 32 + ob * kG, vdesc, sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv,
-                        (c > 0 || k > 0) ? 1u : 0u);
+                        (c > c0 || k > 0) ? 1u : 0u);
             umma_f16_ss(tmem + 32 + ob * kG, vdesc, sdesc_interleave(p_addr + kPHalf + k * 512, 256, 128),
                         idesc_pv, 1u);
           }
           umma_commit(kv_empty + cur_stage);
           umma_commit(p_empty + pbuf);
-          if (c == tiles - 1) umma_commit(o_full + ob);
+          if (c == c1 - 1) umma_commit(o_full + ob);
         }
         __syncwarp();
         pbuf ^= 1;
@@ -272,6 +294,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       stage = stage_c;
       phase = phase_c;
+      ++it;
     }
   } else if (warp < 6) {
     // -------------------------------------------------------------- softmax
@@ -282,17 +305,20 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     int sslot = 0, pbuf = 0;
     uint32_t s_ph[2] = {0, 0}, p_ph[2] = {0, 0};
     int it = 0;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      const int64_t item = w / p.parts, part = w - item * p.parts;
       const int64_t i = item / p.hkv;
       const int64_t pos = item_pos(p, i);
       const SelRow sr = load_sel(p, item, pos, lane);
       const int nb = sr.nb;
-      const int tiles = (nb + 1) / 2;
+      int c0, c1;
+      tile_range(p, part, (nb + 1) / 2, &c0, &c1);
+      if (c0 >= c1) continue;
       const int ob = it & 1;
       float mrun[kG], lsum[kG];
 #pragma unroll
       for (int h = 0; h < kG; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; }
-      for (int c = 0; c < tiles; ++c) {
+      for (int c = c0; c < c1; ++c) {
         mbar_wait(s_full + sslot, s_ph[sslot]);
         s_ph[sslot] ^= 1;
         tc_fence_after();
@@ -310,8 +336,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 #pragma unroll
         for (int h = 0; h < kG; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
         // running max: exact on the first tile, rescale later only if z > M + 8
-        bool need = (c == 0);
-        if (c > 0) {
+        bool need = (c == c0);
+        if (c > c0) {
           bool over = false;
 #pragma unroll
           for (int h = 0; h < kG; ++h) over |= z[h] > mrun[h] + 8.f;
@@ -343,12 +369,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const float tm = fmaxf(fmaxf(red[h], red[16 + h]), fmaxf(red[32 + h], red[48 + h]));
             const float mnew = fmaxf(mrun[h], tm);
             corr[h] = (mrun[h] == -INFINITY) ? 1.f : ex2(mrun[h] - mnew);
-            any_corr |= (c > 0) && (corr[h] != 1.f);
+            any_corr |= (c > c0) && (corr[h] != 1.f);
             lsum[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
             mrun[h] = mnew;
           }
           named_bar_sync(2, 128);
-          if (c > 0 && any_corr) {
+          if (c > c0 && any_corr) {
             // rescale O^T (this thread owns d lane == row): wait for PV(c-1),
             // whose completion is the next phase of p_empty[buffer of c-1]
             mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
@@ -408,6 +434,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(st_full + ob);
+      ++it;
     }
   } else {
     // -------------------------------------------------------------- epilogue
@@ -415,11 +442,25 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     const int d = quad * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     int it = 0;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      const int64_t item = w / p.parts, part = w - item * p.parts;
       const int64_t i = item / p.hkv;
       const int grp = (int)(item - i * p.hkv);
+      if (p.split) {
+        const SelRow sr = load_sel(p, item, item_pos(p, i), lane);
+        int c0, c1;
+        tile_range(p, part, (sr.nb + 1) / 2, &c0, &c1);
+        if (c0 >= c1) {   // empty part: neutral partial for the combine
+          if (quad == 0 && lane < kG) {
+            p.part_ml[(w * kG + lane) * 2] = -INFINITY;
+            p.part_ml[(w * kG + lane) * 2 + 1] = 0.f;
+          }
+          continue;
+        }
+      }
       const int ob = it & 1;
       const uint32_t par = (it >> 1) & 1;
+      ++it;
       mbar_wait(o_full + ob, par);
       mbar_wait(st_full + ob, par);
       tc_fence_after();
@@ -433,6 +474,21 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       float l[kG];
 #pragma unroll
       for (int h = 0; h < kG; ++h) l[h] = st[h] + st[16 + h] + st[32 + h] + st[48 + h];
+      if (p.split) {
+        float* po = p.part_o + w * (kG * kD) + d;
+#pragma unroll
+        for (int h = 0; h < kG; ++h) po[h * kD] = o[h];
+        if (quad == 0 && lane < kG) {
+          float lh = l[0];
+#pragma unroll
+          for (int h = 1; h < kG; ++h) lh = (lane == h) ? l[h] : lh;
+          p.part_ml[(w * kG + lane) * 2] = st[64 + lane];
+          p.part_ml[(w * kG + lane) * 2 + 1] = lh;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(st_empty + ob);
+        continue;
+      }
       const int64_t obase = (i * p.hq + (int64_t)grp * kG) * kD + d;
       if (p.out_f32) {
         float* out = static_cast<float*>(p.out);
@@ -459,14 +515,48 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   if (warp == 1) tmem_dealloc<64>(tmem);
 }
 
+// Merge split-K partials of each (row, group) item: O = sum_p O_p 2^(m_p - M) /
+// sum_p l_p 2^(m_p - M).  One CTA per item, thread = head dim d.
+__global__ void __launch_bounds__(kD) attend_combine_kernel(const float* __restrict__ part_o,
+                                                            const float* __restrict__ part_ml, int64_t parts, int hq,
+                                                            int hkv, void* out, int out_f32, float* lse) {
+  const int64_t item = blockIdx.x;
+  const int64_t i = item / hkv;
+  const int grp = (int)(item - i * hkv);
+  const int d = threadIdx.x;
+  for (int h = 0; h < kG; ++h) {
+    float M = -INFINITY;
+    for (int64_t q = 0; q < parts; ++q) M = fmaxf(M, part_ml[((item * parts + q) * kG + h) * 2]);
+    float L = 0.f, acc = 0.f;
+    for (int64_t q = 0; q < parts; ++q) {
+      const float m = part_ml[((item * parts + q) * kG + h) * 2];
+      if (m == -INFINITY) continue;
+      const float w = ex2(m - M);
+      L += part_ml[((item * parts + q) * kG + h) * 2 + 1] * w;
+      acc += part_o[(item * parts + q) * (kG * kD) + h * kD + d] * w;
+    }
+    const int64_t o = (i * hq + (int64_t)grp * kG + h) * kD + d;
+    if (out_f32)
+      static_cast<float*>(out)[o] = acc / L;
+    else
+      static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(acc / L);
+    if (lse && d == 0) lse[i * hq + grp * kG + h] = (M + log2f(L)) * 0.6931471805599453f;
+  }
+}
+
 }  // namespace
+
+size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel) {
+  const int64_t parts = (max_sel + 1) / 2;
+  return (size_t)n_seq * hkv * parts * (kG * kD + 2 * kG) * sizeof(float);
+}
 
 // Batched decode: one query row per sequence, per-sequence K/V tensor maps in
 // device memory (maps[stride*s + 0] = K, + 1 = V), positions seq_len[s] - 1.
 cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
                                     const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
                                     const int32_t* selection, void* out, int out_f32, float* lse,
-                                    cudaStream_t stream) {
+                                    float* split_ws, cudaStream_t stream) {
   Params p;
   p.n = n_seq;
   p.start = 0;
@@ -480,6 +570,11 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   p.kv_maps = kv_maps;
   p.map_stride = map_stride;
   p.seq_len = seq_len;
+  // split-K: one 2-block tile per CTA so n_seq*hkv*10 CTAs share the gather
+  p.split = split_ws ? 1 : 0;
+  p.parts = split_ws ? (max_sel + 1) / 2 : 1;
+  p.part_o = split_ws;
+  p.part_ml = split_ws ? split_ws + n_seq * hkv * p.parts * (kG * kD) : nullptr;
   CUtensorMap tq;
   const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
   const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
@@ -488,12 +583,17 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   const size_t smem = Smem::total + 1024;
   cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t items = n_seq * hkv;
+  const int64_t items = n_seq * hkv * p.parts;
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(items < sms ? items : sms);
   count_launch();
   attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tq, tq, p);
+  if (split_ws) {
+    count_launch();
+    attend_combine_kernel<<<(int)(n_seq * hkv), kD, 0, stream>>>(p.part_o, p.part_ml, p.parts, hq, hkv, out,
+                                                                 out_f32, lse);
+  }
   return cudaGetLastError();
 }
 
@@ -520,6 +620,10 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.kv_maps = nullptr;
   p.map_stride = 0;
   p.seq_len = nullptr;
+  p.split = 0;
+  p.parts = 1;
+  p.part_o = nullptr;
+  p.part_ml = nullptr;
   CUtensorMap tq, tk, tv;
   {
     const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)cs.n};

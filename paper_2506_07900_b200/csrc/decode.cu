@@ -28,7 +28,8 @@ namespace infllm2 {
 cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
                                     const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
                                     const int32_t* selection, void* out, int out_f32, float* lse,
-                                    cudaStream_t stream);
+                                    float* split_ws, cudaStream_t stream);
+size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel);
 
 namespace {
 
@@ -39,7 +40,7 @@ constexpr int kD = 128;
 constexpr int kS = 16;             // fine stride
 constexpr int kP = 32;             // kernel size
 constexpr int kTile = 128;         // kernels per MMA tile
-constexpr int kChunk = 256;        // kernels per stage-1 work item
+constexpr int kChunk = 1024;       // kernels per stage-1 work item (8 tiles)
 constexpr int kBlkChunk = 64;      // blocks per scores work item
 constexpr int kMaps = 4;           // per sequence: K, V, hi, lo
 
@@ -335,16 +336,28 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
           }
         }
       }
+      // (max, sum) per head: warp butterfly, then the 4 warps through smem
 #pragma unroll
-      for (int h = 0; h < kG; ++h) { red_m[h * 128 + etid] = m[h]; red_s[h * 128 + etid] = sm[h]; }
+      for (int h = 0; h < kG; ++h) {
+        float mm = m[h], ss = sm[h];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const float om = __shfl_xor_sync(0xffffffffu, mm, off);
+          const float os = __shfl_xor_sync(0xffffffffu, ss, off);
+          const float nm = fmaxf(mm, om);
+          ss = (mm == -INFINITY ? 0.f : ss * ex2(mm - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
+          mm = nm;
+        }
+        if (lane == 0) { red_m[h * 4 + quad] = mm; red_s[h * 4 + quad] = ss; }
+      }
       named_bar_sync(1, 128);
       if (etid < kG) {
         float M = -INFINITY;
-        for (int x = 0; x < 128; ++x) M = fmaxf(M, red_m[etid * 128 + x]);
+        for (int x = 0; x < 4; ++x) M = fmaxf(M, red_m[etid * 4 + x]);
         float S = 0.f;
-        for (int x = 0; x < 128; ++x) {
-          const float mm = red_m[etid * 128 + x];
-          if (mm != -INFINITY) S += red_s[etid * 128 + x] * ex2(mm - M);
+        for (int x = 0; x < 4; ++x) {
+          const float mm = red_m[etid * 4 + x];
+          if (mm != -INFINITY) S += red_s[etid * 4 + x] * ex2(mm - M);
         }
         ps[2 * etid] = M;
         ps[2 * etid + 1] = S;
@@ -505,6 +518,7 @@ struct DecodeWs {
   float* zbuf;
   float* pstat;
   float* rbuf;
+  float* split;
   int64_t nchunk, nbchunk, zstride, nb_cap;
   size_t bytes;
 };
@@ -524,6 +538,8 @@ static DecodeWs decode_ws_layout(const infllm2_geometry& g, int n_seq, int hkv, 
   off += align_up(sizeof(float) * n_seq * hkv * w.nchunk * 2 * kG, 256);
   w.rbuf = reinterpret_cast<float*>(b + off);
   off += align_up(sizeof(float) * n_seq * hkv * w.nb_cap, 256);
+  w.split = reinterpret_cast<float*>(b + off);
+  off += align_up(attend_split_workspace(n_seq, hkv, infllm2_max_selected(&g)), 256);
   w.bytes = off;
   return w;
 }
@@ -609,7 +625,7 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   decode_topk_kernel<<<n_seq * hkv, 32, 0, stream>>>(tp);
   // 5. stage 2
   cudaError_t e = launch_attend_tc_decode(hq, hkv, max_sel, n_seq, q, tvd.maps, kMaps, tvd.len, selection, out,
-                                          out_f32, lse, stream);
+                                          out_f32, lse, w.split, stream);
   if (e != cudaSuccess) return INFLLM2_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? INFLLM2_OK : INFLLM2_ERR_CUDA;
 }

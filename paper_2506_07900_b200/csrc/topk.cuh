@@ -89,18 +89,33 @@ __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, i
     // dense regime: every candidate is selected (assembled below)
   } else if (budget > 0 && budget <= 32) {
     float m = -1.f;
-    for (int b = lo + lane; b < hi; b += 32) m = fmaxf(m, rq[b]);
+    {
+      int b = lo + lane;
+      for (; b + 96 < hi; b += 128) {
+        const float a0 = rq[b], a1 = rq[b + 32], a2 = rq[b + 64], a3 = rq[b + 96];
+        m = fmaxf(m, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
+      }
+      for (; b < hi; b += 32) m = fmaxf(m, rq[b]);
+    }
     const float t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m, lane), budget - 1);
     int cnt = 0;
     bool overflow = false;
-    for (int base = lo; base < hi; base += 32) {
-      const int b = base + lane;
-      const float r = b < hi ? rq[b] : -2.f;
-      const bool f = r >= t0;
-      const unsigned mask = __ballot_sync(0xffffffffu, f);
-      const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
-      if (f && pos < kListCap - kOutCap) { lkey[pos] = r; lid[pos] = b; }
-      cnt += __popc(mask);
+    for (int base = lo; base < hi; base += 128) {
+      float r4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = base + 32 * u + lane;
+        r4[u] = b < hi ? rq[b] : -2.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = base + 32 * u + lane;
+        const bool f = r4[u] >= t0;
+        const unsigned mask = __ballot_sync(0xffffffffu, f);
+        const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
+        if (f && pos < kListCap - kOutCap) { lkey[pos] = r4[u]; lid[pos] = b; }
+        cnt += __popc(mask);
+      }
     }
     overflow = cnt > kListCap - kOutCap;
     __syncwarp();
