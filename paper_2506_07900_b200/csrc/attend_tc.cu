@@ -182,9 +182,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
       if (c0 >= c1) continue;
       const int qb = it & 1;
+      const uint32_t q_par = ((it >> 1) & 1) ^ 1;
       ++it;
       if (lane == 0) {
-        mbar_wait(q_empty + qb, ((it >> 1) & 1) ^ 1);
+        mbar_wait(q_empty + qb, q_par);
         mbar_arrive_expect_tx(q_full + qb, kQBytes);
         uint8_t* qd = smem + Smem::q + qb * kQBytes;
         tma_load_3d(qd, &tm_q, q_full + qb, 0, grp * kG, (int)i);
