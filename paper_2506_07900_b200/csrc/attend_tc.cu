@@ -517,31 +517,44 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 }
 
 // Merge split-K partials of each (row, group) item: O = sum_p O_p 2^(m_p - M) /
-// sum_p l_p 2^(m_p - M).  One CTA per item, thread = head dim d.
-__global__ void __launch_bounds__(kD) attend_combine_kernel(const float* __restrict__ part_o,
-                                                            const float* __restrict__ part_ml, int64_t parts, int hq,
-                                                            int hkv, void* out, int out_f32, float* lse) {
+// sum_p l_p 2^(m_p - M).  One CTA per item; part weights computed once into
+// shared memory, then thread (h, d-slice) streams the parts with independent loads.
+__global__ void __launch_bounds__(512) attend_combine_kernel(const float* __restrict__ part_o,
+                                                             const float* __restrict__ part_ml, int64_t parts, int hq,
+                                                             int hkv, void* out, int out_f32, float* lse) {
+  __shared__ float wgt[16 * kG];   // [part][h], parts <= 16
+  __shared__ float inv_l[kG];
   const int64_t item = blockIdx.x;
   const int64_t i = item / hkv;
   const int grp = (int)(item - i * hkv);
-  const int d = threadIdx.x;
-  for (int h = 0; h < kG; ++h) {
+  const int t = threadIdx.x;
+  if (t < kG) {
     float M = -INFINITY;
-    for (int64_t q = 0; q < parts; ++q) M = fmaxf(M, part_ml[((item * parts + q) * kG + h) * 2]);
-    float L = 0.f, acc = 0.f;
+    for (int64_t q = 0; q < parts; ++q) M = fmaxf(M, part_ml[((item * parts + q) * kG + t) * 2]);
+    float L = 0.f;
     for (int64_t q = 0; q < parts; ++q) {
-      const float m = part_ml[((item * parts + q) * kG + h) * 2];
-      if (m == -INFINITY) continue;
-      const float w = ex2(m - M);
-      L += part_ml[((item * parts + q) * kG + h) * 2 + 1] * w;
-      acc += part_o[(item * parts + q) * (kG * kD) + h * kD + d] * w;
+      const float m = part_ml[((item * parts + q) * kG + t) * 2];
+      const float w = m == -INFINITY ? 0.f : ex2(m - M);
+      wgt[q * kG + t] = w;
+      L += part_ml[((item * parts + q) * kG + t) * 2 + 1] * w;
     }
-    const int64_t o = (i * hq + (int64_t)grp * kG + h) * kD + d;
+    inv_l[t] = 1.f / L;
+    if (lse) lse[i * hq + grp * kG + t] = (M + log2f(L)) * 0.6931471805599453f;
+  }
+  __syncthreads();
+  for (int x = t; x < kG * kD; x += blockDim.x) {
+    const int h = x / kD;
+    float acc = 0.f;
+#pragma unroll 4
+    for (int64_t q = 0; q < parts; ++q) {
+      const float w = wgt[q * kG + h];
+      if (w != 0.f) acc += part_o[(item * parts + q) * (kG * kD) + x] * w;
+    }
+    const int64_t o = (i * hq + (int64_t)grp * kG) * kD + x;
     if (out_f32)
-      static_cast<float*>(out)[o] = acc / L;
+      static_cast<float*>(out)[o] = acc * inv_l[h];
     else
-      static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(acc / L);
-    if (lse && d == 0) lse[i * hq + grp * kG + h] = (M + log2f(L)) * 0.6931471805599453f;
+      static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(acc * inv_l[h]);
   }
 }
 
@@ -592,8 +605,8 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tq, tq, p);
   if (split_ws) {
     count_launch();
-    attend_combine_kernel<<<(int)(n_seq * hkv), kD, 0, stream>>>(p.part_o, p.part_ml, p.parts, hq, hkv, out,
-                                                                 out_f32, lse);
+    attend_combine_kernel<<<(int)(n_seq * hkv), 512, 0, stream>>>(p.part_o, p.part_ml, p.parts, hq, hkv, out,
+                                                                  out_f32, lse);
   }
   return cudaGetLastError();
 }

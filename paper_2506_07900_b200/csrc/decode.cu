@@ -88,9 +88,15 @@ __device__ void window_mean(const __nv_bfloat16* kg, int64_t cap, int d, int64_t
   int64_t r1 = r0 + kP;
   if (r1 > length) r1 = length;
   const __nv_bfloat16* src = kg + r0 * d + e;
-  double acc = (double)__bfloat162float(src[0]);
-  for (int64_t r = 1; r < r1 - r0; ++r) acc += (double)__bfloat162float(src[r * d]);
-  *out_mean = __double2float_rn(acc / (double)(r1 - r0));
+  const int w = (int)(r1 - r0);
+  float x[kP];
+#pragma unroll
+  for (int r = 0; r < kP; ++r) x[r] = r < w ? __bfloat162float(src[(int64_t)r * d]) : 0.f;   // loads in flight together
+  double acc = (double)x[0];
+#pragma unroll
+  for (int r = 1; r < kP; ++r)
+    if (r < w) acc += (double)x[r];                                                           // sequential, as numpy
+  *out_mean = __double2float_rn(acc / (double)w);
 }
 
 __global__ void __launch_bounds__(256) decode_append_compress_kernel(void* table, int n_seq, int hkv, int d,
@@ -398,16 +404,27 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
   const int64_t b0 = bc * kBlkChunk;
   if (b0 >= n_cand) return;
   const int64_t b1 = b0 + kBlkChunk < n_cand ? b0 + kBlkChunk : n_cand;
-  if (threadIdx.x < kG) {
+  {
+    // per-head LSE from the chunk partials: 16 lanes per head, shuffle merge
     const float* ps = p.pstat + sg * p.nchunk * (2 * kG);
-    float M = -INFINITY;
-    for (int64_t c = 0; c < p.nchunk; ++c) M = fmaxf(M, ps[c * 2 * kG + 2 * threadIdx.x]);
-    float S = 0.f;
-    for (int64_t c = 0; c < p.nchunk; ++c) {
-      const float mm = ps[c * 2 * kG + 2 * threadIdx.x];
-      if (mm != -INFINITY) S += ps[c * 2 * kG + 2 * threadIdx.x + 1] * ex2(mm - M);
+    const int h = threadIdx.x >> 4, sub = threadIdx.x & 15;     // 256 threads = 16 heads x 16
+    float M = -INFINITY, S = 0.f;
+    for (int64_t c = sub; c < p.nchunk; c += 16) {
+      const float mm = ps[c * 2 * kG + 2 * h], ss = ps[c * 2 * kG + 2 * h + 1];
+      if (mm == -INFINITY) continue;
+      const float nm = fmaxf(M, mm);
+      S = (M == -INFINITY ? 0.f : S * ex2(M - nm)) + ss * ex2(mm - nm);
+      M = nm;
     }
-    lse2[threadIdx.x] = M + log2f(S);
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, M, off);
+      const float os = __shfl_xor_sync(0xffffffffu, S, off);
+      const float nm = fmaxf(M, om);
+      S = (M == -INFINITY ? 0.f : S * ex2(M - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
+      M = nm;
+    }
+    if (sub == 0) lse2[h] = M + log2f(S);
   }
   __syncthreads();
   // kernel range covering blocks [b0, b1): lo of b0 .. hi of b1-1
@@ -451,16 +468,20 @@ struct TopkParams {
   int32_t* selection;
 };
 
-__global__ void __launch_bounds__(32) decode_topk_kernel(const TopkParams p) {
+__global__ void __launch_bounds__(256) decode_topk_kernel(const TopkParams p) {
   __shared__ float lkey[topk::kListCap];
   __shared__ int lid[topk::kListCap];
+  extern __shared__ float rs[];     // the (sequence, group) block scores, staged once
   const TableView tv = table_view(p.table, p.n_seq);
   const int64_t sg = blockIdx.x;
   const int s = (int)(sg / p.hkv);
   const int64_t pos = tv.len[s] - 1;
+  const int64_t n_cand = pos / p.m + 1;
+  for (int64_t b = threadIdx.x; b < n_cand; b += blockDim.x) rs[b] = p.rbuf[sg * p.nb_cap + b];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
   const topk::UnitSel us = topk::unit_sel(pos, p.m, p.top_k, p.n_init, p.n_local, p.consume);
-  topk::warp_select(p.rbuf + sg * p.nb_cap, us, threadIdx.x, lkey, lid, p.selection + sg * p.max_sel, nullptr,
-                    p.max_sel);
+  topk::warp_select(rs, us, threadIdx.x, lkey, lid, p.selection + sg * p.max_sel, nullptr, p.max_sel);
 }
 
 }  // namespace
@@ -621,8 +642,12 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   tp.nb_cap = w.nb_cap;
   tp.rbuf = w.rbuf;
   tp.selection = selection;
+  const size_t tk_smem = sizeof(float) * (size_t)w.nb_cap;
+  if (tk_smem > 48 * 1024 &&
+      cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tk_smem) != cudaSuccess)
+    return INFLLM2_ERR_UNSUPPORTED;
   count_launch();
-  decode_topk_kernel<<<n_seq * hkv, 32, 0, stream>>>(tp);
+  decode_topk_kernel<<<n_seq * hkv, 256, tk_smem, stream>>>(tp);
   // 5. stage 2
   cudaError_t e = launch_attend_tc_decode(hq, hkv, max_sel, n_seq, q, tvd.maps, kMaps, tvd.len, selection, out,
                                           out_f32, lse, w.split, stream);
