@@ -522,7 +522,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 __global__ void __launch_bounds__(512) attend_combine_kernel(const float* __restrict__ part_o,
                                                              const float* __restrict__ part_ml, int64_t parts, int hq,
                                                              int hkv, void* out, int out_f32, float* lse) {
-  __shared__ float wgt[16 * kG];   // [part][h], parts <= 16
+  __shared__ float wgt[(kMaxSel / 2 + 1) * kG];   // [part][h]
   __shared__ float inv_l[kG];
   const int64_t item = blockIdx.x;
   const int64_t i = item / hkv;
