@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--decode-seqs", type=int, default=8, help="sequences per GPU (configs[3]: 64 over 8 GPUs)")
     return ap.parse_args()
 
 
@@ -288,6 +290,13 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dist)
 
+    # free the prefill inputs before the decode caches are built
+    dec = None
+    if not args.no_decode:
+        del q_in, k_in, v_in, caches
+        torch.cuda.empty_cache()
+        dec = run_decode(args, P, cfg, world, rank, dev, barrier, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args)
@@ -302,7 +311,7 @@ def run_ours(args):
                                    f"32q/2kv/d128, m64 p32 s16 k16 init1 local2, query rows zig-zag sharded",
                        "seq_len": seq, "layers": layers, "parallelism": f"query-shard x{world} (NCCL all-gather K/V)",
                        "l2": "inputs 1.2 GiB/layer x 32 layers >> 126 MB L2 (no flush needed)"},
-            "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "decode": dec,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -378,6 +387,114 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
     return {"value": round(args.seq / (ms / args.steps / 1e3), 1), "unit": "tok/s",
             "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
             "note": "pinned host q/k/v per layer, H2D overlapped with compute on a copy stream"}
+
+
+# ----------------------------------------------------------------------------- decode (configs[3])
+
+
+def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
+    """configs[3]: sequences partitioned over ranks (decode_seqs per GPU), each
+    with a seq_len-token cache in all `layers` layers; one step = every sequence
+    appends one token and attends one query row in every layer.  The 32-layer
+    step is captured once in a CUDA graph (fixed split-K bound) and replayed."""
+    import torch
+
+    S, L, layers = args.decode_seqs, args.seq, args.layers
+    extra = args.warmup + args.steps + 8
+    gen = torch.Generator(device=dev)
+    batches = []
+    for layer in range(layers):
+        caches = []
+        for s in range(S):
+            gen.manual_seed(7_000_003 * layer + 101 * s + rank)
+            c = P.BlockizedLayerCache(HKV, D, cfg, capacity=L + extra, device=dev)
+            k = torch.randn((L, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
+            v = torch.randn((L, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
+            c.append(k, v)
+            caches.append(c)
+        b = P.DecodeBatch(caches, cfg)
+        b.reserve(extra)
+        batches.append(b)
+    bound = L + extra
+    q = torch.randn((layers, S, HQ, D), generator=gen, device=dev).to(torch.bfloat16)
+    kn = torch.randn((layers, S, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
+    vn = torch.randn((layers, S, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
+    outs = [None] * layers
+
+    def step(bookkeep=True):
+        for i, b in enumerate(batches):
+            outs[i] = b.step(q[i], kn[i], vn[i], max_len=bound, bookkeep=bookkeep)
+
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        step()
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(graph, stream=side):
+            step(bookkeep=False)
+    for b in batches:
+        b.advance(1)
+    for _ in range(args.warmup):
+        graph.replay()
+        for b in batches:
+            b.advance(1)
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        graph.replay()
+    t1.record()
+    barrier()
+    for b in batches:
+        b.advance(args.steps)
+    ms = t0.elapsed_time(t1)
+    # e2e: per step H2D of every layer's q/k/v from pinned host memory and D2H
+    # of the last layer's outputs, through DecodeBatch.step (eager launches)
+    hq_ = q.cpu().pin_memory()
+    hk_ = kn.cpu().pin_memory()
+    hv_ = vn.cpu().pin_memory()
+    out_host = torch.empty((S, HQ, D), dtype=torch.bfloat16).pin_memory()
+    te0 = torch.cuda.Event(enable_timing=True)
+    te1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    te0.record()
+    for _ in range(args.steps):
+        qd, kd, vd = hq_.to(dev, non_blocking=True), hk_.to(dev, non_blocking=True), hv_.to(dev, non_blocking=True)
+        o = None
+        for i, b in enumerate(batches):
+            o = b.step(qd[i], kd[i], vd[i], max_len=bound)
+        out_host.copy_(o, non_blocking=True)
+    te1.record()
+    barrier()
+    ms_e2e = te0.elapsed_time(te1)
+    if world > 1:
+        t = torch.tensor([ms, ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+    step_ms = ms / args.steps
+    nk = L // 16
+    rows = 19 * 64
+    # SURVEY §8(d): fp32-sized means (the bf16 hi+lo pair is the same 4 B/elem) +
+    # bf16 K+V of the selected rows + q/o + the append (window recompute)
+    per_seq_layer = HKV * nk * D * 4 + HKV * rows * D * 2 * 2 + HQ * D * 2 * 2 + HKV * (32 * D * 2 + 2 * D * 4 + D * 2 * 2)
+    bytes_step = per_seq_layer * S * layers
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    gbs = bytes_step / (step_ms / 1e3) / 1e9
+    return {"metric": "decode us/token (configs[3]: batched decode, 128K context)",
+            "seqs_per_gpu": S, "total_seqs": S * world, "context": L, "layers": layers,
+            "ms_per_step": round(step_ms, 4), "us_per_token": round(step_ms * 1e3 / (S * world), 2),
+            "tokens_per_s": round(S * world / (step_ms / 1e3), 1),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks.get("hbm_gbs", 6541.8),
+                         "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs", 6541.8), 4),
+                         "algorithmic_bytes_per_step": int(bytes_step)},
+            "e2e": {"ms_per_step": round(ms_e2e / args.steps, 4),
+                    "us_per_token": round(ms_e2e / args.steps * 1e3 / (S * world), 2),
+                    "h2d_bytes_per_step": int((q.numel() + kn.numel() + vn.numel()) * 2),
+                    "d2h_bytes_per_step": int(out_host.numel() * 2)},
+            "graph": "32-layer step captured once (5-6 launches per layer), replayed per step"}
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle)
