@@ -89,7 +89,9 @@ __device__ __forceinline__ void tile_range(const Params& p, int64_t part, int ti
 }
 
 __device__ __forceinline__ int64_t item_pos(const Params& p, int64_t i) {
-  return p.seq_len ? p.seq_len[i] - 1 : p.start + i;
+  // decode: seq_len holds the length before this step's append = the new
+  // token's position
+  return p.seq_len ? p.seq_len[i] : p.start + i;
 }
 
 // The item's selection row, read once per warp with lane-parallel loads
@@ -158,10 +160,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     tma_prefetch(&tm_v);
   }
   if (warp == 1) tmem_alloc<64>(tmem_slot);
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;       // cols [0,32): S slots, [32,64): O slots
+  pdl_wait();                             // no-op unless launched as a dependent
   const int64_t items = p.n * p.hkv * p.parts;   // work units (item, part)
 
   if (warp == 0) {
@@ -521,9 +525,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 // shared memory, then thread (h, d-slice) streams the parts with independent loads.
 __global__ void __launch_bounds__(512) attend_combine_kernel(const float* __restrict__ part_o,
                                                              const float* __restrict__ part_ml, int64_t parts, int hq,
-                                                             int hkv, void* out, int out_f32, float* lse) {
+                                                             int hkv, void* out, int out_f32, float* lse,
+                                                             int64_t* seq_len) {
   __shared__ float wgt[(kMaxSel / 2 + 1) * kG];   // [part][h]
   __shared__ float inv_l[kG];
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t item = blockIdx.x;
   const int64_t i = item / hkv;
   const int grp = (int)(item - i * hkv);
@@ -556,6 +563,8 @@ __global__ void __launch_bounds__(512) attend_combine_kernel(const float* __rest
     else
       static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(acc * inv_l[h]);
   }
+  // end of the decode step: the new token is now part of the cache
+  if (seq_len && grp == 0 && t == 0) seq_len[i] += 1;
 }
 
 }  // namespace
@@ -601,12 +610,27 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(items < sms ? items : sms);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   count_launch();
-  attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tq, tq, p);
+  e = cudaLaunchKernelEx(&cfg, attend_tc_kernel, tq, tq, tq, p);
+  if (e != cudaSuccess) return e;
   if (split_ws) {
+    cfg.gridDim = dim3((unsigned)(n_seq * hkv));
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = 0;
     count_launch();
-    attend_combine_kernel<<<(int)(n_seq * hkv), 512, 0, stream>>>(p.part_o, p.part_ml, p.parts, hq, hkv, out,
-                                                                  out_f32, lse);
+    e = cudaLaunchKernelEx(&cfg, attend_combine_kernel, (const float*)p.part_o, (const float*)p.part_ml, p.parts, hq,
+                           hkv, out, out_f32, lse, const_cast<int64_t*>(seq_len));
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

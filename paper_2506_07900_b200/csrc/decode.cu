@@ -18,6 +18,8 @@
 #include <float.h>
 #include <string.h>
 
+#include <utility>
+
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tc_dispatch.cuh"
@@ -60,8 +62,10 @@ struct SeqDesc {
 struct TableView {
   const SeqDesc* desc;
   const CUtensorMap* maps;
-  int64_t* len;
+  int64_t* len;        // OLD length during a step; bumped by the last kernel
+  int* counters;       // [n_seq][8] last-CTA-done counters of the scores kernel
 };
+constexpr int kMaxHkv = 8;
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -73,82 +77,93 @@ __host__ __device__ inline TableView table_view(void* base, int n_seq) {
   t.desc = reinterpret_cast<const SeqDesc*>(b);
   t.maps = reinterpret_cast<const CUtensorMap*>(b + maps_off);
   t.len = reinterpret_cast<int64_t*>(b + len_off);
+  t.counters = reinterpret_cast<int*>(b + len_off + sizeof(int64_t) * n_seq);
   return t;
 }
 
 size_t table_bytes(int n_seq) {
-  return align_up(sizeof(SeqDesc) * n_seq, 128) + sizeof(CUtensorMap) * kMaps * n_seq + sizeof(int64_t) * n_seq;
+  return align_up(sizeof(SeqDesc) * n_seq, 128) + sizeof(CUtensorMap) * kMaps * n_seq + sizeof(int64_t) * n_seq +
+         sizeof(int) * kMaxHkv * n_seq;
+}
+
+// PDL launch: the kernel may start while its predecessor drains; it calls
+// pdl_wait() before reading the predecessor's output.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------------ 1. append + compress
 
-__device__ void window_mean(const __nv_bfloat16* kg, int64_t cap, int d, int64_t j, int stride, int64_t length,
-                            int e, float* out_mean) {
+// Window mean over the cache rows, with row `new_row` taken from `knew` (the
+// token being appended in this step) so no CTA waits for the cache write.
+__device__ __forceinline__ float window_mean(const __nv_bfloat16* kg, int d, int64_t j, int stride, int64_t length,
+                                             int e, int64_t new_row, float knew) {
   const int64_t r0 = j * stride;
   int64_t r1 = r0 + kP;
   if (r1 > length) r1 = length;
-  const __nv_bfloat16* src = kg + r0 * d + e;
   const int w = (int)(r1 - r0);
   float x[kP];
 #pragma unroll
-  for (int r = 0; r < kP; ++r) x[r] = r < w ? __bfloat162float(src[(int64_t)r * d]) : 0.f;   // loads in flight together
+  for (int r = 0; r < kP; ++r)   // all loads in flight together
+    x[r] = r < w ? (r0 + r == new_row ? knew : __bfloat162float(kg[(r0 + r) * d + e])) : 0.f;
   double acc = (double)x[0];
 #pragma unroll
   for (int r = 1; r < kP; ++r)
-    if (r < w) acc += (double)x[r];                                                           // sequential, as numpy
-  *out_mean = __double2float_rn(acc / (double)w);
+    if (r < w) acc += (double)x[r];   // sequential, as numpy's reduce
+  return __double2float_rn(acc / (double)w);
 }
 
+// grid (n_seq, 3): y = 0 writes the new row and re-syncs the first dirty fine
+// window, y = 1 the second, y = 2 the coarse window (sparse.py:116-127; first
+// dirty window clipped to the windows that already existed, F18).
 __global__ void __launch_bounds__(256) decode_append_compress_kernel(void* table, int n_seq, int hkv, int d,
                                                                      const __nv_bfloat16* __restrict__ k_new,
                                                                      const __nv_bfloat16* __restrict__ v_new,
                                                                      int coarse_stride) {
-  const int s = blockIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();
+  const int s = blockIdx.x, role = blockIdx.y;
   TableView tv = table_view(table, n_seq);
   const SeqDesc ds = tv.desc[s];
   const int64_t l_old = tv.len[s];
   const int64_t l_new = l_old + 1;
+  const int stride = role < 2 ? kS : coarse_stride;
+  int64_t first = l_old < kP ? 0 : (l_old - kP) / stride + 1;
+  const int64_t count_old = l_old / stride, count = l_new / stride;
+  if (first > count_old) first = count_old;
+  const int64_t j = first + (role == 1 ? 1 : 0);
   for (int idx = threadIdx.x; idx < hkv * d; idx += blockDim.x) {
     const int g = idx / d, e = idx - g * d;
-    ds.k[((int64_t)g * ds.cap + l_old) * d + e] = k_new[(int64_t)s * hkv * d + idx];
-    ds.v[((int64_t)g * ds.cap + l_old) * d + e] = v_new[(int64_t)s * hkv * d + idx];
-  }
-  __syncthreads();
-  // fine windows (stride 16): first dirty window clipped to those that existed (F18)
-  {
-    int64_t first = l_old < kP ? 0 : (l_old - kP) / kS + 1;
-    const int64_t count_old = l_old / kS, count = l_new / kS;
-    if (first > count_old) first = count_old;
-    const int64_t nwin = count - first;
-    for (int64_t idx = threadIdx.x; idx < nwin * hkv * d; idx += blockDim.x) {
-      const int64_t j = first + idx / (hkv * d);
-      const int rem = (int)(idx % (hkv * d));
-      const int g = rem / d, e = rem - g * d;
-      float mu;
-      window_mean(ds.k + (int64_t)g * ds.cap * d, ds.cap, d, j, kS, l_new, e, &mu);
+    const float knew = __bfloat162float(k_new[(int64_t)s * hkv * d + idx]);
+    if (role == 0) {
+      ds.k[((int64_t)g * ds.cap + l_old) * d + e] = k_new[(int64_t)s * hkv * d + idx];
+      ds.v[((int64_t)g * ds.cap + l_old) * d + e] = v_new[(int64_t)s * hkv * d + idx];
+    }
+    if (j >= count) continue;
+    const float mu = window_mean(ds.k + (int64_t)g * ds.cap * d, d, j, stride, l_new, e, l_old, knew);
+    if (role < 2) {
       const int64_t dst = ((int64_t)g * ds.means_cap + j) * d + e;
       ds.fine[dst] = mu;
       const __nv_bfloat16 h = __float2bfloat16_rn(mu);
       ds.hi[dst] = h;
       ds.lo[dst] = __float2bfloat16_rn(mu - __bfloat162float(h));
-    }
-  }
-  {
-    int64_t first = l_old < kP ? 0 : (l_old - kP) / coarse_stride + 1;
-    const int64_t count_old = l_old / coarse_stride, count = l_new / coarse_stride;
-    if (first > count_old) first = count_old;
-    const int64_t nwin = count - first;
-    for (int64_t idx = threadIdx.x; idx < nwin * hkv * d; idx += blockDim.x) {
-      const int64_t j = first + idx / (hkv * d);
-      const int rem = (int)(idx % (hkv * d));
-      const int g = rem / d, e = rem - g * d;
-      float mu;
-      window_mean(ds.k + (int64_t)g * ds.cap * d, ds.cap, d, j, coarse_stride, l_new, e, &mu);
+    } else {
       ds.coarse[((int64_t)g * ds.coarse_cap + j) * d + e] = mu;
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) tv.len[s] = l_new;
 }
 
 // ------------------------------------------------------------------ 2. stage-1 (tcgen05, split-K)
@@ -183,7 +198,7 @@ __device__ __forceinline__ void s1_item(const S1Params& p, const TableView& tv, 
   const int64_t c = item - sg * p.nchunk;
   *s = (int)(sg / p.hkv);
   *g = (int)(sg - (int64_t)(*s) * p.hkv);
-  const int64_t nk = tv.len[*s] / kS;
+  const int64_t nk = (tv.len[*s] + 1) / kS;   // length after this step's append
   *j0 = c * kChunk;
   int64_t e = *j0 + kChunk;
   *j1 = e < nk ? e : nk;
@@ -217,10 +232,12 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
     tma_prefetch(&tm_q);
   }
   if (warp == 1) tmem_alloc<32>(tmem_slot);
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();     // means / lengths of this step's append are visible past here
   const int64_t items = (int64_t)p.n_seq * p.hkv * p.nchunk;
 
   if (warp == 0) {
@@ -381,23 +398,34 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
 struct ScoreParams {
   void* table;
   int n_seq, hkv, m, kpb;
+  int top_k, n_init, n_local, consume, max_sel;
   int64_t nchunk, nbchunk, zstride, nb_cap;
   const float* zbuf;
   const float* pstat;
   float* rbuf;               // [seq][g][nb_cap]
+  int32_t* selection;        // [seq][g][max_sel]
 };
 
+// Block scores for 64 blocks of one (sequence, group); the last CTA of the
+// (sequence, group) to finish (device counter) then runs the top-k over all of
+// them, so selection needs no extra launch.
 __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p) {
   __shared__ float lse2[kG];
   __shared__ float sk[kBlkChunk * 8 + 8];   // kernels of this block range (kpb <= 8)
+  __shared__ float lkey[topk::kListCap];
+  __shared__ int lid[topk::kListCap];
+  __shared__ int is_last;
+  extern __shared__ float rs[];             // staged block scores for the top-k
+  pdl_launch_dependents();
+  pdl_wait();
   const TableView tv = table_view(p.table, p.n_seq);
   const int64_t item = blockIdx.x;
   const int64_t sg = item / p.nbchunk;
   const int64_t bc = item - sg * p.nbchunk;
   const int s = (int)(sg / p.hkv);
   const int g = (int)(sg - (int64_t)s * p.hkv);
-  const int64_t L = tv.len[s];
-  const int64_t pos = L - 1;
+  const int64_t pos = tv.len[s];            // the new token's position
+  const int64_t L = pos + 1;
   int64_t nk_t = pos / kS + 1;
   if (nk_t > L / kS) nk_t = L / kS;
   const int64_t n_cand = pos / p.m + 1;
@@ -427,7 +455,6 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
     if (sub == 0) lse2[h] = M + log2f(S);
   }
   __syncthreads();
-  // kernel range covering blocks [b0, b1): lo of b0 .. hi of b1-1
   int64_t jlo, jhi, tmp;
   kernel_range_for_block(b0 * p.m, b0 * p.m + p.m, kP, kS, nk_t, &jlo, &tmp);
   jhi = b1 * p.kpb < nk_t ? b1 * p.kpb : nk_t;
@@ -444,6 +471,7 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
     sk[j - jlo] = (a0 + a1) * (1.0f / kG);
   }
   __syncthreads();
+  float* rrow = p.rbuf + sg * p.nb_cap;
   for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
     int64_t end = (b + 1) * p.m;
     if (end > pos + 1) end = pos + 1;
@@ -454,30 +482,21 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
       r = sk[lo - jlo];
       for (int64_t j = lo + 1; j < hi; ++j) r = fmaxf(r, sk[j - jlo]);
     }
-    p.rbuf[sg * p.nb_cap + b] = r;
+    rrow[b] = r;
   }
-}
-
-// ------------------------------------------------------------------ 4. top-k
-
-struct TopkParams {
-  void* table;
-  int n_seq, hkv, m, top_k, n_init, n_local, consume, max_sel;
-  int64_t nb_cap;
-  const float* rbuf;
-  int32_t* selection;
-};
-
-__global__ void __launch_bounds__(256) decode_topk_kernel(const TopkParams p) {
-  __shared__ float lkey[topk::kListCap];
-  __shared__ int lid[topk::kListCap];
-  extern __shared__ float rs[];     // the (sequence, group) block scores, staged once
-  const TableView tv = table_view(p.table, p.n_seq);
-  const int64_t sg = blockIdx.x;
-  const int s = (int)(sg / p.hkv);
-  const int64_t pos = tv.len[s] - 1;
-  const int64_t n_cand = pos / p.m + 1;
-  for (int64_t b = threadIdx.x; b < n_cand; b += blockDim.x) rs[b] = p.rbuf[sg * p.nb_cap + b];
+  // ---- last CTA of this (sequence, group) selects
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int n_active = (int)((n_cand + kBlkChunk - 1) / kBlkChunk);
+    const int done = atomicAdd(&tv.counters[s * kMaxHkv + g], 1);
+    is_last = (done == n_active - 1);
+    if (is_last) tv.counters[s * kMaxHkv + g] = 0;   // reset for the next step
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int64_t b = threadIdx.x; b < n_cand; b += blockDim.x) rs[b] = __ldcg(rrow + b);
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const topk::UnitSel us = topk::unit_sel(pos, p.m, p.top_k, p.n_init, p.n_local, p.consume);
@@ -566,7 +585,7 @@ static DecodeWs decode_ws_layout(const infllm2_geometry& g, int n_seq, int hkv, 
 }
 
 bool decode_supported(const infllm2_geometry& g, int hq, int hkv, int d) {
-  return hq / hkv == kG && hq % hkv == 0 && d == kD && g.kernel_stride == kS && g.kernel_size == kP &&
+  return hkv <= kMaxHkv && hq / hkv == kG && hq % hkv == 0 && d == kD && g.kernel_stride == kS && g.kernel_size == kP &&
          g.block_size == 64 && g.coarse_stride % kS == 0 && infllm2_max_selected(&g) <= 80;
 }
 
@@ -581,11 +600,11 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
   const int max_sel = infllm2_max_selected(&g);
   const TableView tvd = table_view(table, n_seq);
-  // 1. append + compress
-  count_launch();
-  decode_append_compress_kernel<<<n_seq, 256, 0, stream>>>(table, n_seq, hkv, d,
-                                                            static_cast<const __nv_bfloat16*>(k_new),
-                                                            static_cast<const __nv_bfloat16*>(v_new), g.coarse_stride);
+  // 1. append + compress (3 CTAs per sequence)
+  if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,
+                 static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
+                 (int)g.coarse_stride) != cudaSuccess)
+    return INFLLM2_ERR_CUDA;
   // 2. stage-1 split-K
   S1Params sp;
   sp.table = table;
@@ -610,15 +629,21 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items1 = (int64_t)n_seq * hkv * w.nchunk;
-  count_launch();
-  decode_stage1_kernel<<<(int)(items1 < sms ? items1 : sms), kS1Threads, smem1, stream>>>(tq, sp);
-  // 3. block scores
+  if (launch_pdl(decode_stage1_kernel, dim3((unsigned)(items1 < sms ? items1 : sms)), dim3(kS1Threads), smem1, stream,
+                 tq, sp) != cudaSuccess)
+    return INFLLM2_ERR_CUDA;
+  // 3. block scores + (last CTA) top-k
   ScoreParams scp;
   scp.table = table;
   scp.n_seq = n_seq;
   scp.hkv = hkv;
   scp.m = g.block_size;
   scp.kpb = g.block_size / kS;
+  scp.top_k = g.top_k;
+  scp.n_init = g.n_init_blocks;
+  scp.n_local = g.n_local_blocks;
+  scp.consume = g.forced_consume_budget;
+  scp.max_sel = max_sel;
   scp.nchunk = w.nchunk;
   scp.nbchunk = w.nbchunk;
   scp.zstride = w.zstride;
@@ -626,28 +651,15 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   scp.zbuf = w.zbuf;
   scp.pstat = w.pstat;
   scp.rbuf = w.rbuf;
-  count_launch();
-  decode_scores_kernel<<<(int)(n_seq * hkv * w.nbchunk), 256, 0, stream>>>(scp);
-  // 4. top-k
-  TopkParams tp;
-  tp.table = table;
-  tp.n_seq = n_seq;
-  tp.hkv = hkv;
-  tp.m = g.block_size;
-  tp.top_k = g.top_k;
-  tp.n_init = g.n_init_blocks;
-  tp.n_local = g.n_local_blocks;
-  tp.consume = g.forced_consume_budget;
-  tp.max_sel = max_sel;
-  tp.nb_cap = w.nb_cap;
-  tp.rbuf = w.rbuf;
-  tp.selection = selection;
-  const size_t tk_smem = sizeof(float) * (size_t)w.nb_cap;
-  if (tk_smem > 48 * 1024 &&
-      cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tk_smem) != cudaSuccess)
+  scp.selection = selection;
+  const size_t sc_smem = sizeof(float) * (size_t)w.nb_cap;
+  if (sc_smem > 40 * 1024 &&
+      cudaFuncSetAttribute(decode_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem) !=
+          cudaSuccess)
     return INFLLM2_ERR_UNSUPPORTED;
-  count_launch();
-  decode_topk_kernel<<<n_seq * hkv, 256, tk_smem, stream>>>(tp);
+  if (launch_pdl(decode_scores_kernel, dim3((unsigned)(n_seq * hkv * w.nbchunk)), dim3(256), sc_smem, stream, scp) !=
+      cudaSuccess)
+    return INFLLM2_ERR_CUDA;
   // 5. stage 2
   cudaError_t e = launch_attend_tc_decode(hq, hkv, max_sel, n_seq, q, tvd.maps, kMaps, tvd.len, selection, out,
                                           out_f32, lse, w.split, stream);
