@@ -37,6 +37,20 @@ GEOM = dict(block_size=64, kernel_size=32, kernel_stride=16, coarse_stride=128, 
 METRIC = "InfLLM v2 prefill tok/s @128K (32-layer 8B-shaped sparse attention stack)"
 
 
+def load_peaks():
+    """Roofline denominators: the driver-written MEASURED_PEAKS.json when present,
+    else the fallback of /opt/skills/guides/B200_PROFILING.md (6.65 TB/s copy,
+    ~1.4 PFLOP/s sustained bf16 under the power cap), labelled as such."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        m = json.load(open(path))
+        return {"hbm_gbs": float(m.get("hbm_gbs", 6650.0)),
+                "bf16_tflops_sustained": float(m.get("bf16_tflops_sustained", m.get("bf16_tflops", 1400.0))),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md: MEASURED_PEAKS.json absent)"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -265,9 +279,8 @@ def run_ours(args):
     f1, f2, rows2 = algorithmic_work(seq, chunks)
     f1 *= layers
     f2 *= layers
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
-    peak_t = peaks.get("bf16_tflops_sustained", 1383.3)
+    peaks = load_peaks()
+    peak_t = peaks["bf16_tflops_sustained"]
     sel_tflops = f1 / (t_sel / 1e3) / 1e12
     att_tflops = f2 / (t_att / 1e3) / 1e12
     if t_sel >= t_att:
@@ -278,6 +291,7 @@ def run_ours(args):
         roof = {"kernel": "attend (stage-2)", "bound": "tensor", "achieved": round(att_tflops, 2), "peak": peak_t,
                 "unit": "TFLOP/s", "frac": round(att_tflops / peak_t, 4), "traffic": None,
                 "share_of_step": round(t_att / (t_sel + t_att), 3)}
+    roof["peak_source"] = peaks["source"]
     roof["stage1_ms_per_step"] = round(t_sel, 3)
     roof["stage2_ms_per_step"] = round(t_att, 3)
     roof["stage1_tflops"] = round(sel_tflops, 2)
@@ -480,16 +494,15 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
     # bf16 K+V of the selected rows + q/o + the append (window recompute)
     per_seq_layer = HKV * nk * D * 4 + HKV * rows * D * 2 * 2 + HQ * D * 2 * 2 + HKV * (32 * D * 2 + 2 * D * 4 + D * 2 * 2)
     bytes_step = per_seq_layer * S * layers
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peaks = load_peaks()
     gbs = bytes_step / (step_ms / 1e3) / 1e9
     return {"metric": "decode us/token (configs[3]: batched decode, 128K context)",
             "seqs_per_gpu": S, "total_seqs": S * world, "context": L, "layers": layers,
             "ms_per_step": round(step_ms, 4), "us_per_token": round(step_ms * 1e3 / (S * world), 2),
             "tokens_per_s": round(S * world / (step_ms / 1e3), 1),
-            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks.get("hbm_gbs", 6541.8),
-                         "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs", 6541.8), 4),
-                         "algorithmic_bytes_per_step": int(bytes_step)},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
+                         "peak_source": peaks["source"], "algorithmic_bytes_per_step": int(bytes_step)},
             "e2e": {"ms_per_step": round(ms_e2e / args.steps, 4),
                     "us_per_token": round(ms_e2e / args.steps * 1e3 / (S * world), 2),
                     "h2d_bytes_per_step": int((q.numel() + kn.numel() + vn.numel()) * 2),

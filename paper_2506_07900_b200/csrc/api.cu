@@ -160,15 +160,8 @@ int infllm2_attend(const infllm2_geometry* g, const void* q, int64_t q_row_strid
   cudaStream_t st = (cudaStream_t)stream;
   const int out_f32 = (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0;
   if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_attend_supported(*g, cs)) {
-    static const bool one_team = [] {
-      const char* e = getenv("INFLLM2_ATTEND");
-      return e && e[0] == '1';
-    }();
-    if (one_team)
-      return cuda_status(launch_attend_tc(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out,
-                                          out_f32, lse, st));
-    return cuda_status(launch_attend_tc2(cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32, lse,
-                                         st));
+    return cuda_status(launch_attend_tc(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32,
+                                        lse, st));
   }
   return cuda_status(launch_attend_simt(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out,
                                         out_f32, lse, st));
