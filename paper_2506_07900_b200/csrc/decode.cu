@@ -24,14 +24,22 @@
 #include "sm100.cuh"
 #include "tc_dispatch.cuh"
 #include "topk.cuh"
+#include "decode_common.cuh"
 
 namespace infllm2 {
+
+using namespace dec;
 
 cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
                                     const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
                                     const int32_t* selection, void* out, int out_f32, float* lse,
                                     float* split_ws, cudaStream_t stream);
 size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel);
+size_t decode_fused_workspace_bytes(int n_seq, int hkv);
+bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int sms);
+int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int hq, int hkv, const void* q,
+                      const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32, float* lse,
+                      void* ws, cudaStream_t stream, int sms);
 
 namespace {
 
@@ -40,52 +48,9 @@ using namespace sm100;
 constexpr int kG = 16;
 constexpr int kD = 128;
 constexpr int kS = 16;             // fine stride
-constexpr int kP = 32;             // kernel size
 constexpr int kTile = 128;         // kernels per MMA tile
 constexpr int kChunk = 1024;       // kernels per stage-1 work item (8 tiles)
 constexpr int kBlkChunk = 64;      // blocks per scores work item
-constexpr int kMaps = 4;           // per sequence: K, V, hi, lo
-
-// Device-side table: [n_seq] descriptors, [n_seq][4] tensor maps, [n_seq] lengths.
-struct SeqDesc {
-  __nv_bfloat16* k;
-  __nv_bfloat16* v;
-  int64_t cap;
-  float* fine;
-  __nv_bfloat16* hi;
-  __nv_bfloat16* lo;
-  int64_t means_cap;
-  float* coarse;
-  int64_t coarse_cap;
-};
-
-struct TableView {
-  const SeqDesc* desc;
-  const CUtensorMap* maps;
-  int64_t* len;        // OLD length during a step; bumped by the last kernel
-  int* counters;       // [n_seq][8] last-CTA-done counters of the scores kernel
-};
-constexpr int kMaxHkv = 8;
-
-__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-__host__ __device__ inline TableView table_view(void* base, int n_seq) {
-  uint8_t* b = static_cast<uint8_t*>(base);
-  TableView t;
-  const size_t maps_off = align_up(sizeof(SeqDesc) * n_seq, 128);
-  const size_t len_off = maps_off + sizeof(CUtensorMap) * kMaps * n_seq;
-  t.desc = reinterpret_cast<const SeqDesc*>(b);
-  t.maps = reinterpret_cast<const CUtensorMap*>(b + maps_off);
-  t.len = reinterpret_cast<int64_t*>(b + len_off);
-  t.counters = reinterpret_cast<int*>(b + len_off + sizeof(int64_t) * n_seq);
-  return t;
-}
-
-size_t table_bytes(int n_seq) {
-  return align_up(sizeof(SeqDesc) * n_seq, 128) + sizeof(CUtensorMap) * kMaps * n_seq + sizeof(int64_t) * n_seq +
-         sizeof(int) * kMaxHkv * n_seq;
-}
-
 // PDL launch: the kernel may start while its predecessor drains; it calls
 // pdl_wait() before reading the predecessor's output.
 template <typename... KArgs, typename... Args>
@@ -106,25 +71,6 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // ------------------------------------------------------------------ 1. append + compress
-
-// Window mean over the cache rows, with row `new_row` taken from `knew` (the
-// token being appended in this step) so no CTA waits for the cache write.
-__device__ __forceinline__ float window_mean(const __nv_bfloat16* kg, int d, int64_t j, int stride, int64_t length,
-                                             int e, int64_t new_row, float knew) {
-  const int64_t r0 = j * stride;
-  int64_t r1 = r0 + kP;
-  if (r1 > length) r1 = length;
-  const int w = (int)(r1 - r0);
-  float x[kP];
-#pragma unroll
-  for (int r = 0; r < kP; ++r)   // all loads in flight together
-    x[r] = r < w ? (r0 + r == new_row ? knew : __bfloat162float(kg[(r0 + r) * d + e])) : 0.f;
-  double acc = (double)x[0];
-#pragma unroll
-  for (int r = 1; r < kP; ++r)
-    if (r < w) acc += (double)x[r];   // sequential, as numpy's reduce
-  return __double2float_rn(acc / (double)w);
-}
 
 // grid (n_seq, 3): y = 0 writes the new row and re-syncs the first dirty fine
 // window, y = 1 the second, y = 2 the coarse window (sparse.py:116-127; first
@@ -559,6 +505,7 @@ struct DecodeWs {
   float* pstat;
   float* rbuf;
   float* split;
+  void* fused;
   int64_t nchunk, nbchunk, zstride, nb_cap;
   size_t bytes;
 };
@@ -580,6 +527,8 @@ static DecodeWs decode_ws_layout(const infllm2_geometry& g, int n_seq, int hkv, 
   off += align_up(sizeof(float) * n_seq * hkv * w.nb_cap, 256);
   w.split = reinterpret_cast<float*>(b + off);
   off += align_up(attend_split_workspace(n_seq, hkv, infllm2_max_selected(&g)), 256);
+  w.fused = b + off;
+  off += align_up(decode_fused_workspace_bytes(n_seq, hkv), 256);
   w.bytes = off;
   return w;
 }
@@ -600,6 +549,13 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
   const int max_sel = infllm2_max_selected(&g);
   const TableView tvd = table_view(table, n_seq);
+  {
+    int dev = 0, sms = kNumSMs;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (decode_fused_supported(g, n_seq, hkv, max_len_after, sms))
+      return decode_fused_step(g, table, n_seq, hq, hkv, q, k_new, v_new, selection, out, out_f32, lse, w.fused,
+                               stream, sms);
+  }
   // 1. append + compress (3 CTAs per sequence)
   if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,
                  static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),

@@ -84,3 +84,46 @@ def test_decode_table_rebuilds_after_external_append_and_growth():
     ref.append(torch.from_numpy(k[:n]).cuda(), torch.from_numpy(v[:n]).cuda())
     assert digest(_means(layer.fine_means)) == digest(_means(ref.fine_means))
     assert torch.equal(layer.keys.contiguous(), ref.keys.contiguous())
+
+
+@pytest.mark.parametrize("lengths", [[3000, 5000, 777, 8190, 64, 1, 130, 20000], [16383, 16385]])
+def test_fused_decode_matches_five_launch_path(lengths, monkeypatch):
+    """The single-launch decode (decode_fused.cu) against the five-launch path
+    (decode.cu) over several steps: identical selections and kernel means,
+    outputs within float32 noise."""
+    cfg = P.SparseAttentionConfig(top_k=16)
+    steps = 5
+    full = [make_qkv(71 + i, L + steps, steps, 32, 2, 128) for i, L in enumerate(lengths)]
+
+    def run(legacy):
+        if legacy:
+            monkeypatch.setenv("INFLLM2_DECODE_LEGACY", "1")
+        else:
+            monkeypatch.delenv("INFLLM2_DECODE_LEGACY", raising=False)
+        layers = []
+        for (q, k, v), L in zip(full, lengths):
+            layer = P.BlockizedLayerCache(2, 128, cfg)
+            layer.append(torch.from_numpy(k[:L]).cuda(), torch.from_numpy(v[:L]).cuda())
+            layers.append(layer)
+        batch = P.DecodeBatch(layers, cfg)
+        res = []
+        for st in range(steps):
+            qs = torch.stack([torch.from_numpy(f[0][st]) for f in full]).cuda()
+            ks = torch.stack([torch.from_numpy(f[1][L + st]) for f, L in zip(full, lengths)]).cuda()
+            vs = torch.stack([torch.from_numpy(f[2][L + st]) for f, L in zip(full, lengths)]).cuda()
+            res.append(batch.step(qs, ks, vs, return_selection=True, return_lse=True, out_dtype=torch.float32))
+        torch.cuda.synchronize()
+        return res, layers
+
+    got, lay_f = run(False)
+    ref, lay_l = run(True)
+    for (o1, s1, l1), (o2, s2, l2) in zip(got, ref):
+        assert torch.equal(s1, s2)
+        assert (o1 - o2).abs().max().item() < 1e-4
+        assert (l1 - l2).abs().max().item() < 1e-4
+    for a, b in zip(lay_f, lay_l):
+        assert a.length == b.length
+        assert torch.equal(a.keys.contiguous(), b.keys.contiguous())
+        assert torch.equal(a.values.contiguous(), b.values.contiguous())
+        assert digest(_means(a.fine_means)) == digest(_means(b.fine_means))
+        assert digest(_means(a.coarse_means)) == digest(_means(b.coarse_means))
