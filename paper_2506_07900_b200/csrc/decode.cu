@@ -37,9 +37,9 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
 size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel);
 size_t decode_fused_workspace_bytes(int n_seq, int hkv);
 bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int sms);
-int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int hq, int hkv, const void* q,
-                      const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32, float* lse,
-                      void* ws, cudaStream_t stream, int sms);
+int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
+                      const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
+                      int out_f32, float* lse, void* ws, cudaStream_t stream, int sms);
 
 namespace {
 
@@ -553,8 +553,8 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
     int dev = 0, sms = kNumSMs;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (decode_fused_supported(g, n_seq, hkv, max_len_after, sms))
-      return decode_fused_step(g, table, n_seq, hq, hkv, q, k_new, v_new, selection, out, out_f32, lse, w.fused,
-                               stream, sms);
+      return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
+                               lse, w.fused, stream, sms);
   }
   // 1. append + compress (3 CTAs per sequence)
   if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,

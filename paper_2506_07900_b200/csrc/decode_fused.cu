@@ -2,47 +2,43 @@
 //
 // The five-launch path (decode.cu) spends most of a 128K layer-step in launch
 // ramps and tails: each phase is a few microseconds of HBM traffic behind a
-// kernel boundary.  Here one persistent CTA per SM runs the whole step and the
-// phases of each (sequence, KV group) "segment" are chained by device-scope
-// counters instead of kernel boundaries, so the means stream of stage 1 —
-// the HBM-bound part, 8.4 MB per 128K segment — runs back to back on all SMs
-// and the dependent tail (LSE merge, block scores, top-k, stage 2) costs a few
-// microseconds per segment.
+// kernel boundary.  Here the whole step is one launch of 8-CTA thread-block
+// clusters (one CTA per SM); each cluster owns one (sequence, KV group)
+// "segment" at a time and its eight CTAs ("pieces") exchange the small
+// intermediate results through distributed shared memory, signalled by
+// cluster-scope mbarrier arrivals — no global-memory round trips between the
+// phases of a segment.  Stage 1's means stream (8.4 MB per 128K segment, the
+// HBM-bound part) runs on every SM at once; the dependent tail costs a few
+// microseconds.
 //
-// Work split.  Segment sg = (s, g) has n_cand = pos/64 + 1 candidate blocks
-// (pos = the new token's position).  Every CTA computes the same partition from
-// the device-side lengths: each segment gets 1 + floor(avail * n_cand / total)
-// CTAs ("pieces"), capped so the top-k merge list fits shared memory, and each
-// piece owns a contiguous block range [b0, b1) of its segment.
-//
-// Per piece (warp 0 = TMA producer, warp 1 = MMA issuer, warps 2..5 = 128
-// epilogue threads):
-//   A. append.  Kernel windows containing the new row (the last one or two of
-//      the segment) are recomputed, bitwise as build_kernels (sparse.py:70-91,
-//      116-127, F18 clip), by every piece whose row range holds them (identical
-//      values, so concurrent writers agree); the segment's last piece also
-//      writes the K/V row and the dirty coarse window.
-//   B. stage-1 scores z = mu . q for the piece's kernels [4*b0 - 1, 4*b1)
-//      (one halo kernel on the left, so every block's kernel range
-//      [4b-1, 4b+4) is local) on tcgen05: M = 128 kernels, N = 16 heads,
-//      bf16 hi + lo means; the z tiles STAY IN TMEM (16 columns per tile).
-//      Online per-head (max, sum 2^z) over the owned kernels [4*b0, 4*b1) ->
-//      global partial; arrive on the segment's stage-1 counter.
-//   C. when all pieces arrived: exact per-head LSE from the partials,
-//      S_j = mean_h 2^(z - lse) (sparse.py:163-188) from TMEM, block max R_b
+// Per segment, piece r owns the contiguous candidate-block range
+// [r*nb/8, (r+1)*nb/8) (nb = pos/64 + 1, pos = the new token's position).
+// Warp 0 = TMA producer, warp 1 = MMA issuer, warps 2..5 = 128 epilogue threads.
+//   A. append.  The kernel windows that contain the new row (the last one or
+//      two) are recomputed bitwise as build_kernels (sparse.py:70-91, 116-127,
+//      F18 clip) by every piece whose row range holds them (identical values,
+//      so concurrent writers agree); piece 7 also writes the K/V row and the
+//      dirty coarse window.
+//   B. stage-1 scores z = mu . q for the piece's kernels [4*b0 - 1, 4*b1) (one
+//      halo kernel on the left makes every block's kernel range [4b-1, 4b+4)
+//      local) on tcgen05: M = 128 kernels, N = 16 heads, bf16 hi + lo means.
+//      The z tiles STAY IN TMEM (16 columns per tile).  Per-head (max, sum 2^z)
+//      over the owned kernels [4*b0, 4*b1) is exchanged across the cluster ->
+//      exact LSE (model.py:172-191).
+//   C. S_j = mean_h 2^(z - lse) (sparse.py:163-188) from TMEM, block max R_b
 //      (sparse.py:191-215), local top-`budget` by (score desc, id asc)
-//      (sparse.py:273) -> global candidates; the last piece to arrive merges
-//      the candidate lists (the global top-B is contained in the union of the
-//      local top-Bs) and publishes the selection (force_blocks + select_topk,
-//      sparse.py:218-277).
-//   D. stage 2: the selection's 64-row blocks, forced ones first, are cut into
-//      128-row tiles; tile t goes to piece t mod c.  Forced-only tiles do not
-//      wait for the selection.  Per tile: S^T = K . Q^T, masked softmax
-//      (sparse.py:370-372), P as bf16 hi + lo, O^T = V^T . P^T, written as an
-//      unnormalised partial; the last tile to finish merges the partials into
-//      the output row and its LSE.
-// The last CTA to finish bumps every sequence's device-side length and resets
-// the counters for the next step.
+//      (sparse.py:273); the eight local lists are exchanged and every piece
+//      merges them (the global top-B lies in the union of the local top-Bs)
+//      into the selection (force_blocks + select_topk, sparse.py:218-277).
+//   D. stage 2: the selection's 64-row blocks in 128-row tiles, forced-only
+//      tiles first (they do not wait for the selection) and assigned from the
+//      last piece down, chosen tiles from piece 0 up.  Per tile: S^T = K . Q^T,
+//      masked softmax (sparse.py:370-372), P as bf16 hi + lo, O^T = V^T . P^T,
+//      kept as an unnormalised partial in shared memory; after the cluster
+//      exchange piece r merges heads 2r, 2r+1 of all partials into the output
+//      row and its LSE.
+// Clusters loop over segments; the last CTA to finish bumps every sequence's
+// device-side length and resets the done counter.
 #include <float.h>
 #include <stdlib.h>
 
@@ -64,15 +60,15 @@ constexpr int kG = 16;
 constexpr int kD = 128;
 constexpr int kS = 16;
 constexpr int kM = 64;
+constexpr int kMaxCl = 8;                     // CTAs per cluster = pieces per segment (runtime 3..8)
 constexpr int kThreads = 192;
 constexpr int kStages = 3;
 constexpr int kMaxTiles = 28;                 // z tiles resident in TMEM (16 columns each)
 constexpr int kMaxRows = kMaxTiles * 128;     // kernels per piece
 constexpr int kMaxPieceBlocks = (kMaxRows - 1) / 4;
-constexpr int kCandCap = kMaxRows * 4 / 8;    // (key, id) pairs in the sarr alias
-constexpr int kMaxPieces = 160;               // >= SM count
-constexpr int kMaxT2 = 40;                    // stage-2 tiles per segment (max_sel <= 80)
+constexpr int kMaxBudget = 32;
 constexpr int kPartStride = kG * kD + 2 * kG; // floats per stage-2 partial
+constexpr int kMaxSeq = 160;
 constexpr uint32_t kColS2 = 448;
 constexpr uint32_t kColO = 464;
 
@@ -84,115 +80,56 @@ constexpr uint32_t kPHalf = 128 * kG * 2;     // 4 KB
 struct Smem {
   static constexpr uint32_t ring = 0;
   static constexpr uint32_t q = ring + kStages * kStageBytes;
-  static constexpr uint32_t p = q + kQB;                         // P hi/lo; top-k lists alias it
-  static constexpr uint32_t sarr = p + 2 * kPHalf;               // S_j per kernel; merge list alias
-  static constexpr uint32_t rarr = sarr + kMaxRows * 4;          // R_b per block
-  static constexpr uint32_t red = rarr + (kMaxPieceBlocks + 9) * 4;
+  static constexpr uint32_t p = q + kQB;                         // P hi/lo; top-k lists / merge flags alias it
+  static constexpr uint32_t sarr = p + 2 * kPHalf;               // S_j; merge list; stage-2 partial slots
+  static constexpr uint32_t rarr = sarr + kMaxRows * 4;          // R_b; filtered merge list
+  static constexpr uint32_t xch = rarr + (kMaxPieceBlocks + 9) * 4;   // published: [32] LSE partial, [64] candidates
+  static constexpr uint32_t red = xch + (2 * kG + 2 * kMaxBudget) * 4;
   static constexpr uint32_t bars = (red + (4 * kG * 2 + 2 * kG + 8) * 4 + 7) / 8 * 8;
-  static constexpr uint32_t total = bars + (kMaxTiles + 16) * 8 + 16;
+  static constexpr uint32_t total = bars + (kMaxTiles + 24) * 8 + 16;
 };
-static_assert(Smem::total + 1024 <= 232448, "fused decode shared memory");
+static_assert(Smem::total + 1024 + 2048 <= 232448, "fused decode shared memory");
 static_assert(topk::kListCap * 8 <= 2 * kPHalf, "top-k lists alias the P buffer");
-static_assert(kCandCap * 4 <= 2 * kPHalf, "merge flags alias the P buffer");
+static_assert(kPartStride * 4 <= Smem::xch - Smem::sarr, "the stage-2 partial fits the sarr/rarr region");
 
 struct Params {
   void* table;
   int n_seq, hkv, hq;
-  int top_k, n_init, n_local, consume, max_sel, coarse_stride, cmax;
+  int top_k, n_init, n_local, consume, max_sel, coarse_stride;
   const __nv_bfloat16* k_new;
   const __nv_bfloat16* v_new;
   int32_t* selection;      // [seq][g][max_sel]
   void* out;
   int out_f32;
   float* lse;
-  float* pstat;            // [seg][kMaxPieces][16][2]
-  float* cand;             // [seg][kMaxPieces][32][2]  (key, id bits)
-  float* part;             // [seg][kMaxT2][kPartStride]
   float zscale;            // log2(e) / sqrt(D)
   int trace;
 };
 
-// Per-CTA assignment (thread 0 computes, everyone reads).
+// One piece's view of one segment.
 struct Info {
-  int active, s, g, sg, piece, c;
-  int64_t pos, nk, n_cand, b0, b1, r0, r1;
+  int np;                      // pieces = cluster size
+  int s, g;
+  int64_t pos, nk, n_cand, b0, b1, r0, r1, dlo;
   int ntiles, dirty_tile;
-  int64_t dlo;                 // first dirty window (rows [dlo, nk) change this step)
   // selection geometry (force_blocks / select_topk rules)
-  int n_init, local_lo, n_loc, budget, n_free, n_ch, n_sel, nf, t2;
+  int n_init, local_lo, n_loc, budget, n_free, n_ch, n_sel, nf, tf, t2;
 };
 
-// Optional phase timeline (INFLLM2_DECODE_TRACE=1): %globaltimer per CTA and
-// phase, read back with infllm2_debug_decode_trace (tools/decode_trace.py).
-// `on` = launch number + 1; the last kTraceRing launches are kept.
-constexpr int kTracePts = 16;
-constexpr int kTraceRing = 4;
-__device__ unsigned long long g_trace[kTraceRing * kMaxPieces * kTracePts];
-__device__ __forceinline__ void trace(int on, int pt) {
-  if (on) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_trace[(((on - 1) % kTraceRing) * kMaxPieces + blockIdx.x) * kTracePts + pt] = t;
-  }
-}
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// Bounded spin: a broken dependency chain traps (launch error) instead of
-// hanging the GPU.
-__device__ __forceinline__ void spin_until(const int* p, int target) {
-  for (uint32_t n = 0; ld_acquire(p) < target; ++n) {
-    __nanosleep(32);
-    if (n > (1u << 26)) __trap();
-  }
-}
-// Publish this CTA's prior global writes (made visible to thread 0 by the
-// preceding bar.sync) and count one arrival: one gpu-scope fence per CTA.
-__device__ __forceinline__ int publish_arrive(int* ctr) {
-  int old;
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
-  return old;
-}
-__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-
-__device__ void compute_info(const Params& p, const int64_t* len, Info& I) {
-  const int nseg = p.n_seq * p.hkv;
-  int64_t total = 0;
-  for (int s = 0; s < p.n_seq; ++s) total += (int64_t)p.hkv * (len[s] / kM + 1);
-  const int64_t avail = (int64_t)gridDim.x - nseg;
-  I.active = 0;
-  int acc = 0;
-  for (int sg = 0; sg < nseg; ++sg) {
-    const int s = sg / p.hkv;
-    const int64_t nb = len[s] / kM + 1;
-    int64_t c = 1 + (avail > 0 ? avail * nb / total : 0);
-    if (c > p.cmax) c = p.cmax;
-    if (c > nb) c = nb;
-    if ((int)blockIdx.x < acc + c) {
-      I.active = 1;
-      I.s = s;
-      I.g = sg - s * p.hkv;
-      I.sg = sg;
-      I.piece = (int)blockIdx.x - acc;
-      I.c = (int)c;
-      I.pos = len[s];
-      I.n_cand = nb;
-      I.b0 = I.piece * nb / c;
-      I.b1 = (I.piece + 1) * nb / c;
-      break;
-    }
-    acc += (int)c;
-  }
-  if (!I.active) return;
+__device__ __forceinline__ void seg_info(const Params& p, const int64_t* len, int sg, int rank, int np, Info& I) {
+  I.np = np;
+  I.s = sg / p.hkv;
+  I.g = sg - I.s * p.hkv;
+  I.pos = len[I.s];
+  const int64_t nb = I.pos / kM + 1;
+  I.n_cand = nb;
+  I.b0 = rank * nb / np;
+  I.b1 = (rank + 1) * nb / np;
   const int64_t L = I.pos + 1;
   I.nk = L / kS;                                       // nk_t == nk for the newest row
   I.r0 = I.b0 == 0 ? 0 : 4 * I.b0 - 1;
   I.r1 = 4 * I.b1 < I.nk ? 4 * I.b1 : I.nk;
-  if (I.r1 < I.r0) I.r1 = I.r0;
+  if (I.b1 == I.b0 || I.r1 < I.r0) I.r1 = I.r0;
   I.ntiles = (int)((I.r1 - I.r0 + 127) / 128);
   int64_t first = I.pos < kP ? 0 : (I.pos - kP) / kS + 1;
   const int64_t count_old = I.pos / kS;
@@ -212,19 +149,143 @@ __device__ void compute_info(const Params& p, const int64_t* len, Info& I) {
   I.n_ch = I.budget >= I.n_free ? I.n_free : I.budget;
   I.n_sel = I.n_init + I.n_ch + I.n_loc;
   I.nf = I.n_init + I.n_loc;
-  I.t2 = (I.n_sel + 1) / 2;
+  I.tf = (I.nf + 1) / 2;
+  I.t2 = I.tf + (I.n_ch + 1) / 2;
 }
 
-// Stage-2 order: forced blocks first (init, then local), then the chosen ones.
-__device__ __forceinline__ bool tile_needs_sel(const Info& I, int t) {
-  const int e1 = 2 * t + 1 < I.n_sel ? 2 * t + 1 : 2 * t;
-  return e1 >= I.nf;
+// Stage-2 tiles: t < tf hold forced entries (init, then local) 2t, 2t+1; t >= tf
+// hold chosen entries 2(t-tf), 2(t-tf)+1.  Forced tiles are owned from the last
+// piece down, chosen ones from piece 0 up (round robin).
+__device__ __forceinline__ int tile_owner(const Info& I, int t) {
+  return t < I.tf ? (((I.np - 1 - t) % I.np) + I.np) % I.np : (t - I.tf) % I.np;
 }
-__device__ __forceinline__ int entry_block(const Info& I, const int* sel_s, int e) {
-  if (e >= I.n_sel) return -1;
-  if (e < I.n_init) return e;
-  if (e < I.nf) return I.local_lo + (e - I.n_init);
-  return sel_s[I.n_init + (e - I.nf)];
+__device__ __forceinline__ int tile_blocks(const Info& I, int t) {
+  const int n = t < I.tf ? I.nf - 2 * t : I.n_ch - 2 * (t - I.tf);
+  return n >= 2 ? 2 : n;
+}
+__device__ __forceinline__ int tile_block(const Info& I, const int* sel_s, int t, int x) {
+  if (x >= tile_blocks(I, t)) return -1;
+  if (t < I.tf) {
+    const int e = 2 * t + x;
+    return e < I.n_init ? e : I.local_lo + (e - I.n_init);
+  }
+  return sel_s[I.n_init + 2 * (t - I.tf) + x];
+}
+
+// ---------------------------------------------------------------- cluster / sync helpers
+// Optional phase timeline (INFLLM2_DECODE_TRACE=1): %globaltimer per CTA and
+// phase of the first segment, read back with infllm2_debug_decode_trace
+// (tools/decode_trace.py).  `on` = launch number + 1; the last kTraceRing
+// launches are kept.
+constexpr int kTracePts = 16;
+constexpr int kTraceRing = 4;
+constexpr int kTraceCtas = 160;
+__device__ unsigned long long g_trace[kTraceRing * kTraceCtas * kTracePts];
+__device__ __forceinline__ void trace(int on, int pt) {
+  if (on && blockIdx.x < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[(((on - 1) % kTraceRing) * kTraceCtas + blockIdx.x) * kTracePts + pt] = t;
+  }
+}
+
+__device__ long long g_cyc[kTraceCtas * 32];
+#define CYC(k)                                                                        \
+  do {                                                                                \
+    if (tr && tid == 0 && blockIdx.x < kTraceCtas) g_cyc[blockIdx.x * 32 + (k)] = clock64(); \
+  } while (0)
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+// One arrival (release at cluster scope) on the same barrier of every CTA of
+// the cluster: called by a whole warp after a CTA barrier; lane r signals CTA r,
+// so the eight remote arrivals are in flight together.
+__device__ __forceinline__ void arrive_all(uint64_t* bar, int lane, int np) {
+  if (lane < np)
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(map_rank(smem_u32(bar), lane))
+                 : "memory");
+  __syncwarp();
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ float ld_dsmem(const float* local, uint32_t rank) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(map_rank(smem_u32(local), rank)));
+  return v;
+}
+__device__ __forceinline__ float2 ld_dsmem2(const float* local, uint32_t rank) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
+               : "=f"(v.x), "=f"(v.y)
+               : "r"(map_rank(smem_u32(local), rank)));
+  return v;
+}
+// Reduce-scatter of 16 per-lane values across a warp in 16 shuffles (instead of
+// 16 x 5 butterflies): returns the warp-wide reduction of head
+// reduce_head(lane); lanes l and l^1 hold the same head.
+__device__ __forceinline__ int reduce_head(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+template <typename Op>
+__device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane, Op op) {
+#pragma unroll
+  for (int w = 8, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
+    }
+  }
+  return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+}
+// Same for (max, sum 2^(x - max)) pairs.
+__device__ __forceinline__ void lse_merge(float& m, float& s, float om, float os) {
+  const float nm = fmaxf(m, om);
+  s = (m == -INFINITY ? 0.f : s * ex2(m - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
+  m = nm;
+}
+__device__ __forceinline__ void warp_reduce16_lse(float (&m)[16], float (&s)[16], int lane) {
+#pragma unroll
+  for (int w = 8, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float sm_ = up ? m[i] : m[i + w], ss_ = up ? s[i] : s[i + w];
+      float km = up ? m[i + w] : m[i], ks = up ? s[i + w] : s[i];
+      lse_merge(km, ks, __shfl_xor_sync(0xffffffffu, sm_, off), __shfl_xor_sync(0xffffffffu, ss_, off));
+      m[i] = km;
+      s[i] = ks;
+    }
+  }
+  lse_merge(m[0], s[0], __shfl_xor_sync(0xffffffffu, m[0], 1), __shfl_xor_sync(0xffffffffu, s[0], 1));
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ int publish_arrive(int* ctr) {
+  int old;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+  return old;
 }
 
 // Local top-`budget` of r[lo..hi) (indices relative to block id base) by
@@ -266,6 +327,7 @@ __device__ void local_topk(const float* r, int64_t base, int lo, int hi, int bud
         rk = lkey[x];
         bk = lid[x];
         int rank = 0;
+#pragma unroll 8
         for (int f = 0; f < cnt; ++f) rank += topk::better(lkey[f], lid[f], rk, bk) ? 1 : 0;
         keep = rank < budget;
       }
@@ -294,54 +356,115 @@ __device__ void local_topk(const float* r, int64_t base, int lo, int hi, int bud
   }
 }
 
+// Top-`budget` (<= 32) of r[lo..hi) by (score desc, id asc), id = base + index,
+// computed by the 128 epilogue threads (named barrier 1).  A threshold T0 with
+// >= budget values reaching it bounds the answer to {r >= T0}; that set is
+// compacted and ranked, and the
+// result is written SORTED: out[2k], out[2k+1] = key, id bits of the k-th best
+// (id -1 padding when fewer than `budget` values).  Returns false (nothing
+// written) if the threshold set overflows `cap` (massive exact ties).
+__device__ bool cta_topk(const float* r, int64_t base, int lo, int hi, int budget, int tid, int lane, int wq,
+                         float* scratch, int* cnt, float* out) {
+  const int n = hi - lo;
+  float* wmax = scratch;                                  // [4]
+  float* lk = scratch + 128;                              // [cap][2]
+  const int cap = 256;
+  if (n <= budget) {
+    // fewer candidates than the budget: all of them (order irrelevant: list not full)
+    for (int x = tid; x < budget; x += 128) {
+      out[2 * x] = x < n ? r[lo + x] : -1.f;
+      out[2 * x + 1] = __int_as_float(x < n ? (int)(base + lo + x) : -1);
+    }
+    return true;
+  }
+  float m = -1.f;
+  for (int b = lo + tid; b < hi; b += 128) m = fmaxf(m, r[b]);
+  const float ws = topk::warp_sort_desc(m, lane);
+  if (tid == 0) *cnt = 0;
+  // T0 = max over the 4 warps of the warp's budget-th largest thread maximum:
+  // that warp alone has >= budget values >= T0, so the top-budget set lies in
+  // {r >= T0} (no exact order statistic needed)
+  if (lane == budget - 1) wmax[wq] = ws;
+  named_bar_sync(1, 128);
+  const float t0 = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
+  for (int b = lo + tid; b < hi; b += 128) {
+    const float v = r[b];
+    if (v >= t0) {
+      const int slot = atomicAdd(cnt, 1);
+      if (slot < cap) { lk[2 * slot] = v; lk[2 * slot + 1] = __int_as_float((int)(base + b)); }
+    }
+  }
+  named_bar_sync(1, 128);
+  const int mm = *cnt;
+  if (mm > cap) return false;
+  for (int x = tid; x < mm; x += 128) {
+    const float rk = lk[2 * x];
+    const int bk = __float_as_int(lk[2 * x + 1]);
+    int rank = 0;
+#pragma unroll 8
+    for (int y = 0; y < mm; ++y) rank += topk::better(lk[2 * y], __float_as_int(lk[2 * y + 1]), rk, bk) ? 1 : 0;
+    if (rank < budget) { out[2 * rank] = rk; out[2 * rank + 1] = __int_as_float(bk); }
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
+decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
   uint64_t* full = bars;                 // [3]
   uint64_t* empty = bars + 3;            // [3]
   uint64_t* q_full = bars + 6;
-  uint64_t* appended = bars + 7;         // 128 epilogue arrivals
-  uint64_t* s2_full = bars + 8;
-  uint64_t* s2_empty = bars + 9;         // 4 warps
-  uint64_t* p_full = bars + 10;          // 4 warps
-  uint64_t* o_full = bars + 11;
-  uint64_t* o_empty = bars + 12;         // 4 warps
-  uint64_t* sel_ready = bars + 13;       // selection merged into sel_s
-  uint64_t* s_full = bars + 16;          // [kMaxTiles], one phase each
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + kMaxTiles);
+  uint64_t* q_empty = bars + 7;
+  uint64_t* appended = bars + 8;         // 128 epilogue arrivals
+  uint64_t* z_free = bars + 9;           // 128 epilogue arrivals: z tiles read, TMEM reusable
+  uint64_t* s2_full = bars + 10;
+  uint64_t* s2_empty = bars + 11;        // 4 warps
+  uint64_t* p_full = bars + 12;          // 4 warps
+  uint64_t* o_full = bars + 13;
+  uint64_t* o_empty = bars + 14;         // 4 warps
+  uint64_t* sel_ready = bars + 15;       // selection merged into sel_s
+  uint64_t* x1 = bars + 16;              // cluster exchanges: 8 arrivals each
+  uint64_t* x2 = bars + 17;
+  uint64_t* x3 = bars + 18;
+  uint64_t* s_full = bars + 24;          // [kMaxTiles], one phase per segment
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24 + kMaxTiles);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
-  __shared__ Info I;
-  __shared__ int s_flag;
-  __shared__ int sel_s[96];              // this segment's selection (every piece merges it)
+  float* xpart = reinterpret_cast<float*>(smem + Smem::xch);          // [16][2] (max, sum 2^z)
+  float* xcand = xpart + 2 * kG;                                      // [budget][2] (key, id bits)
+  __shared__ int sel_s[96];
+  __shared__ int64_t len_s[kMaxSeq];
+  __shared__ int s_cnt;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  uint32_t np_u;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(np_u));
+  const int P = (int)np_u;
+  const int ncl = gridDim.x / P;
+  const int cid = blockIdx.x / P;
+  const int nseg = p.n_seq * p.hkv;
   const TableView tv = table_view(p.table, p.n_seq);
-  {
-    int64_t* len_s = reinterpret_cast<int64_t*>(smem + Smem::sarr);   // free until phase C
-    for (int s = threadIdx.x; s < p.n_seq; s += blockDim.x) len_s[s] = tv.len[s];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      trace(p.trace, 0);
-      if (p.trace) {
-        unsigned int smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_trace[(((p.trace - 1) % kTraceRing) * kMaxPieces + blockIdx.x) * kTracePts + 11] = smid;
-      }
-      compute_info(p, len_s, I);
-    }
-  }
+  for (int s = threadIdx.x; s < p.n_seq; s += blockDim.x) len_s[s] = tv.len[s];
   if (threadIdx.x == 0) {
+    trace(p.trace, 0);
+    if (p.trace && blockIdx.x < kTraceCtas)
+      g_trace[(((p.trace - 1) % kTraceRing) * kTraceCtas + blockIdx.x) * kTracePts + 15] = clock64();
     for (int i = 0; i < kStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     mbar_init(appended, 128);
+    mbar_init(z_free, 128);
     mbar_init(s2_full, 1);
     mbar_init(s2_empty, 4);
     mbar_init(p_full, 4);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 4);
     mbar_init(sel_ready, 1);
+    mbar_init(x1, P);
+    mbar_init(x2, P);
+    mbar_init(x3, P);
     for (int t = 0; t < kMaxTiles; ++t) mbar_init(s_full + t, 1);
     fence_barrier_init();
     tma_prefetch(&tm_q);
@@ -349,28 +472,35 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();                    // barrier inits visible to the cluster before any remote arrival
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  int* seg_ctr = tv.fused + 4 * (I.active ? I.sg : 0);   // [0] stage-1, [1] candidates, [3] stage-2
-  const SeqDesc ds = tv.desc[I.active ? I.s : 0];
-  int32_t* sel_row = p.selection + (int64_t)(I.active ? I.sg : 0) * p.max_sel;   // output
 
-  if (I.active) {
-    if (warp == 0) {
-      // ============================================================ producer
-      if (elect_one()) {
+  if (warp == 0) {
+    // ============================================================ producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int sg = cid; sg < nseg; sg += ncl, ++it) {
+        Info I;
+        seg_info(p, len_s, sg, rank, P, I);
+        const uint32_t par = it & 1;
         const CUtensorMap* mhi = tv.maps + (int64_t)kMaps * I.s + 2;
         const CUtensorMap* mlo = tv.maps + (int64_t)kMaps * I.s + 3;
         const CUtensorMap* mk = tv.maps + (int64_t)kMaps * I.s + 0;
         const CUtensorMap* mv = tv.maps + (int64_t)kMaps * I.s + 1;
+        tma_prefetch(mhi);
+        tma_prefetch(mlo);
+        tma_prefetch(mk);
+        tma_prefetch(mv);
+        mbar_wait(q_empty, par ^ 1);
         mbar_arrive_expect_tx(q_full, kQB);
         uint8_t* qd = smem + Smem::q;
         tma_load_3d(qd, &tm_q, q_full, 0, I.g * kG, I.s);
         tma_load_3d(qd + kQB / 2, &tm_q, q_full, 64, I.g * kG, I.s);
-        int stage = 0;
-        uint32_t phase = 0;
         for (int t = 0; t < I.ntiles; ++t) {
-          if (t == I.dirty_tile) mbar_wait(appended, 0);   // this CTA's window re-sync is in global memory
+          if (t == I.dirty_tile) mbar_wait(appended, par);   // this CTA's window re-sync is in global memory
           mbar_wait(empty + stage, phase ^ 1);
           mbar_arrive_expect_tx(full + stage, kStageBytes);
           uint8_t* dst = smem + Smem::ring + stage * kStageBytes;
@@ -381,15 +511,16 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
           tma_load_3d(dst + 3 * kHalf, mlo, full + stage, 64, row, I.g);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        trace(p.trace, 1);
-        for (int t = I.piece; t < I.t2; t += I.c) {
-          // K/V row of this step is written before the segment's stage-1 counter completes
-          if (tile_needs_sel(I, t)) mbar_wait(sel_ready, 0);   // implies the segment's stage 1 is complete
-          else spin_until(seg_ctr + 0, I.c);
+        if (it == 0) trace(p.trace, 1);
+        for (int t = 0; t < I.t2; ++t) {
+          if (tile_owner(I, t) != (int)rank) continue;
+          // the K/V row of this step (piece 7) is published with the stage-1 exchange
+          if (t < I.tf) mbar_wait_cluster(x1, par);
+          else mbar_wait(sel_ready, par);
           fence_proxy_async_global();
-          if (t == I.piece) trace(p.trace, 7);
-          const int b0 = entry_block(I, sel_s, 2 * t), b1 = entry_block(I, sel_s, 2 * t + 1);
-          const int nt = b1 >= 0 ? 2 : 1;
+          if (it == 0) trace(p.trace, 7);
+          const int nt = tile_blocks(I, t);
+          const int b0 = tile_block(I, sel_s, t, 0), b1 = tile_block(I, sel_s, t, 1);
           mbar_wait(empty + stage, phase ^ 1);
           mbar_arrive_expect_tx(full + stage, nt * 4 * (kM * 128));
           uint8_t* kd = smem + Smem::ring + stage * kStageBytes;
@@ -405,15 +536,23 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
-      __syncwarp();
-    } else if (warp == 1) {
-      // ============================================================ MMA issuer
-      const uint32_t idesc = idesc_bf16_f32(128, kG);
-      const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
-      mbar_wait(q_full, 0);
-      const uint32_t q_addr = smem_u32(smem + Smem::q);
-      int stage = 0;
-      uint32_t phase = 0;
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ============================================================ MMA issuer
+    const uint32_t idesc = idesc_bf16_f32(128, kG);
+    const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
+    const uint32_t q_addr = smem_u32(smem + Smem::q);
+    int stage = 0;
+    uint32_t phase = 0;
+    int i2 = 0;
+    int it = 0;
+    for (int sg = cid; sg < nseg; sg += ncl, ++it) {
+      Info I;
+      seg_info(p, len_s, sg, rank, P, I);
+      const uint32_t par = it & 1;
+      mbar_wait(q_full, par);
+      if (it > 0) mbar_wait(z_free, par ^ 1);      // previous segment's z tiles have been read
       for (int t = 0; t < I.ntiles; ++t) {
         mbar_wait(full + stage, phase);
         tc_fence_after();
@@ -431,25 +570,28 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-      int i2 = 0;
-      for (int t = I.piece; t < I.t2; t += I.c, ++i2) {
-        const int nt = (I.n_sel - 2 * t) >= 2 ? 2 : 1;
-        const uint32_t par = i2 & 1;
+      int ti = 0;                                      // this piece's tile index within the segment
+      for (int t = 0; t < I.t2; ++t) {
+        if (tile_owner(I, t) != (int)rank) continue;
+        const int nt = tile_blocks(I, t);
+        const uint32_t tp = i2 & 1;                    // per-tile barrier parity (running count)
+        ++i2;
         mbar_wait(full + stage, phase);
-        mbar_wait(s2_empty, par ^ 1);
+        mbar_wait(s2_empty, tp ^ 1);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(smem + Smem::ring + stage * kStageBytes);
         if (elect_one()) {
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
             const uint32_t qoff = (k >> 2) * (kQB / 2) + (k & 3) * 32;
-            umma_f16_ss(tmem + kColS2, sdesc_k_sw128(k_addr + off), sdesc_k_sw128(q_addr + qoff), idesc, k > 0 ? 1u : 0u);
+            umma_f16_ss(tmem + kColS2, sdesc_k_sw128(k_addr + off), sdesc_k_sw128(q_addr + qoff), idesc,
+                        k > 0 ? 1u : 0u);
           }
           umma_commit(s2_full);
         }
         __syncwarp();
-        mbar_wait(p_full, par);
-        mbar_wait(o_empty, par ^ 1);
+        mbar_wait(p_full, tp);
+        if (ti == 0) mbar_wait(o_empty, par ^ 1);    // the previous segment's O has been read
         tc_fence_after();
         if (elect_one()) {
           const uint32_t v_addr = k_addr + 2 * kHalf;
@@ -457,30 +599,49 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
           const int ksteps = nt == 2 ? 8 : 4;
           for (int k = 0; k < ksteps; ++k) {
             const uint64_t vdesc = sdesc_mn_sw128(v_addr + k * 2048, kHalf, 1024);
-            umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv, k > 0 ? 1u : 0u);
+            umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv,
+                        (ti > 0 || k > 0) ? 1u : 0u);
             umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + kPHalf + k * 512, 256, 128), idesc_pv, 1u);
           }
           umma_commit(empty + stage);
-          umma_commit(o_full);
+          umma_commit(o_full);                         // after every PV: P buffer free, O stable
         }
         __syncwarp();
+        ++ti;
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-    } else {
-      // ============================================================ epilogue (128 threads)
-      const int tid = threadIdx.x - 64;
-      const int quad = warp & 3;
-      const int row = quad * 32 + lane;                // TMEM lane
-      const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+      if (elect_one()) umma_commit(q_empty);          // every MMA reading this segment's Q is issued
+      __syncwarp();
+    }
+  } else {
+    // ============================================================ epilogue (128 threads)
+    const int tid = threadIdx.x - 64;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;                // TMEM lane
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    float* red_m = red;
+    float* red_s = red + 4 * kG;
+    float* lse2 = red + 8 * kG;
+    float* sarr = reinterpret_cast<float*>(smem + Smem::sarr);
+    float* rarr = reinterpret_cast<float*>(smem + Smem::rarr);
+    int i2 = 0;
+    int it = 0;
+    uint32_t sfpar = 0;                              // bit t: parity of the next s_full[t] phase
+    for (int sg = cid; sg < nseg; sg += ncl, ++it) {
+      Info I;
+      seg_info(p, len_s, sg, rank, P, I);
+      const uint32_t par = it & 1;
+      const int tr = it == 0 ? p.trace : 0;
+      const SeqDesc ds = tv.desc[I.s];
       const int64_t L = I.pos + 1;
-      // ---- A. append: dirty windows in [r0, r1) (+ K/V row and coarse window on the last piece)
+      // ---- A. append: dirty windows in [r0, r1) (+ K/V row and coarse window on piece 7)
       const int d = tid;
       const __nv_bfloat16* kg = ds.k + (int64_t)I.g * ds.cap * kD;
       const int64_t knew_idx = ((int64_t)I.s * p.hkv + I.g) * kD + d;
       {
         // at most two fine windows change (nk - dlo <= 2): their <= 48 rows are
-        // loaded in ONE round (latency under the stage-1 stream is microseconds),
-        // summed as window_mean does (sequential float64, numpy reduce order)
+        // loaded in ONE round, summed as window_mean does (sequential float64,
+        // numpy reduce order)
         const int64_t jlo = I.dlo > I.r0 ? I.dlo : I.r0;
         if (jlo < I.r1) {
           const float knew = __bfloat162float(p.k_new[knew_idx]);
@@ -495,7 +656,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
           for (int i = 0; i < kP + kS; ++i)
             if (row0 + i == I.pos) x[i] = knew;
           auto emit = [&](int64_t j, const float* xs) {
-            int64_t w64 = L - j * kS;
+            const int64_t w64 = L - j * kS;
             const int w = (int)(w64 < kP ? w64 : kP);
             double acc = (double)xs[0];
 #pragma unroll
@@ -513,8 +674,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
         }
         fence_proxy_async_global();
         mbar_arrive(appended);
-        if (tid == 0) trace(p.trace, 13);
-        if (I.piece == I.c - 1) {   // not needed by stage 1: after the arrival
+        if (tid == 0) trace(tr, 13);
+        if ((int)rank == P - 1) {   // not needed by stage 1: after the arrival
           const float knew = __bfloat162float(p.k_new[knew_idx]);
           ds.k[((int64_t)I.g * ds.cap + I.pos) * kD + d] = p.k_new[knew_idx];
           ds.v[((int64_t)I.g * ds.cap + I.pos) * kD + d] = p.v_new[knew_idx];
@@ -530,48 +691,40 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
       }
       // ---- B. stage-1 partial (max, sum 2^z) over owned kernels [4*b0, r1)
       const int64_t own0 = 4 * I.b0;
-      float m[kG], sm[kG];
+      {
+        float m[kG], sm[kG];
 #pragma unroll
-      for (int h = 0; h < kG; ++h) { m[h] = -INFINITY; sm[h] = 0.f; }
-      for (int t = 0; t < I.ntiles; ++t) {
-        mbar_wait(s_full + t, 0);
-        tc_fence_after();
-        float v[kG];
-        tmem_ld16(tmem + lane_base + t * kG, v);
-        tmem_wait_ld();
-        if (t == 0 && tid == 0) trace(p.trace, 12);
-        const int64_t j = I.r0 + 128 * t + row;
-        if (j >= own0 && j < I.r1) {
+        for (int h = 0; h < kG; ++h) { m[h] = -INFINITY; sm[h] = 0.f; }
+        for (int t = 0; t < I.ntiles; ++t) {
+          mbar_wait(s_full + t, (sfpar >> t) & 1u);
+          sfpar ^= 1u << t;
+          tc_fence_after();
+          float v[kG];
+          tmem_ld16(tmem + lane_base + t * kG, v);
+          tmem_wait_ld();
+          if (t == 0 && tid == 0) trace(tr, 12);
+          const int64_t j = I.r0 + 128 * t + row;
+          if (j >= own0 && j < I.r1) {
 #pragma unroll
-          for (int h = 0; h < kG; ++h) {
-            const float z = v[h] * p.zscale;
-            if (z > m[h]) {
-              sm[h] = sm[h] * ex2(m[h] - z) + 1.f;
-              m[h] = z;
-            } else {
-              sm[h] += ex2(z - m[h]);
+            for (int h = 0; h < kG; ++h) {
+              const float z = v[h] * p.zscale;
+              if (z > m[h]) {
+                sm[h] = sm[h] * ex2(m[h] - z) + 1.f;
+                m[h] = z;
+              } else {
+                sm[h] += ex2(z - m[h]);
+              }
             }
           }
         }
-      }
-      float* red_m = red;
-      float* red_s = red + 4 * kG;
-      float* lse2 = red + 8 * kG;
-#pragma unroll
-      for (int h = 0; h < kG; ++h) {
-        float mm = m[h], ss = sm[h];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const float om = __shfl_xor_sync(0xffffffffu, mm, off);
-          const float os = __shfl_xor_sync(0xffffffffu, ss, off);
-          const float nm = fmaxf(mm, om);
-          ss = (mm == -INFINITY ? 0.f : ss * ex2(mm - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
-          mm = nm;
+        warp_reduce16_lse(m, sm, lane);
+        if ((lane & 1) == 0) {
+          const int h = reduce_head(lane);
+          red_m[h * 4 + quad] = m[0];
+          red_s[h * 4 + quad] = sm[0];
         }
-        if (lane == 0) { red_m[h * 4 + quad] = mm; red_s[h * 4 + quad] = ss; }
       }
       named_bar_sync(1, 128);
-      float* ps_seg = p.pstat + (int64_t)I.sg * kMaxPieces * (2 * kG);
       if (tid < kG) {
         float M = -INFINITY;
         for (int x = 0; x < 4; ++x) M = fmaxf(M, red_m[tid * 4 + x]);
@@ -580,42 +733,46 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
           const float mm = red_m[tid * 4 + x];
           if (mm != -INFINITY) S += red_s[tid * 4 + x] * ex2(mm - M);
         }
-        ps_seg[I.piece * 2 * kG + 2 * tid] = M;
-        ps_seg[I.piece * 2 * kG + 2 * tid + 1] = S;
+        xpart[2 * tid] = M;
+        xpart[2 * tid + 1] = S;
       }
       named_bar_sync(1, 128);
-      if (tid == 0) {
-        trace(p.trace, 2);
-        publish_arrive(seg_ctr + 0);
-        spin_until(seg_ctr + 0, I.c);
-        trace(p.trace, 3);
-      }
-      named_bar_sync(1, 128);
-      // ---- C. LSE, group scores, block scores, local top-k
-      float* sarr = reinterpret_cast<float*>(smem + Smem::sarr);
-      for (int x = tid; x < I.c * 2 * kG; x += 128) sarr[x] = __ldcg(ps_seg + x);   // all partials in flight
-      named_bar_sync(1, 128);
-      if (tid < kG) {
+      if (tid == 0) trace(tr, 2);
+      if (warp == 2) arrive_all(x1, lane, P);
+      mbar_wait_cluster(x1, par);
+      if (tid == 0) trace(tr, 3);
+      CYC(0);
+      // ---- C. LSE (all pieces' partials over DSMEM), group scores, block scores, local top-k
+      {
+        const int h = tid >> 3, r = tid & 7;           // 16 heads x 8 pieces
         float M = -INFINITY, S = 0.f;
-        for (int x = 0; x < I.c; ++x) {
-          const float mm = sarr[x * 2 * kG + 2 * tid], ss = sarr[x * 2 * kG + 2 * tid + 1];
-          if (mm == -INFINITY) continue;
-          const float nm = fmaxf(M, mm);
-          S = (M == -INFINITY ? 0.f : S * ex2(M - nm)) + ss * ex2(mm - nm);
+        if (r < P) {
+          const float2 ms = ld_dsmem2(xpart + 2 * h, r);
+          M = ms.x;
+          S = ms.y;
+        }
+#pragma unroll
+        for (int off = 1; off < 8; off <<= 1) {
+          const float om = __shfl_xor_sync(0xffffffffu, M, off);
+          const float os = __shfl_xor_sync(0xffffffffu, S, off);
+          const float nm = fmaxf(M, om);
+          S = (M == -INFINITY ? 0.f : S * ex2(M - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
           M = nm;
         }
-        lse2[tid] = M == -INFINITY ? INFINITY : M + log2f(S);
+        if (r == 0) lse2[h] = M == -INFINITY ? INFINITY : M + log2f(S);
       }
       named_bar_sync(1, 128);
-      float* rarr = reinterpret_cast<float*>(smem + Smem::rarr);
+      CYC(1);
       {
         float l2[kG];
 #pragma unroll
         for (int h = 0; h < kG; ++h) l2[h] = lse2[h];
         tc_fence_after();
-        for (int t = 0; t < I.ntiles; ++t) {
-          float v[kG];
+        // two TMEM tiles per wait: the load latency is paid once per pair
+        for (int t = 0; t < I.ntiles; t += 2) {
+          float v[kG], w[kG];
           tmem_ld16(tmem + lane_base + t * kG, v);
+          if (t + 1 < I.ntiles) tmem_ld16(tmem + lane_base + (t + 1) * kG, w);
           tmem_wait_ld();
           const int64_t jl = 128 * t + row;
           if (I.r0 + jl < I.r1) {
@@ -624,7 +781,16 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
             for (int h = 0; h < kG; ++h) a += ex2(v[h] * p.zscale - l2[h]);
             sarr[jl] = a * (1.0f / kG);
           }
+          if (t + 1 < I.ntiles && I.r0 + jl + 128 < I.r1) {
+            float a = 0.f;
+#pragma unroll
+            for (int h = 0; h < kG; ++h) a += ex2(w[h] * p.zscale - l2[h]);
+            sarr[jl + 128] = a * (1.0f / kG);
+          }
         }
+        CYC(2);
+        tc_fence_before();
+        mbar_arrive(z_free);
       }
       named_bar_sync(1, 128);
       for (int64_t b = I.b0 + tid; b < I.b1; b += 128) {
@@ -640,123 +806,38 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
         rarr[b - I.b0] = r;
       }
       named_bar_sync(1, 128);
-      if (tid == 0) trace(p.trace, 4);
+      if (tid == 0) trace(tr, 4);
+      CYC(3);
       const bool dense = I.budget >= I.n_free || I.budget == 0;
-      float* cand_seg = p.cand + (int64_t)I.sg * kMaxPieces * 64;
-      if (!dense && warp == 2) {
+      if (!dense) {
         int lo = (int)((I.b0 > I.n_init ? I.b0 : I.n_init) - I.b0);
         int hi = (int)((I.b1 < I.local_lo ? I.b1 : I.local_lo) - I.b0);
         if (hi < lo) hi = lo;
-        float* lkey = reinterpret_cast<float*>(smem + Smem::p);
-        int* lid = reinterpret_cast<int*>(lkey + topk::kListCap);
-        local_topk(rarr, I.b0, lo, hi, I.budget, lane, lkey, lid, cand_seg + I.piece * 64);
+        float* scratch = reinterpret_cast<float*>(smem + Smem::p);
+        if (!cta_topk(rarr, I.b0, lo, hi, I.budget, tid, lane, warp - 2, scratch, &s_cnt, xcand) && warp == 2) {
+          float* lkey = scratch;
+          int* lid = reinterpret_cast<int*>(lkey + topk::kListCap);
+          local_topk(rarr, I.b0, lo, hi, I.budget, lane, lkey, lid, xcand);   // massive ties: exact fallback
+        }
       }
       named_bar_sync(1, 128);
       if (tid == 0) {
-        trace(p.trace, 5);
-        publish_arrive(seg_ctr + 1);
-        spin_until(seg_ctr + 1, I.c);
+        trace(tr, 5);
+        CYC(4);
       }
-      named_bar_sync(1, 128);
-      {
-        // ---- merge (every piece, redundantly: no publish hop): the global
-        // top-B lies in the union of the pieces' local top-B lists
-        float* lk = sarr;                                         // [n][2] (key, id bits)
-        int* chosen = reinterpret_cast<int*>(smem + Smem::p);    // flags (P buffer is idle here)
-        const int n = dense ? 0 : I.c * I.budget;
-        for (int x = tid; x < n; x += 128) {
-          const int off = 2 * x + (x / I.budget) * (64 - 2 * I.budget);
-          const float2 kv = __ldcg(reinterpret_cast<const float2*>(cand_seg + off));
-          lk[2 * x] = kv.x;
-          lk[2 * x + 1] = kv.y;
-        }
-        named_bar_sync(1, 128);
-        // Filter: a full local list's worst key tau_i is <= the global B-th
-        // best (that list alone has B keys >= tau_i), so keys < max_i tau_i
-        // cannot be selected.  Typically leaves ~B..2B of the c*B candidates.
-        int* cnt = reinterpret_cast<int*>(red + 8 * kG + kG);     // after lse2
-        float* fl = rarr;                                          // filtered (key, id) pairs
-        const int fcap = (kMaxPieceBlocks + 8) / 2;
-        if (tid == 0) *cnt = 0;
-        float tau = -INFINITY;
-        for (int i = tid; i < (dense ? 0 : I.c); i += 128) {
-          float mn = INFINITY;
-          bool full_list = true;
-          for (int k = 0; k < I.budget; ++k) {
-            full_list &= __float_as_int(lk[2 * (i * I.budget + k) + 1]) >= 0;
-            mn = fminf(mn, lk[2 * (i * I.budget + k)]);
-          }
-          if (full_list) tau = fmaxf(tau, mn);
-        }
+      // ---- D (part 1). stage-2 state of this piece: all its tiles accumulate
+      // into one O^T in TMEM with a running per-head max (rescaled only when a
+      // tile's max exceeds it by more than 2^8), per-thread row sums
+      float m_run[kG], lrow[kG];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, off));
-        if (lane == 0) red_m[quad] = tau;
-        named_bar_sync(1, 128);
-        tau = fmaxf(fmaxf(red_m[0], red_m[1]), fmaxf(red_m[2], red_m[3]));
-        for (int x = tid; x < n; x += 128) {
-          const float k = lk[2 * x];
-          const int id = __float_as_int(lk[2 * x + 1]);
-          if (id >= 0 && k >= tau) {
-            const int slot = atomicAdd(cnt, 1);
-            if (slot < fcap) { fl[2 * slot] = k; fl[2 * slot + 1] = lk[2 * x + 1]; }
-          }
-        }
-        named_bar_sync(1, 128);
-        const int m = *cnt;
-        const bool use_f = m <= fcap;
-        const float* L2 = use_f ? fl : lk;
-        const int nn = use_f ? m : n;
-        for (int x = tid; x < nn; x += 128) {
-          const float rk = L2[2 * x];
-          const int bk = __float_as_int(L2[2 * x + 1]);
-          int keep = 0;
-          if (bk >= 0 && rk >= tau) {
-            int rank = 0;
-#pragma unroll 8
-            for (int y = 0; y < nn; ++y) {
-              const int by = __float_as_int(L2[2 * y + 1]);
-              rank += (by >= 0 && topk::better(L2[2 * y], by, rk, bk)) ? 1 : 0;
-            }
-            keep = rank < I.budget;
-          }
-          chosen[x] = keep ? bk : -1;
-        }
-        named_bar_sync(1, 128);
-        for (int x = tid; x < nn; x += 128) {
-          const int bk = chosen[x];
-          if (bk < 0) continue;
-          int posn = 0;
-#pragma unroll 8
-          for (int y = 0; y < nn; ++y) {
-            const int cy = chosen[y];
-            posn += (cy >= 0 && cy < bk) ? 1 : 0;
-          }
-          sel_s[I.n_init + posn] = bk;
-        }
-        for (int x = tid; x < p.max_sel; x += 128) {
-          int id = -2;
-          if (dense) id = x < I.n_cand ? x : -1;
-          else if (x < I.n_init) id = x;
-          else if (x >= I.n_init + I.n_ch && x < I.n_sel) id = I.local_lo + (x - I.n_init - I.n_ch);
-          else if (x >= I.n_sel) id = -1;
-          if (id != -2) sel_s[x] = id;
-        }
-        named_bar_sync(1, 128);
-        if (tid == 0) {
-          mbar_arrive(sel_ready);
-          trace(p.trace, 6);
-        }
-        if (I.piece == 0)
-          for (int x = tid; x < p.max_sel; x += 128) sel_row[x] = sel_s[x];
-      }
-      // ---- D. stage 2 (this piece's tiles)
-      const float c2 = p.zscale;
-      int i2 = 0;
-      float* part_seg = p.part + (int64_t)I.sg * kMaxT2 * kPartStride;
-      for (int t = I.piece; t < I.t2; t += I.c, ++i2) {
-        const uint32_t par = i2 & 1;
-        const int bx = entry_block(I, sel_s, 2 * t + (row >> 6));
-        mbar_wait(s2_full, par);
+      for (int h = 0; h < kG; ++h) { m_run[h] = -INFINITY; lrow[h] = 0.f; }
+      int ti = 0;
+      uint32_t tp_prev = 0;
+      auto stage2_tile = [&](int t) {
+        const uint32_t tp = i2 & 1;
+        ++i2;
+        const int bx = tile_block(I, sel_s, t, row >> 6);
+        mbar_wait(s2_full, tp);
         tc_fence_after();
         float z[kG];
         tmem_ld16(tmem + lane_base + kColS2, z);
@@ -766,28 +847,56 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
         if (lane == 0) mbar_arrive(s2_empty);
         const bool valid = bx >= 0 && (int64_t)bx * kM + (row & 63) <= I.pos;
 #pragma unroll
-        for (int h = 0; h < kG; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
-        // tile max per head across the 128 rows
+        for (int h = 0; h < kG; ++h) z[h] = valid ? z[h] * p.zscale : -INFINITY;
+        {
+          float zz[kG];
 #pragma unroll
-        for (int h = 0; h < kG; ++h) {
-          float v = z[h];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == h) red_m[quad * kG + h] = v;
+          for (int h = 0; h < kG; ++h) zz[h] = z[h];
+          const float v = warp_reduce16(zz, lane, [](float a, float b) { return fmaxf(a, b); });
+          if ((lane & 1) == 0) red_m[quad * kG + reduce_head(lane)] = v;
         }
         named_bar_sync(1, 128);
-        float mt[kG];
+        float mnew[kG];
+        bool need = ti == 0;
 #pragma unroll
-        for (int h = 0; h < kG; ++h)
-          mt[h] = fmaxf(fmaxf(red_m[h], red_m[kG + h]), fmaxf(red_m[2 * kG + h], red_m[3 * kG + h]));
+        for (int h = 0; h < kG; ++h) {
+          const float tm = fmaxf(fmaxf(red_m[h], red_m[kG + h]), fmaxf(red_m[2 * kG + h], red_m[3 * kG + h]));
+          mnew[h] = fmaxf(m_run[h], tm);
+          need |= tm > m_run[h] + 8.f;
+        }
+        named_bar_sync(1, 128);                        // red_m reads done
+        if (ti > 0) {
+          mbar_wait(o_full, tp_prev);                  // PV of the previous tile: P buffer free, O stable
+          tc_fence_after();
+        }
+        if (need) {
+          float corr[kG];
+          bool any = false;
+#pragma unroll
+          for (int h = 0; h < kG; ++h) {
+            corr[h] = m_run[h] == -INFINITY ? 0.f : ex2(m_run[h] - mnew[h]);
+            any |= ti > 0 && corr[h] != 1.f;
+            lrow[h] *= corr[h];
+            m_run[h] = mnew[h];
+          }
+          if (any) {
+            float o[kG];
+            tmem_ld16(tmem + lane_base + kColO, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int h = 0; h < kG; ++h) o[h] *= corr[h];
+            tmem_st16(tmem + lane_base + kColO, o);
+            tmem_wait_st();
+            tc_fence_before();
+          }
+        }
         uint32_t phi[kG / 2], plo[kG / 2];
-        float pl[kG];
 #pragma unroll
         for (int h = 0; h < kG; h += 2) {
-          const float a = ex2(z[h] - mt[h]);
-          const float b = ex2(z[h + 1] - mt[h + 1]);
-          pl[h] = a;
-          pl[h + 1] = b;
+          const float a = ex2(z[h] - m_run[h]);
+          const float b = ex2(z[h + 1] - m_run[h + 1]);
+          lrow[h] += a;
+          lrow[h + 1] += b;
           const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
           const __nv_bfloat162 lo2 = __floats2bfloat162_rn(a - __low2float(hi2), b - __high2float(hi2));
           phi[h / 2] = *reinterpret_cast<const uint32_t*>(&hi2);
@@ -802,119 +911,191 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
-        // row sums per head
-#pragma unroll
-        for (int h = 0; h < kG; ++h) {
-          float v = pl[h];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          if (lane == h) red_s[quad * kG + h] = v;
+        tp_prev = tp;
+        ++ti;
+      };
+      // forced-only tiles do not depend on the selection: run them while the
+      // candidate exchange is in flight
+      if (warp == 2) arrive_all(x2, lane, P);
+      for (int t = 0; t < I.tf; ++t)
+        if (tile_owner(I, t) == (int)rank) stage2_tile(t);
+      mbar_wait_cluster(x2, par);
+      CYC(5);
+      {
+        // ---- merge (every piece): the global top-B lies in the union of the local lists
+        float* lk = sarr;                                         // [n][2] (key, id bits)
+        int* chosen = reinterpret_cast<int*>(smem + Smem::p);    // P buffer is idle here
+        const int n = dense ? 0 : P * I.budget;
+        for (int x = tid; x < n; x += 128) {
+          const float2 kv = ld_dsmem2(xcand + 2 * (x % I.budget), x / I.budget);
+          lk[2 * x] = kv.x;
+          lk[2 * x + 1] = kv.y;
         }
-        mbar_wait(o_full, par);
-        tc_fence_after();
-        float o[kG];
-        tmem_ld16(tmem + lane_base + kColO, o);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(o_empty);
-        float* pt = part_seg + (int64_t)t * kPartStride;
-        const int d = row;                              // O^T lane == d
+        if (tid == 0) s_cnt = 0;
+        named_bar_sync(1, 128);
+        CYC(6);
+        // a full local list's worst key tau_i is <= the global B-th best (that
+        // list alone has B keys >= tau_i): keys < max_i tau_i cannot be chosen
+        float tau = -INFINITY;
+        if (tid < (dense ? 0 : P)) {
+          float mn = INFINITY;
+          bool full_list = true;
+          for (int k = 0; k < I.budget; ++k) {
+            full_list &= __float_as_int(lk[2 * (tid * I.budget + k) + 1]) >= 0;
+            mn = fminf(mn, lk[2 * (tid * I.budget + k)]);
+          }
+          if (full_list) tau = mn;
+        }
 #pragma unroll
-        for (int h = 0; h < kG; ++h) pt[h * kD + d] = o[h];
-        named_bar_sync(1, 128);                         // red_s complete
-        if (tid < kG) {
-          pt[kG * kD + 2 * tid] = mt[tid];
-          pt[kG * kD + 2 * tid + 1] = red_s[tid] + red_s[kG + tid] + red_s[2 * kG + tid] + red_s[3 * kG + tid];
+        for (int off = 4; off > 0; off >>= 1) tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, off));
+        if (tid == 0) red_m[0] = tau;
+        named_bar_sync(1, 128);
+        tau = red_m[0];
+        CYC(7);
+        float* fl = rarr;                                          // filtered (key, id) pairs
+        for (int x = tid; x < n; x += 128) {
+          const float k = lk[2 * x];
+          const int id = __float_as_int(lk[2 * x + 1]);
+          if (id >= 0 && k >= tau) {
+            const int slot = atomicAdd(&s_cnt, 1);
+            fl[2 * slot] = k;
+            fl[2 * slot + 1] = lk[2 * x + 1];
+          }
+        }
+        named_bar_sync(1, 128);
+        const int m = s_cnt;
+        CYC(8);
+        for (int x = tid; x < m; x += 128) {
+          const float rk = fl[2 * x];
+          const int bk = __float_as_int(fl[2 * x + 1]);
+          int rnk = 0;
+#pragma unroll 8
+          for (int y = 0; y < m; ++y) rnk += topk::better(fl[2 * y], __float_as_int(fl[2 * y + 1]), rk, bk) ? 1 : 0;
+          if (rnk < I.budget) chosen[rnk] = bk;          // ranks are distinct: exactly budget writers
+        }
+        named_bar_sync(1, 128);
+        CYC(9);
+        if (!dense && warp == 2) {
+          // chosen ids ascending (select_topk returns sorted ids, sparse.py:277)
+          const int id = lane < I.budget ? chosen[lane] : INT_MAX;
+          const int srt = topk::warp_sort_asc(id, lane);
+          if (lane < I.budget) sel_s[I.n_init + lane] = srt;
+        }
+        for (int x = tid; x < p.max_sel; x += 128) {
+          int id = -2;
+          if (dense) id = x < I.n_cand ? x : -1;
+          else if (x < I.n_init) id = x;
+          else if (x >= I.n_init + I.n_ch && x < I.n_sel) id = I.local_lo + (x - I.n_init - I.n_ch);
+          else if (x >= I.n_sel) id = -1;
+          if (id != -2) sel_s[x] = id;
         }
         named_bar_sync(1, 128);
         if (tid == 0) {
-          if (i2 == 0) trace(p.trace, 8);
-          s_flag = (publish_arrive(seg_ctr + 3) == I.t2 - 1);
-          if (s_flag) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          mbar_arrive(sel_ready);
+          trace(tr, 6);
+        }
+        CYC(10);
+        if (rank == 0) {
+          int32_t* sel_row = p.selection + (int64_t)sg * p.max_sel;
+          for (int x = tid; x < p.max_sel; x += 128) sel_row[x] = sel_s[x];
+        }
+      }
+      // ---- D (part 2). chosen tiles, then this piece's partial -> shared memory
+      for (int t = I.tf; t < I.t2; ++t)
+        if (tile_owner(I, t) == (int)rank) stage2_tile(t);
+      if (tid == 0 && it == 0) trace(tr, 8);
+      CYC(14);
+      {
+        float* pt = sarr;                                  // [16][128] O^T, [16][2] (max, sum)
+        if (ti > 0) {
+          mbar_wait(o_full, tp_prev);
+          tc_fence_after();
+          float o[kG];
+          tmem_ld16(tmem + lane_base + kColO, o);
+          tmem_wait_ld();
+          tc_fence_before();
+#pragma unroll
+          for (int h = 0; h < kG; ++h) pt[h * kD + row] = o[h];   // O^T lane == d
+          const float v = warp_reduce16(lrow, lane, [](float a, float b) { return a + b; });
+          if ((lane & 1) == 0) red_s[quad * kG + reduce_head(lane)] = v;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty);               // once per segment, with or without tiles
+        named_bar_sync(1, 128);
+        if (tid < kG) {
+          pt[kG * kD + 2 * tid] = ti > 0 ? m_run[tid] : -INFINITY;
+          pt[kG * kD + 2 * tid + 1] =
+              ti > 0 ? red_s[tid] + red_s[kG + tid] + red_s[2 * kG + tid] + red_s[3 * kG + tid] : 0.f;
         }
         named_bar_sync(1, 128);
-        if (s_flag) {
-          // ---- merge the segment's stage-2 partials -> output row + LSE
-          if (tid == 0) trace(p.trace, 14);
-          float* wgt = sarr;                             // [t2][16]
-          float* inv_l = sarr + kMaxT2 * kG;
-          float* ml = inv_l + kG;                        // [t2][16][2]
-          for (int x = tid; x < I.t2 * 2 * kG; x += 128)
-            ml[x] = __ldcg(part_seg + (int64_t)(x / (2 * kG)) * kPartStride + kG * kD + (x % (2 * kG)));
-          named_bar_sync(1, 128);
-          if (tid < kG) {
-            float M = -INFINITY;
-            for (int x = 0; x < I.t2; ++x) M = fmaxf(M, ml[(x * kG + tid) * 2]);
-            float Lsum = 0.f;
-            for (int x = 0; x < I.t2; ++x) {
-              const float mm = ml[(x * kG + tid) * 2];
-              const float w = mm == -INFINITY ? 0.f : ex2(mm - M);
-              wgt[x * kG + tid] = w;
-              Lsum += ml[(x * kG + tid) * 2 + 1] * w;
-            }
-            inv_l[tid] = 1.f / Lsum;
-            if (p.lse) p.lse[(int64_t)I.s * p.hq + I.g * kG + tid] = (M + log2f(Lsum)) * 0.6931471805599453f;
-          }
-          named_bar_sync(1, 128);
-          if (tid == 0) trace(p.trace, 15);
-          // thread -> heads 4*hp..4*hp+3 at d in [4*c4, 4*c4+4): every partial's
-          // float4 loads are independent, so many are in flight per thread
-          const int c4 = tid & 31, hp = tid >> 5;        // hp in 0..3 -> heads 4*hp .. 4*hp+3
-          float4 acc[4];
+      }
+      if (warp == 2) arrive_all(x3, lane, P);
+      mbar_wait_cluster(x3, par);
+      if (tid == 0) trace(tr, 14);
+      CYC(15);
+      {
+        // ---- combine: piece r merges heads r, r + P, ... of the P partials (DSMEM)
+        const int hh = tid >> 6, dp = tid & 63;
+        for (int j2 = 0; (int)rank + P * 2 * j2 < kG; ++j2) {
+          const int h = (int)rank + P * (2 * j2 + hh);
+          const bool act = h < kG;
+          const int hs = act ? h : (int)rank;
+          float mq[kMaxCl], lq[kMaxCl];
+          float2 oq[kMaxCl];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 5
-          for (int x = 0; x < I.t2; ++x) {
-            float4 v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              v[k] = __ldcg(reinterpret_cast<const float4*>(part_seg + (int64_t)x * kPartStride + (4 * hp + k) * kD) + c4);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float w = wgt[x * kG + 4 * hp + k];
-              acc[k].x += v[k].x * w;
-              acc[k].y += v[k].y * w;
-              acc[k].z += v[k].z * w;
-              acc[k].w += v[k].w * w;
+          for (int q = 0; q < kMaxCl; ++q) {
+            if (q < P) {
+              mq[q] = ld_dsmem(sarr + kG * kD + 2 * hs, q);
+              lq[q] = ld_dsmem(sarr + kG * kD + 2 * hs + 1, q);
+              oq[q] = ld_dsmem2(sarr + hs * kD + 2 * dp, q);
             }
           }
+          float M = -INFINITY;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int h = 4 * hp + k;
-            const float il = inv_l[h];
-            const int64_t oi = ((int64_t)I.s * p.hq + I.g * kG + h) * kD + 4 * c4;
+          for (int q = 0; q < kMaxCl; ++q)
+            if (q < P) M = fmaxf(M, mq[q]);
+          CYC(16);
+          float Ls = 0.f, ax = 0.f, ay = 0.f;
+#pragma unroll
+          for (int q = 0; q < kMaxCl; ++q) {
+            if (q < P && mq[q] != -INFINITY) {
+              const float w = ex2(mq[q] - M);
+              Ls += lq[q] * w;
+              ax += oq[q].x * w;
+              ay += oq[q].y * w;
+            }
+          }
+          if (act) {
+            const float il = 1.f / Ls;
+            const int64_t oi = ((int64_t)I.s * p.hq + I.g * kG + h) * kD + 2 * dp;
             if (p.out_f32) {
-              *reinterpret_cast<float4*>(static_cast<float*>(p.out) + oi) =
-                  make_float4(acc[k].x * il, acc[k].y * il, acc[k].z * il, acc[k].w * il);
+              *reinterpret_cast<float2*>(static_cast<float*>(p.out) + oi) = make_float2(ax * il, ay * il);
             } else {
-              __nv_bfloat162 a = __floats2bfloat162_rn(acc[k].x * il, acc[k].y * il);
-              __nv_bfloat162 b = __floats2bfloat162_rn(acc[k].z * il, acc[k].w * il);
-              uint2 u;
-              u.x = *reinterpret_cast<uint32_t*>(&a);
-              u.y = *reinterpret_cast<uint32_t*>(&b);
-              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.out) + oi) = u;
+              *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.out) + oi) =
+                  __floats2bfloat162_rn(ax * il, ay * il);
             }
+            if (p.lse && dp == 0) p.lse[(int64_t)I.s * p.hq + I.g * kG + h] = (M + log2f(Ls)) * 0.6931471805599453f;
           }
         }
-        if (s_flag && tid == 0) trace(p.trace, 9);
-        named_bar_sync(1, 128);                          // red_m / red_s / s_flag reuse
       }
+      if (tid == 0) trace(tr, 9);
+      CYC(17);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();                     // no CTA leaves while its shared memory may still be read
   if (warp == 1) tmem_dealloc<512>(tmem);
   if (threadIdx.x == 0) {
     trace(p.trace, 10);
-    const int nseg = p.n_seq * p.hkv;
+    if (p.trace && blockIdx.x < kTraceCtas)
+      g_trace[(((p.trace - 1) % kTraceRing) * kTraceCtas + blockIdx.x) * kTracePts + 11] = clock64();
     int* done = tv.fused + 4 * nseg;
     if (publish_arrive(done) == (int)gridDim.x - 1) {
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       // every CTA has finished: the new token is part of the caches now
       for (int s = 0; s < p.n_seq; ++s) tv.len[s] += 1;
-      for (int x = 0; x < 4 * nseg; ++x) tv.fused[x] = 0;
       *done = 0;
       __threadfence();
     }
@@ -924,31 +1105,71 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
 }  // namespace
 
 size_t decode_fused_workspace_bytes(int n_seq, int hkv) {
-  const size_t nseg = (size_t)n_seq * hkv;
-  return align_up(nseg * kMaxPieces * 2 * kG * sizeof(float), 256) + align_up(nseg * kMaxPieces * 64 * sizeof(float), 256) +
-         align_up(nseg * kMaxT2 * kPartStride * sizeof(float), 256);
+  (void)n_seq;
+  (void)hkv;
+  return 0;
 }
 
-// Host-side eligibility: the partition must fit the TMEM-resident z tiles and
-// the merge list for every length up to max_len_after.
-bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int sms) {
-  if (getenv("INFLLM2_DECODE_LEGACY")) return false;
-  const int nseg = n_seq * hkv;
-  if (nseg > sms || sms > kMaxPieces) return false;
-  if (g.top_k > 32 || g.top_k < 1) return false;
-  if (infllm2_max_selected(&g) > 2 * kMaxT2) return false;
+static int max_active_clusters(int np) {
+  static int cached[kMaxCl + 1] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  if (cached[np] >= 0) return cached[np];
+  const size_t smem = Smem::total + 1024;
+  if (cudaFuncSetAttribute(decode_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return cached[np] = 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = np;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(np * 32);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel, &cfg) != cudaSuccess) n = 0;
+  return cached[np] = n;
+}
+
+// Cluster size (= pieces per segment): the largest per-round parallelism
+// np / rounds over the sizes whose pieces fit the TMEM-resident z tiles.  On a
+// B200 (1 CTA/SM) 8-CTA clusters reach 15 co-resident clusters, 6-CTA ones 22.
+static int choose_cluster(int nseg, int64_t max_len_after) {
   const int64_t nb_max = max_len_after / kM + 1;
-  const int64_t avail = sms - nseg;
-  const int cmax = kCandCap / g.top_k;
-  int64_t per_piece = avail > 0 ? (nseg * nb_max + avail - 1) / avail : nb_max;
-  const int64_t capped = (nb_max + cmax - 1) / cmax;
-  if (capped > per_piece) per_piece = capped;
-  return per_piece + 1 <= kMaxPieceBlocks;
+  int best = 0;
+  double best_score = -1.0;
+  for (int np = kMaxCl; np >= 3; --np) {
+    if ((nb_max + np - 1) / np + 1 > kMaxPieceBlocks) continue;
+    const int n = max_active_clusters(np);
+    if (n <= 0) continue;
+    const int rounds = (nseg + n - 1) / n;
+    const double score = (double)np / rounds;
+    if (score > best_score) {
+      best_score = score;
+      best = np;
+    }
+  }
+  return best;
 }
 
-int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int hq, int hkv, const void* q,
-                      const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32, float* lse,
-                      void* ws, cudaStream_t stream, int sms) {
+// Host-side eligibility: pieces must fit the TMEM-resident z tiles for every
+// length up to max_len_after and budgets must fit the warp top-k.
+bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int sms) {
+  (void)sms;
+  if (getenv("INFLLM2_DECODE_LEGACY")) return false;
+  if (n_seq > kMaxSeq || n_seq < 1) return false;
+  if (g.top_k > kMaxBudget || g.top_k < 1) return false;
+  if (infllm2_max_selected(&g) > 96) return false;
+  return choose_cluster(n_seq * hkv, max_len_after) > 0;
+}
+
+int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
+                      const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
+                      int out_f32, float* lse, void* ws, cudaStream_t stream, int sms) {
+  (void)ws;
+  (void)sms;
   Params p;
   p.table = table;
   p.n_seq = n_seq;
@@ -960,21 +1181,12 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int hq,
   p.consume = g.forced_consume_budget;
   p.max_sel = infllm2_max_selected(&g);
   p.coarse_stride = (int)g.coarse_stride;
-  p.cmax = kCandCap / g.top_k;
-  if (p.cmax > kMaxPieces) p.cmax = kMaxPieces;
   p.k_new = static_cast<const __nv_bfloat16*>(k_new);
   p.v_new = static_cast<const __nv_bfloat16*>(v_new);
   p.selection = selection;
   p.out = out;
   p.out_f32 = out_f32;
   p.lse = lse;
-  const size_t nseg = (size_t)n_seq * hkv;
-  uint8_t* b = static_cast<uint8_t*>(ws);
-  p.pstat = reinterpret_cast<float*>(b);
-  b += align_up(nseg * kMaxPieces * 2 * kG * sizeof(float), 256);
-  p.cand = reinterpret_cast<float*>(b);
-  b += align_up(nseg * kMaxPieces * 64 * sizeof(float), 256);
-  p.part = reinterpret_cast<float*>(b);
   p.zscale = 1.4426950408889634f / sqrtf((float)kD);
   static const bool tr = getenv("INFLLM2_DECODE_TRACE") != nullptr;
   static int launches = 0;
@@ -984,31 +1196,40 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int hq,
   const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
   const uint32_t box[3] = {64, (uint32_t)kG, 1};
   if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
-  const size_t smem = Smem::total + 1024;
-  if (cudaFuncSetAttribute(decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return INFLLM2_ERR_CUDA;
-  static const bool coop = getenv("INFLLM2_DECODE_NOCOOP") == nullptr;
+  const int nseg = n_seq * hkv;
+  const int np = choose_cluster(nseg, max_len_after);
+  if (np <= 0) return INFLLM2_ERR_UNSUPPORTED;
+  int ncl = max_active_clusters(np);
+  if (ncl > nseg) ncl = nseg;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = np;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)sms);
+  cfg.gridDim = dim3((unsigned)(ncl * np));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = Smem::total + 1024;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = coop ? 1 : 0;
+  cfg.numAttrs = 1;
   count_launch();
-  if (cudaLaunchKernelEx(&cfg, decode_fused_kernel, tq, p) != cudaSuccess) return INFLLM2_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, decode_cluster_kernel, tq, p) != cudaSuccess) return INFLLM2_ERR_CUDA;
   return INFLLM2_OK;
 }
 
 }  // namespace infllm2
 
 // Debug: copy the traced launches' per-CTA phase timestamps (ns,
-// [4 launches][kMaxPieces][12], ring by launch number) to host memory.
+// [4 launches][160 CTAs][16], ring by launch number) to host memory.
+extern "C" int infllm2_debug_decode_cycles(long long* host, int max_entries) {
+  const int cap = infllm2::kTraceCtas * 32;
+  const int n = max_entries < cap ? max_entries : cap;
+  return cudaMemcpyFromSymbol(host, infllm2::g_cyc, sizeof(long long) * n) == cudaSuccess ? 0 : -1;
+}
+
 extern "C" int infllm2_debug_decode_trace(unsigned long long* host, int max_entries) {
-  const int cap = infllm2::kTraceRing * infllm2::kMaxPieces * infllm2::kTracePts;
+  const int cap = infllm2::kTraceRing * infllm2::kTraceCtas * infllm2::kTracePts;
   const int n = max_entries < cap ? max_entries : cap;
   return cudaMemcpyFromSymbol(host, infllm2::g_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
 }

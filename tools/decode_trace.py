@@ -65,12 +65,15 @@ for i in range(3):
     print(f"launch {i}: duration {dur / 1e3:.2f} us, gap to next launch {gap / 1e3:.2f} us")
 t = ring[3]
 t0 = np.nanmin(t[:, 0])
+ok = ~np.isnan(t[:, 15]) & ~np.isnan(t[:, 11])
+mhz = (t[ok, 11] - t[ok, 15]) / (t[ok, 10] - t[ok, 0]) * 1e3
+print(f"SM clock inside the kernel: median {np.median(mhz):.0f} MHz (min {mhz.min():.0f}, max {mhz.max():.0f})")
 names = ["start", "prod: stage-1 TMA issued", "epi: stage-1 partial", "epi: segment stage-1 complete",
          "epi: block scores", "epi: local top-k", "merge published", "prod: selection seen",
-         "epi: first stage-2 partial", "combine done", "CTA end", "(smid)", "epi: first z tile", "epi: append done",
-         "combine start", "combine weights"]
+         "epi: first stage-2 partial", "epi: segment done", "CTA end", "(smid)", "epi: first z tile", "epi: append done",
+         "combine start (after x3)", "-"]
 for i, n in enumerate(names):
-    if i == 11:
+    if i in (11, 15):
         continue
     col = (t[:, i] - t0) / 1e3
     col = col[~np.isnan(col)]
@@ -85,5 +88,13 @@ print("fastest:")
 for c in order[-150:][::-1][:0]:
     pass
 fin = np.nan_to_num(t[:144, 2] - t0, nan=0) / 1e3
-print("stage-1 partial by piece index (mean over segments):", np.round(fin.reshape(16, 9).mean(0), 2))
-print("stage-1 partial by segment (mean over pieces):", np.round(fin.reshape(16, 9).mean(1), 2))
+cb = (ctypes.c_longlong * (160 * 32))()
+lib.infllm2_debug_decode_cycles(cb, 160 * 32)
+cy = np.array(cb, dtype=np.float64).reshape(160, 32)[:8, :18]
+steps = ["x1->LSE", "LSE->S_j", "S_j->R_b", "R_b->localtopk", "topk->x2", "x2->merge loads", "loads->tau",
+         "tau->filter", "filter->rank", "rank->sel_s", "sel_s->s2_full", "s2_full->tilemax", "tilemax->o_full",
+         "o_full->partial(unused)", "tiles->x3", "x3->combine loads", "loads->end"]
+d = np.diff(cy, axis=1)
+print("cycles per phase (cluster 0, pieces 0..7):")
+for i, n in enumerate(steps):
+    print(f"  {n:22s} " + " ".join(f"{v:7.0f}" for v in d[:, i]))
