@@ -410,7 +410,7 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
     """configs[3]: sequences partitioned over ranks (decode_seqs per GPU), each
     with a seq_len-token cache in all `layers` layers; one step = every sequence
     appends one token and attends one query row in every layer.  The 32-layer
-    step is captured once in a CUDA graph (fixed split-K bound) and replayed."""
+    step is captured once in a CUDA graph (fixed length bound) and replayed."""
     import torch
 
     S, L, layers = args.decode_seqs, args.seq, args.layers
@@ -442,11 +442,14 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
     graph = torch.cuda.CUDAGraph()
+    lib = P._lib.load()
     with torch.cuda.stream(side):
         step()
         torch.cuda.synchronize(dev)
+        n0 = lib.infllm2_launch_count()
         with torch.cuda.graph(graph, stream=side):
             step(bookkeep=False)
+        launches_per_step = lib.infllm2_launch_count() - n0
     for b in batches:
         b.advance(1)
     for _ in range(args.warmup):
@@ -507,7 +510,9 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
                     "us_per_token": round(ms_e2e / args.steps * 1e3 / (S * world), 2),
                     "h2d_bytes_per_step": int((q.numel() + kn.numel() + vn.numel()) * 2),
                     "d2h_bytes_per_step": int(out_host.numel() * 2)},
-            "graph": "32-layer step captured once (5-6 launches per layer), replayed per step"}
+            "gpu_launches_per_step": int(launches_per_step),
+            "graph": f"{layers}-layer step captured once ({launches_per_step // max(1, layers)} launch(es) per layer: "
+                     "fused cluster kernel), replayed per step"}
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle)

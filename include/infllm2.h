@@ -75,7 +75,9 @@ typedef struct infllm2_geometry {
 enum {
   INFLLM2_FLAG_EXACT_SIMT = 1 << 0,  /* force the CUDA-core float64 scorer (verifier) */
   INFLLM2_FLAG_CHECK_FINITE = 1 << 1,/* report non-finite q / means (costs a sync)    */
-  INFLLM2_FLAG_OUT_F32 = 1 << 2      /* `out` is float32 instead of bf16              */
+  INFLLM2_FLAG_OUT_F32 = 1 << 2,     /* `out` is float32 instead of bf16              */
+  INFLLM2_FLAG_P_SPLIT = 1 << 3      /* stage 2: softmax weights as bf16 hi + lo (two PV
+                                        MMAs, ~1e-5 outputs) instead of bf16 P          */
 };
 
 const char* infllm2_strerror(int code);

@@ -161,7 +161,7 @@ int infllm2_attend(const infllm2_geometry* g, const void* q, int64_t q_row_strid
   const int out_f32 = (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0;
   if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_attend_supported(*g, cs)) {
     return cuda_status(launch_attend_tc(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32,
-                                        lse, st));
+                                        lse, (flags & INFLLM2_FLAG_P_SPLIT) ? 1 : 0, st));
   }
   return cuda_status(launch_attend_simt(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out,
                                         out_f32, lse, st));

@@ -22,6 +22,7 @@
 // 2..5 = softmax (128 threads = tile rows), 6..9 = epilogue (thread = d lane
 // of O^T: normalise, store bf16/f32 output and the natural-log LSE).
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -40,7 +41,9 @@ constexpr int kD = 128;
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
 constexpr int kStages = 3;
-constexpr int kThreads = 320;
+constexpr int kThreads = 352;
+constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to 4 tiles ahead of softmax)
+constexpr uint32_t kColO = kSlots * 16;  // O^T columns [kColO, kColO + 32)
 constexpr int kMaxSel = 80;
 
 constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
@@ -54,10 +57,10 @@ struct Smem {
   static constexpr uint32_t kv = 0;
   static constexpr uint32_t q = kv + kStages * kStageBytes;     // 2 buffers
   static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
-  static constexpr uint32_t stats = p + 2 * kPBytes;            // [2][4 warps][16] l + [2][16] M
-  static constexpr uint32_t red = stats + 2 * 5 * 16 * 4;       // [4 warps][16] reduction scratch
+  static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
+  static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [4 warps][16] reduction scratch
   static constexpr uint32_t bars = red + 4 * 16 * 4;
-  static constexpr uint32_t total = bars + 32 * 8;
+  static constexpr uint32_t total = bars + 40 * 8;
 };
 
 struct Params {
@@ -76,6 +79,8 @@ struct Params {
   // [part*split, (part+1)*split); partial O^T (unnormalised), max and row sum go
   // to part_o / part_ml and attend_combine_kernel merges them.  split == 0: off.
   int split;
+  int p_split;        // 1: P as bf16 hi + lo (two PV MMAs per k-step), 0: P in bf16
+  int group_major;    // prefill: items ordered (group, row) so one group's K/V is the L2 working set
   int64_t parts;
   float* part_o;      // [item][part][16][128]
   float* part_ml;     // [item][part][16][2]
@@ -86,6 +91,21 @@ __device__ __forceinline__ void tile_range(const Params& p, int64_t part, int ti
   const int64_t a = part * p.split, b = a + p.split;
   *c0 = (int)(a < tiles ? a : tiles);
   *c1 = (int)(b < tiles ? b : tiles);
+}
+
+// Work unit w -> (selection/output item = i*hkv + grp, split part, row i, group).
+__device__ __forceinline__ void unit_of(const Params& p, int64_t w, int64_t* item, int64_t* part, int64_t* i,
+                                        int* grp) {
+  const int64_t u = w / p.parts;
+  *part = w - u * p.parts;
+  if (p.group_major) {
+    *grp = (int)(u / p.n);
+    *i = u - (int64_t)(*grp) * p.n;
+  } else {
+    *i = u / p.hkv;
+    *grp = (int)(u - *i * p.hkv);
+  }
+  *item = *i * p.hkv + *grp;
 }
 
 __device__ __forceinline__ int64_t item_pos(const Params& p, int64_t i) {
@@ -105,17 +125,50 @@ struct SelRow {
   }
 };
 
-__device__ __forceinline__ SelRow load_sel(const Params& p, int64_t item, int64_t pos, int lane) {
+__device__ __forceinline__ SelRow sel_raw(const Params& p, int64_t item, int lane) {
   const int32_t* s = p.sel + item * p.max_sel;
   SelRow r;
   r.r0 = lane < p.max_sel ? s[lane] : -1;
   r.r1 = lane + 32 < p.max_sel ? s[lane + 32] : -1;
   r.r2 = lane + 64 < p.max_sel ? s[lane + 64] : -1;
+  r.nb = 0;
+  return r;
+}
+__device__ __forceinline__ SelRow sel_finish(SelRow r, int64_t pos) {
   auto ok = [&](int b) { return b >= 0 && (int64_t)b * kM <= pos; };
   r.nb = __popc(__ballot_sync(0xffffffffu, ok(r.r0))) + __popc(__ballot_sync(0xffffffffu, ok(r.r1))) +
          __popc(__ballot_sync(0xffffffffu, ok(r.r2)));
   return r;
 }
+__device__ __forceinline__ SelRow load_sel(const Params& p, int64_t item, int64_t pos, int lane) {
+  return sel_finish(sel_raw(p, item, lane), pos);
+}
+// Selection rows of a warp's item stream, fetched one item ahead so the
+// global-memory latency hides behind the current item.
+struct SelPrefetch {
+  SelRow nxt;
+  __device__ __forceinline__ void init(const Params& p, int64_t w, int64_t items, int lane) {
+    if (w < items) {
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w, &item, &part, &i, &grp);
+      nxt = sel_raw(p, item, lane);
+    }
+  }
+  // row of unit w (which must be the prefetched one); prefetches w + stride
+  __device__ __forceinline__ SelRow take(const Params& p, int64_t w, int64_t items, int64_t pos, int lane) {
+    const SelRow cur = nxt;
+    const int64_t w2 = w + gridDim.x;
+    if (w2 < items) {
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w2, &item, &part, &i, &grp);
+      nxt = sel_raw(p, item, lane);
+    }
+    return sel_finish(cur, pos);
+  }
+};
+
 
 __global__ void __launch_bounds__(kThreads, 1)
 attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -127,15 +180,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   uint64_t* kv_empty = bars + 3;          // [3]
   uint64_t* q_full = bars + 6;            // [2]
   uint64_t* q_empty = bars + 8;           // [2]
-  uint64_t* s_full = bars + 10;           // [2]
-  uint64_t* s_empty = bars + 12;          // [2]
+  uint64_t* s_full = bars + 28;           // [kSlots]
+  uint64_t* s_empty = bars + 32;          // [kSlots]
   uint64_t* p_full = bars + 14;           // [2]
   uint64_t* p_empty = bars + 16;          // [2]
   uint64_t* o_full = bars + 18;           // [2]
   uint64_t* o_empty = bars + 20;          // [2]
   uint64_t* st_full = bars + 22;          // [2]
   uint64_t* st_empty = bars + 24;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
   float* stats = reinterpret_cast<float*>(smem + Smem::stats);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
 
@@ -145,8 +198,6 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
-      mbar_init(s_full + i, 1);
-      mbar_init(s_empty + i, 4);
       mbar_init(p_full + i, 4);
       mbar_init(p_empty + i, 1);
       mbar_init(o_full + i, 1);
@@ -154,17 +205,18 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_init(st_full + i, 4);
       mbar_init(st_empty + i, 4);
     }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, 4); }
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
   }
-  if (warp == 1) tmem_alloc<64>(tmem_slot);
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
   pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;       // cols [0,32): S slots, [32,64): O slots
+  const uint32_t tmem = *tmem_slot;       // cols [0,64): S slots, [64,96): O buffers
   pdl_wait();                             // no-op unless launched as a dependent
   const int64_t items = p.n * p.hkv * p.parts;   // work units (item, part)
 
@@ -173,14 +225,16 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
+    SelPrefetch pf;
+    pf.init(p, blockIdx.x, items, lane);
     for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-      const int64_t item = w / p.parts, part = w - item * p.parts;
-      const int64_t i = item / p.hkv;
-      const int grp = (int)(item - i * p.hkv);
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w, &item, &part, &i, &grp);
       const int64_t pos = item_pos(p, i);
       const CUtensorMap* mk = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i : &tm_k;
       const CUtensorMap* mv = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i + 1 : &tm_v;
-      const SelRow sr = load_sel(p, item, pos, lane);
+      const SelRow sr = pf.take(p, w, items, pos, lane);
       const int nb = sr.nb;
       int c0, c1;
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
@@ -218,87 +272,97 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    // -------------------------------------------------------------- MMA issuer
+    // -------------------------------------------------------------- QK issuer
+    // S^T[slot] = K_tile . Q^T for every tile of the CTA's item stream, up to
+    // kSlots tiles ahead of the softmax warps.  QK and PV are issued from two
+    // warps: each tcgen05.mma costs ~50 cycles of A-operand fetch whatever N
+    // (N = 16 here), so one issuer stalled on a barrier leaves the tensor
+    // pipe idle.
     const uint32_t idesc_qk = idesc_bf16_f32(128, kG);
-    const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
     int stage = 0;
     uint32_t phase = 0;
-    int sslot = 0, pbuf = 0;
-    uint32_t s_ph[2] = {0, 0}, p_ph[2] = {0, 0};
+    uint32_t tcount = 0;
     int it = 0;
+    SelPrefetch pf;
+    pf.init(p, blockIdx.x, items, lane);
     for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-      const int64_t item = w / p.parts, part = w - item * p.parts;
-      const int64_t i = item / p.hkv;
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w, &item, &part, &i, &grp);
       const int64_t pos = item_pos(p, i);
-      const SelRow sr = load_sel(p, item, pos, lane);
+      const SelRow sr = pf.take(p, w, items, pos, lane);
+      int c0, c1;
+      tile_range(p, part, (sr.nb + 1) / 2, &c0, &c1);
+      if (c0 >= c1) continue;
+      const int qb = it & 1;
+      mbar_wait(q_full + qb, (it >> 1) & 1);
+      const uint64_t dq = sdesc_k_sw128(smem_u32(smem + Smem::q + qb * kQBytes));
+      for (int c = c0; c < c1; ++c, ++tcount) {
+        const int slot = tcount % kSlots;
+        mbar_wait(kv_full + stage, phase);
+        mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dk = sdesc_k_sw128(smem_u32(smem + Smem::kv + stage * kStageBytes));
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
+            const uint32_t qoff = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+            umma_f16_ss(tmem + slot * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk, k > 0 ? 1u : 0u);
+          }
+          umma_commit(s_full + slot);
+          if (c == c1 - 1) umma_commit(q_empty + qb);
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      ++it;
+    }
+  } else if (warp == 10) {
+    // -------------------------------------------------------------- PV issuer
+    const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
+    int stage = 0;
+    uint32_t pcount = 0;
+    int it = 0;
+    SelPrefetch pf;
+    pf.init(p, blockIdx.x, items, lane);
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w, &item, &part, &i, &grp);
+      const int64_t pos = item_pos(p, i);
+      const SelRow sr = pf.take(p, w, items, pos, lane);
       const int nb = sr.nb;
       int c0, c1;
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
       if (c0 >= c1) continue;
-      const int qb = it & 1, ob = it & 1;
-      mbar_wait(q_full + qb, (it >> 1) & 1);
-      const uint32_t q_addr = smem_u32(smem + Smem::q + qb * kQBytes);
-      int stage_c = stage;
-      uint32_t phase_c = phase;
-      auto issue_qk = [&](int st, int slot) {
-        const uint32_t k_addr = smem_u32(smem + Smem::kv + st * kStageBytes);
-        tc_fence_after();
-        if (elect_one()) {
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
-            const uint32_t qoff = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-            umma_f16_ss(tmem + slot * kG, sdesc_k_sw128(k_addr + off), sdesc_k_sw128(q_addr + qoff), idesc_qk,
-                        k > 0 ? 1u : 0u);
-          }
-          umma_commit(s_full + slot);
-        }
-        __syncwarp();
-      };
-      // prologue: QK of tile 0
-      mbar_wait(kv_full + stage_c, phase_c);
-      mbar_wait(s_empty + sslot, s_ph[sslot] ^ 1);
-      s_ph[sslot] ^= 1;
-      issue_qk(stage_c, sslot);
-      for (int c = c0; c < c1; ++c) {
-        const int cur_stage = stage_c, cur_slot = sslot;
-        if (++stage_c == kStages) { stage_c = 0; phase_c ^= 1; }
-        sslot ^= 1;
-        if (c + 1 < c1) {
-          mbar_wait(kv_full + stage_c, phase_c);
-          mbar_wait(s_empty + sslot, s_ph[sslot] ^ 1);
-          s_ph[sslot] ^= 1;
-          issue_qk(stage_c, sslot);
-        }
-        if (c == c1 - 1) {
-          if (elect_one()) umma_commit(q_empty + qb);
-          __syncwarp();
-        }
-        // PV of tile c once its P is in shared memory
-        mbar_wait(p_full + pbuf, p_ph[pbuf]);
-        p_ph[pbuf] ^= 1;
+      const int ob = it & 1;
+      for (int c = c0; c < c1; ++c, ++pcount) {
+        const int pbuf = pcount & 1;
+        mbar_wait(p_full + pbuf, (pcount >> 1) & 1);
         if (c == c0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
         if (elect_one()) {
-          const uint32_t v_addr = smem_u32(smem + Smem::kv + cur_stage * kStageBytes + kTileBytes);
-          const uint32_t p_addr = smem_u32(smem + Smem::p + pbuf * kPBytes);
-          for (int k = 0; k < ksteps; ++k) {
-            const uint64_t vdesc = sdesc_mn_sw128(v_addr + k * 2048, kHalfBytes, 1024);
-            umma_f16_ss(tmem + 32 + ob * kG, vdesc, sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv,
-                        (c > c0 || k > 0) ? 1u : 0u);
-            umma_f16_ss(tmem + 32 + ob * kG, vdesc, sdesc_interleave(p_addr + kPHalf + k * 512, 256, 128),
-                        idesc_pv, 1u);
+          const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + stage * kStageBytes + kTileBytes),
+                                             kHalfBytes, 1024);
+          const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 256, 128);
+          const uint32_t ocol = tmem + kColO + ob * kG;
+          const uint32_t acc0 = c > c0 ? 1u : 0u;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (k < ksteps) {
+              umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + (k * 512 >> 4), idesc_pv, (acc0 | k) ? 1u : 0u);
+              if (p.p_split) umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + ((kPHalf + k * 512) >> 4), idesc_pv, 1u);
+            }
           }
-          umma_commit(kv_empty + cur_stage);
+          umma_commit(kv_empty + stage);
           umma_commit(p_empty + pbuf);
           if (c == c1 - 1) umma_commit(o_full + ob);
         }
         __syncwarp();
-        pbuf ^= 1;
-        (void)cur_slot;
+        if (++stage == kStages) stage = 0;
       }
-      stage = stage_c;
-      phase = phase_c;
       ++it;
     }
   } else if (warp < 6) {
@@ -307,25 +371,30 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     const int row = quad * 32 + lane;                  // tile row == TMEM lane
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const float c2 = 1.4426950408889634f / sqrtf((float)kD);
-    int sslot = 0, pbuf = 0;
-    uint32_t s_ph[2] = {0, 0}, p_ph[2] = {0, 0};
+    int pbuf = 0;
+    uint32_t p_ph[2] = {0, 0};
+    uint32_t tcount = 0;
     int it = 0;
+    SelPrefetch pf;
+    pf.init(p, blockIdx.x, items, lane);
     for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-      const int64_t item = w / p.parts, part = w - item * p.parts;
-      const int64_t i = item / p.hkv;
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w, &item, &part, &i, &grp);
       const int64_t pos = item_pos(p, i);
-      const SelRow sr = load_sel(p, item, pos, lane);
+      const SelRow sr = pf.take(p, w, items, pos, lane);
       const int nb = sr.nb;
       int c0, c1;
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
-      float mrun[kG], lsum[kG];
+      float mrun[kG], lsum[kG], lsx[kG];     // lsum: weights as used by PV; lsx: unrounded (LSE)
 #pragma unroll
-      for (int h = 0; h < kG; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; }
+      for (int h = 0; h < kG; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
       for (int c = c0; c < c1; ++c) {
-        mbar_wait(s_full + sslot, s_ph[sslot]);
-        s_ph[sslot] ^= 1;
+        const int sslot = tcount % kSlots;
+        mbar_wait(s_full + sslot, (tcount / kSlots) & 1);
+        ++tcount;
         tc_fence_after();
         float z[kG];
         tmem_ld16(tmem + lane_base + sslot * kG, z);
@@ -333,7 +402,6 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + sslot);
-        sslot ^= 1;
         const int x = row >> 6;
         const int b0 = sr.get(2 * c), b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         bool valid = (2 * c + x) < nb;
@@ -376,6 +444,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             corr[h] = (mrun[h] == -INFINITY) ? 1.f : ex2(mrun[h] - mnew);
             any_corr |= (c > c0) && (corr[h] != 1.f);
             lsum[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
+            lsx[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
             mrun[h] = mnew;
           }
           named_bar_sync(2, 128);
@@ -385,11 +454,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
             tc_fence_after();
             float o[kG];
-            tmem_ld16(tmem + lane_base + 32 + ob * kG, o);
+            tmem_ld16(tmem + lane_base + kColO + ob * kG, o);
             tmem_wait_ld();
 #pragma unroll
             for (int h = 0; h < kG; ++h) o[h] *= corr[h];
-            tmem_st16(tmem + lane_base + 32 + ob * kG, o);
+            tmem_st16(tmem + lane_base + kColO + ob * kG, o);
             tmem_wait_st();
             tc_fence_before();
           }
@@ -397,17 +466,21 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         // P = 2^(z - M) as bf16 into the MN-major interleaved buffer
         mbar_wait(p_empty + pbuf, p_ph[pbuf] ^ 1);
         p_ph[pbuf] ^= 1;
-        // P split into bf16 hi + lo (two PV MMAs): ~16-bit P, so the output
-        // is not limited by bf16 rounding of the softmax weights.
+        // P in bf16 for one PV MMA per k-step; the row sums use the ROUNDED
+        // weights, so O = sum P~ V / sum P~ stays a convex combination (error
+        // ~2^-9 |V| / sqrt(rows)).  p_split: P also as a bf16 lo part (second
+        // PV MMA), ~16-bit weights, for callers that want 1e-5 outputs.
         uint32_t phi[kG / 2], plo[kG / 2];
 #pragma unroll
         for (int h = 0; h < kG; h += 2) {
           const float a = ex2(z[h] - mrun[h]);
           const float b = ex2(z[h + 1] - mrun[h + 1]);
-          lsum[h] += a;
-          lsum[h + 1] += b;
           const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
           const __nv_bfloat162 lo2 = __floats2bfloat162_rn(a - __low2float(hi2), b - __high2float(hi2));
+          lsum[h] += p.p_split ? a : __low2float(hi2);
+          lsum[h + 1] += p.p_split ? b : __high2float(hi2);
+          lsx[h] += a;
+          lsx[h + 1] += b;
           phi[h / 2] = *reinterpret_cast<const uint32_t*>(&hi2);
           plo[h / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
         }
@@ -415,8 +488,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const uint32_t base = (row >> 3) * 256 + (row & 7) * 16;
         *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
         *reinterpret_cast<uint4*>(pb + base + 128) = make_uint4(phi[4], phi[5], phi[6], phi[7]);
-        *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
-        *reinterpret_cast<uint4*>(pb + kPHalf + base + 128) = make_uint4(plo[4], plo[5], plo[6], plo[7]);
+        if (p.p_split) {
+          *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
+          *reinterpret_cast<uint4*>(pb + kPHalf + base + 128) = make_uint4(plo[4], plo[5], plo[6], plo[7]);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + pbuf);
@@ -424,12 +499,14 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       // per-head row sums -> stats for the epilogue
       mbar_wait(st_empty + ob, ((it >> 1) & 1) ^ 1);
-      float* st = stats + ob * 5 * 16;
-#pragma unroll
-      for (int h = 0; h < kG; ++h) {
-        float v = lsum[h];
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) st[quad * 16 + h] = v;
+      float* st = stats + ob * 9 * 16;
+      {
+        const float v = warp_reduce16(lsum, lane, [](float a, float b) { return a + b; });
+        const float vx = warp_reduce16(lsx, lane, [](float a, float b) { return a + b; });
+        if ((lane & 1) == 0) {
+          st[quad * 16 + reduce_head(lane)] = v;
+          st[80 + quad * 16 + reduce_head(lane)] = vx;
+        }
       }
       if (quad == 0 && lane < kG) {
         float mine = mrun[0];
@@ -448,9 +525,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     int it = 0;
     for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-      const int64_t item = w / p.parts, part = w - item * p.parts;
-      const int64_t i = item / p.hkv;
-      const int grp = (int)(item - i * p.hkv);
+      int64_t item, part, i;
+      int grp;
+      unit_of(p, w, &item, &part, &i, &grp);
       if (p.split) {
         const SelRow sr = load_sel(p, item, item_pos(p, i), lane);
         int c0, c1;
@@ -470,15 +547,16 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(st_full + ob, par);
       tc_fence_after();
       float o[kG];
-      tmem_ld16(tmem + lane_base + 32 + ob * kG, o);
+      tmem_ld16(tmem + lane_base + kColO + ob * kG, o);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty + ob);
-      const float* st = stats + ob * 5 * 16;
+      const float* st = stats + ob * 9 * 16;
       float l[kG];
 #pragma unroll
       for (int h = 0; h < kG; ++h) l[h] = st[h] + st[16 + h] + st[32 + h] + st[48 + h];
+      auto lsum_exact = [&](int h) { return st[80 + h] + st[96 + h] + st[112 + h] + st[128 + h]; };
       if (p.split) {
         float* po = p.part_o + w * (kG * kD) + d;
 #pragma unroll
@@ -504,12 +582,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 #pragma unroll
         for (int h = 0; h < kG; ++h) out[obase + h * kD] = __float2bfloat16_rn(o[h] / l[h]);
       }
-      if (p.lse && quad == 0 && lane < kG) {
-        float lh = l[0];
-#pragma unroll
-        for (int h = 1; h < kG; ++h) lh = (lane == h) ? l[h] : lh;
-        p.lse[i * p.hq + grp * kG + lane] = (st[64 + lane] + log2f(lh)) * 0.6931471805599453f;
-      }
+      if (p.lse && quad == 0 && lane < kG)
+        p.lse[i * p.hq + grp * kG + lane] = (st[64 + lane] + log2f(lsum_exact(lane))) * 0.6931471805599453f;
       __syncwarp();
       if (lane == 0) mbar_arrive(st_empty + ob);
     }
@@ -517,7 +591,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<64>(tmem);
+  if (warp == 1) tmem_dealloc<128>(tmem);
 }
 
 // Merge split-K partials of each (row, group) item: O = sum_p O_p 2^(m_p - M) /
@@ -595,6 +669,8 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   p.seq_len = seq_len;
   // split-K: one 2-block tile per CTA so n_seq*hkv*10 CTAs share the gather
   p.split = split_ws ? 1 : 0;
+  p.p_split = 1;
+  p.group_major = 0;
   p.parts = split_ws ? (max_sel + 1) / 2 : 1;
   p.part_o = split_ws;
   p.part_ml = split_ws ? split_ws + n_seq * hkv * p.parts * (kG * kD) : nullptr;
@@ -635,6 +711,14 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   return cudaGetLastError();
 }
 
+static int group_major_enabled() {
+  static const int v = [] {
+    const char* e = getenv("INFLLM2_ATTEND_ORDER");
+    return (e && e[0] == 'r') ? 0 : 1;     // default: group-major
+  }();
+  return v;
+}
+
 bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
   if (!tc_kernels_enabled()) return false;
   if (cs.group != kG || cs.d != kD || g.block_size != kM) return false;
@@ -644,7 +728,7 @@ bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
 
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q, int64_t q_row_stride,
                              const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
-                             void* out, int out_f32, float* lse, cudaStream_t stream) {
+                             void* out, int out_f32, float* lse, int p_split, cudaStream_t stream) {
   Params p;
   p.n = cs.n;
   p.start = cs.start;
@@ -659,6 +743,8 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.map_stride = 0;
   p.seq_len = nullptr;
   p.split = 0;
+  p.p_split = p_split;
+  p.group_major = group_major_enabled();
   p.parts = 1;
   p.part_o = nullptr;
   p.part_ml = nullptr;
@@ -686,6 +772,11 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = cs.n * cs.hkv;
+  static const int ctas_cap = [] {
+    const char* e = getenv("INFLLM2_ATTEND_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (ctas_cap > 0 && ctas_cap < sms) sms = ctas_cap;
   const int grid = (int)(items < sms ? items : sms);
   count_launch();
   attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
@@ -693,3 +784,4 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
 }
 
 }  // namespace infllm2
+

@@ -238,26 +238,6 @@ __device__ __forceinline__ float2 ld_dsmem2(const float* local, uint32_t rank) {
                : "r"(map_rank(smem_u32(local), rank)));
   return v;
 }
-// Reduce-scatter of 16 per-lane values across a warp in 16 shuffles (instead of
-// 16 x 5 butterflies): returns the warp-wide reduction of head
-// reduce_head(lane); lanes l and l^1 hold the same head.
-__device__ __forceinline__ int reduce_head(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
-template <typename Op>
-__device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane, Op op) {
-#pragma unroll
-  for (int w = 8, off = 16; w >= 1; w >>= 1, off >>= 1) {
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = up ? v[i] : v[i + w];
-      const float keep = up ? v[i + w] : v[i];
-      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
-    }
-  }
-  return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
-}
 // Same for (max, sum 2^(x - max)) pairs.
 __device__ __forceinline__ void lse_merge(float& m, float& s, float om, float os) {
   const float nm = fmaxf(m, om);

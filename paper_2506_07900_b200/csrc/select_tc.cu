@@ -421,6 +421,11 @@ bool encode_tmap_3d_bf16(CUtensorMap* map, const void* base, const uint64_t dims
 static int tc_grid(int64_t n_units) {
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const int cap = [] {
+    const char* e = getenv("INFLLM2_SELECT_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (cap > 0 && cap < sms) sms = cap;
   return (int)(n_units < sms ? n_units : sms);
 }
 

@@ -77,6 +77,26 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Reduce-scatter of 16 per-lane values across a warp in 16 shuffles (instead of
+// 16 x 5 butterflies): returns the warp-wide reduction of head
+// reduce_head(lane); lanes l and l^1 hold the same head.
+__device__ __forceinline__ int reduce_head(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+template <typename Op>
+__device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane, Op op) {
+#pragma unroll
+  for (int w = 8, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
+    }
+  }
+  return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+}
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

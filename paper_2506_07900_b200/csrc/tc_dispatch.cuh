@@ -15,7 +15,7 @@ bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs);
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
                              int64_t q_row_stride, const void* k_cache, const void* v_cache,
                              int64_t cap, const int32_t* selection, void* out, int out_f32,
-                             float* lse, cudaStream_t stream);
+                             float* lse, int p_split, cudaStream_t stream);
 size_t decode_table_bytes(int n_seq);
 int decode_table_build(const infllm2_seq_desc* host, const int64_t* lens, int n_seq, int hkv, int d,
                        void* table_dev, cudaStream_t stream);

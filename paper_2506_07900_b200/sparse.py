@@ -358,7 +358,7 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
                         start_position: int, *, stats: Optional[TouchStats] = None,
                         traces: Optional[list] = None, return_selection: bool = False,
                         return_lse: bool = False, out_dtype: Optional[torch.dtype] = None,
-                        exact: bool = False):
+                        exact: bool = False, split_p: bool = False):
     """Block-sparse attention for ``q`` of shape (n, n_q_heads, head_dim).
 
     Same semantics as the reference (sparse.py:387-468): row i sits at
@@ -368,6 +368,9 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     int32 selection (n, HKV, max_selected; ascending, -1 padded) and/or the
     float32 LSE (n, HQ) when requested.  ``exact=True`` forces the float64
     CUDA-core scorer (the verifier) instead of the tensor-core one.
+    ``split_p=True`` makes the tensor-core stage 2 carry the softmax weights as
+    bf16 hi + lo (outputs ~1e-5 of the float64 reference instead of ~1e-4, at
+    ~1.3x the stage-2 cost); the default uses bf16 weights.
     """
     if not isinstance(q, torch.Tensor) or q.dim() != 3:
         raise ValidationError("q must be a (n, n_q_heads, head_dim) tensor")
@@ -391,7 +394,8 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     out = torch.empty((n, hq, d), dtype=out_dtype, device=dev)
     lse = torch.empty((n, hq), dtype=torch.float32, device=dev) if return_lse else None
     sel_scores = torch.empty((n, hkv, smax), dtype=torch.float64, device=dev) if traces is not None else None
-    flags = (_lib.FLAG_EXACT_SIMT if exact else 0) | (_lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0)
+    flags = ((_lib.FLAG_EXACT_SIMT if exact else 0) | (_lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0)
+             | (_lib.FLAG_P_SPLIT if split_p else 0))
     lib = _lib.load()
     kc, vc, cap, fine, hi, lo, mcap = layer._device_args()
     ws_bytes = lib.infllm2_select_workspace_bytes(ctypes.byref(geom), n, hq, hkv, d, layer.length, flags)

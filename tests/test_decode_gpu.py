@@ -51,7 +51,7 @@ def test_decode_batch_matches_single_sequence_path(lengths, topk):
             assert digest(_means(layers[i].fine_means)) == digest(_means(ref.fine_means))
             assert digest(_means(layers[i].coarse_means)) == digest(_means(ref.coarse_means))
             o2, s2, l2 = P.two_stage_attention(qs[i:i + 1], ref, cfg, n_now - 1, return_selection=True,
-                                               return_lse=True, out_dtype=torch.float32)
+                                               return_lse=True, out_dtype=torch.float32, split_p=True)
             assert torch.equal(sel[i], s2[0]), (i, st, sel[i].tolist(), s2[0].tolist())
             assert (out[i] - o2[0]).abs().max().item() < 1e-4
             assert (lse[i] - l2[0]).abs().max().item() < 1e-4

@@ -64,7 +64,7 @@ def test_incremental_append_truncate_bitwise(name):
         assert digest(_means_np(layer.coarse_means)) == meta["coarse_sha"][step], step
 
 
-def _run_case(name, exact):
+def _run_case(name, exact, split_p=False):
     meta, z = load(name)
     q, k, v = case_inputs(meta)
     cfg = _cfg(meta)
@@ -77,7 +77,7 @@ def _run_case(name, exact):
     for run in runs:
         o, s, l = P.two_stage_attention(qd[run[0]:run[-1] + 1], layer, cfg, meta["start"] + int(rows[run[0]]),
                                         return_selection=True, return_lse=True,
-                                        out_dtype=torch.float32, exact=exact)
+                                        out_dtype=torch.float32, exact=exact, split_p=split_p)
         sels.append(s)
         outs.append(o)
         lses.append(l)
@@ -108,6 +108,18 @@ def test_selection_and_outputs_vs_reference(name, exact):
     ref = O.two_stage_attention(q, k, v, fine, geom, meta["start"], rows=sub)
     tol = 1e-5 if exact else 1e-4
     assert np.max(np.abs(lse[[pos_of[int(r)] for r in sub]] - ref.lse[sub])) <= tol
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_split_p_outputs_tight(name):
+    """Tensor-core stage 2 with the softmax weights as bf16 hi + lo
+    (split_p=True): outputs within 2e-5 + 1e-4|ref| of the reference."""
+    meta, z, q, k, v, cfg, sel, out, lse = _run_case(name, False, split_p=True)
+    assert np.array_equal(sel, z["selection"])
+    pos_of = {int(r): j for j, r in enumerate(z["rows"])}
+    got = out[[pos_of[int(r)] for r in z["out_rows"]]]
+    want = z["out"]
+    assert np.all(np.abs(got - want) <= 2e-5 + 1e-4 * np.abs(want))
 
 
 def test_touch_stats_and_traces_match_reference_counts():

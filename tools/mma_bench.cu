@@ -1,0 +1,64 @@
+// tcgen05.mma issue-rate micro-benchmark: cycles per kind::f16 M=128 x N x K=16
+// MMA (both operands in shared memory, K-major 128-B swizzle), one CTA per SM,
+// one issuing thread, commits every `group` MMAs (like stage 2's QK / PV).
+// Usage: mma_bench <N> <group> [iters]
+#include <cstdio>
+#include <cstdlib>
+#include "../paper_2506_07900_b200/csrc/sm100.cuh"
+
+using namespace infllm2::sm100;
+
+__global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (threadIdx.x < 32) tmem_alloc<256>(&slot);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16_f32(128, n);
+    const uint64_t da = sdesc_k_sw128(smem_u32(sm));
+    const uint64_t db = sdesc_k_sw128(smem_u32(sm + 32768));
+    uint32_t ph = 0;
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int k = 0; k < group; ++k)
+        umma_f16_ss(tmem, da + ((k & 3) * 32 >> 4), db + ((k & 3) * 32 >> 4), idesc, k > 0 ? 1u : 0u);
+      umma_commit(&bar);
+      mbar_wait(&bar, ph);
+      ph ^= 1;
+    }
+    t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
+}
+
+int main(int argc, char** argv) {
+  const int n = argc > 1 ? atoi(argv[1]) : 16;
+  const int group = argc > 2 ? atoi(argv[2]) : 8;
+  const int iters = argc > 3 ? atoi(argv[3]) : 2000;
+  long long* d;
+  cudaMalloc(&d, 148 * sizeof(long long));
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  bench<<<148, 128, 66 * 1024>>>(n, group, 10, d);
+  bench<<<148, 128, 66 * 1024>>>(n, group, iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  avg /= 148;
+  printf("N=%3d group=%2d: %.1f cycles per MMA (%.1f per group incl. commit+wait) %s\n", n, group,
+         avg / (iters * (double)group), avg / iters, cudaGetErrorString(e));
+  return 0;
+}
