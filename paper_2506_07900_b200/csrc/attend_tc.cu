@@ -41,7 +41,7 @@ constexpr int kD = 128;
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
 constexpr int kStages = 3;
-constexpr int kThreads = 352;
+constexpr int kThreads = 480;          // 0 TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue
 constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to 4 tiles ahead of softmax)
 constexpr uint32_t kColO = kSlots * 16;  // O^T columns [kColO, kColO + 32)
 constexpr int kMaxSel = 80;
@@ -58,8 +58,8 @@ struct Smem {
   static constexpr uint32_t q = kv + kStages * kStageBytes;     // 2 buffers
   static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
   static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
-  static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [4 warps][16] reduction scratch
-  static constexpr uint32_t bars = red + 4 * 16 * 4;
+  static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
+  static constexpr uint32_t bars = red + 8 * 16 * 4;
   static constexpr uint32_t total = bars + 40 * 8;
 };
 
@@ -198,14 +198,14 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
-      mbar_init(p_full + i, 4);
+      mbar_init(p_full + i, 8);
       mbar_init(p_empty + i, 1);
       mbar_init(o_full + i, 1);
       mbar_init(o_empty + i, 4);
-      mbar_init(st_full + i, 4);
+      mbar_init(st_full + i, 8);
       mbar_init(st_empty + i, 4);
     }
-    for (int i = 0; i < kSlots; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, 4); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, 8); }
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
@@ -365,9 +365,14 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       ++it;
     }
-  } else if (warp < 6) {
+  } else if (warp < 10) {
     // -------------------------------------------------------------- softmax
+    // 8 warps: warps w and w+4 share TMEM lane quadrant w%4 (tile rows); the
+    // first four take heads 0..7, the others heads 8..15 of every row.
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int h0 = 8 * half;
+    const int ws = warp - 2;                           // scratch row
     const int row = quad * 32 + lane;                  // tile row == TMEM lane
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const float c2 = 1.4426950408889634f / sqrtf((float)kD);
@@ -388,16 +393,16 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
-      float mrun[kG], lsum[kG], lsx[kG];     // lsum: weights as used by PV; lsx: unrounded (LSE)
+      float mrun[8], lsum[8], lsx[8];     // lsum: weights as used by PV; lsx: unrounded (LSE)
 #pragma unroll
-      for (int h = 0; h < kG; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
+      for (int h = 0; h < 8; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
       for (int c = c0; c < c1; ++c) {
         const int sslot = tcount % kSlots;
         mbar_wait(s_full + sslot, (tcount / kSlots) & 1);
         ++tcount;
         tc_fence_after();
-        float z[kG];
-        tmem_ld16(tmem + lane_base + sslot * kG, z);
+        float z[8];
+        tmem_ld8(tmem + lane_base + sslot * kG + h0, z);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -407,39 +412,38 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         bool valid = (2 * c + x) < nb;
         if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
 #pragma unroll
-        for (int h = 0; h < kG; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
+        for (int h = 0; h < 8; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
         // running max: exact on the first tile, rescale later only if z > M + 8
         bool need = (c == c0);
         if (c > c0) {
           bool over = false;
 #pragma unroll
-          for (int h = 0; h < kG; ++h) over |= z[h] > mrun[h] + 8.f;
+          for (int h = 0; h < 8; ++h) over |= z[h] > mrun[h] + 8.f;
           const unsigned any = __ballot_sync(0xffffffffu, over);
-          if (lane == 0) red[quad * 16] = any ? 1.f : 0.f;
-          named_bar_sync(2, 128);
-          need = (red[0] + red[16] + red[32] + red[48]) > 0.f;
-          named_bar_sync(2, 128);
+          if (lane == 0) red[ws * 16] = any ? 1.f : 0.f;
+          named_bar_sync(2, 256);
+          float f = 0.f;
+#pragma unroll
+          for (int x2 = 0; x2 < 8; ++x2) f += red[x2 * 16];
+          need = f > 0.f;
+          named_bar_sync(2, 256);
         }
         if (need) {
-          float tmax[kG];
+          {
+            float zz[8];
 #pragma unroll
-          for (int h = 0; h < kG; ++h) {
-            float v = z[h];
-            for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-            tmax[h] = v;
+            for (int h = 0; h < 8; ++h) zz[h] = z[h];
+            const float v = warp_reduce8(zz, lane, [](float a, float b) { return fmaxf(a, b); });
+            if ((lane & 3) == 0) red[ws * 16 + reduce_head8(lane)] = v;
           }
-          if (lane < kG) {
-            float mine = tmax[0];
-#pragma unroll
-            for (int h = 1; h < kG; ++h) mine = (lane == h) ? tmax[h] : mine;
-            red[quad * 16 + lane] = mine;
-          }
-          named_bar_sync(2, 128);
-          float corr[kG];
+          named_bar_sync(2, 256);
+          float corr[8];
           bool any_corr = false;
 #pragma unroll
-          for (int h = 0; h < kG; ++h) {
-            const float tm = fmaxf(fmaxf(red[h], red[16 + h]), fmaxf(red[32 + h], red[48 + h]));
+          for (int h = 0; h < 8; ++h) {
+            const int hb = 4 * half;                    // this half's four warps: scratch rows hb..hb+3
+            const float tm = fmaxf(fmaxf(red[(hb + 0) * 16 + h], red[(hb + 1) * 16 + h]),
+                                   fmaxf(red[(hb + 2) * 16 + h], red[(hb + 3) * 16 + h]));
             const float mnew = fmaxf(mrun[h], tm);
             corr[h] = (mrun[h] == -INFINITY) ? 1.f : ex2(mrun[h] - mnew);
             any_corr |= (c > c0) && (corr[h] != 1.f);
@@ -447,18 +451,18 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             lsx[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
             mrun[h] = mnew;
           }
-          named_bar_sync(2, 128);
+          named_bar_sync(2, 256);
           if (c > c0 && any_corr) {
-            // rescale O^T (this thread owns d lane == row): wait for PV(c-1),
-            // whose completion is the next phase of p_empty[buffer of c-1]
+            // rescale this thread's 8 O^T columns (d lane == row): wait for
+            // PV(c-1), whose completion is the next phase of p_empty[its buffer]
             mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
             tc_fence_after();
-            float o[kG];
-            tmem_ld16(tmem + lane_base + kColO + ob * kG, o);
+            float o[8];
+            tmem_ld8(tmem + lane_base + kColO + ob * kG + h0, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int h = 0; h < kG; ++h) o[h] *= corr[h];
-            tmem_st16(tmem + lane_base + kColO + ob * kG, o);
+            for (int h = 0; h < 8; ++h) o[h] *= corr[h];
+            tmem_st8(tmem + lane_base + kColO + ob * kG + h0, o);
             tmem_wait_st();
             tc_fence_before();
           }
@@ -470,9 +474,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         // weights, so O = sum P~ V / sum P~ stays a convex combination (error
         // ~2^-9 |V| / sqrt(rows)).  p_split: P also as a bf16 lo part (second
         // PV MMA), ~16-bit weights, for callers that want 1e-5 outputs.
-        uint32_t phi[kG / 2], plo[kG / 2];
+        uint32_t phi[4], plo[4];
 #pragma unroll
-        for (int h = 0; h < kG; h += 2) {
+        for (int h = 0; h < 8; h += 2) {
           const float a = ex2(z[h] - mrun[h]);
           const float b = ex2(z[h + 1] - mrun[h + 1]);
           const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
@@ -485,13 +489,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           plo[h / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
         }
         uint8_t* pb = smem + Smem::p + pbuf * kPBytes;
-        const uint32_t base = (row >> 3) * 256 + (row & 7) * 16;
+        const uint32_t base = (row >> 3) * 256 + (row & 7) * 16 + 128 * half;
         *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
-        *reinterpret_cast<uint4*>(pb + base + 128) = make_uint4(phi[4], phi[5], phi[6], phi[7]);
-        if (p.p_split) {
-          *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
-          *reinterpret_cast<uint4*>(pb + kPHalf + base + 128) = make_uint4(plo[4], plo[5], plo[6], plo[7]);
-        }
+        if (p.p_split) *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + pbuf);
@@ -501,18 +501,18 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(st_empty + ob, ((it >> 1) & 1) ^ 1);
       float* st = stats + ob * 9 * 16;
       {
-        const float v = warp_reduce16(lsum, lane, [](float a, float b) { return a + b; });
-        const float vx = warp_reduce16(lsx, lane, [](float a, float b) { return a + b; });
-        if ((lane & 1) == 0) {
-          st[quad * 16 + reduce_head(lane)] = v;
-          st[80 + quad * 16 + reduce_head(lane)] = vx;
+        const float v = warp_reduce8(lsum, lane, [](float a, float b) { return a + b; });
+        const float vx = warp_reduce8(lsx, lane, [](float a, float b) { return a + b; });
+        if ((lane & 3) == 0) {
+          st[quad * 16 + h0 + reduce_head8(lane)] = v;
+          st[80 + quad * 16 + h0 + reduce_head8(lane)] = vx;
         }
       }
-      if (quad == 0 && lane < kG) {
+      if (quad == 0 && lane < 8) {
         float mine = mrun[0];
 #pragma unroll
-        for (int h = 1; h < kG; ++h) mine = (lane == h) ? mrun[h] : mine;
-        st[64 + lane] = mine;
+        for (int h = 1; h < 8; ++h) mine = (lane == h) ? mrun[h] : mine;
+        st[64 + h0 + lane] = mine;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(st_full + ob);

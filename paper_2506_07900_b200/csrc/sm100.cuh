@@ -97,6 +97,27 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane, Op op) 
   }
   return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
 }
+// 8 per-lane values: lane l ends with head reduce_head8(l) (lanes sharing bits
+// 4..2 agree); 9 shuffles.
+__device__ __forceinline__ int reduce_head8(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+template <typename Op>
+__device__ __forceinline__ float warp_reduce8(float (&v)[8], int lane, Op op) {
+#pragma unroll
+  for (int w = 4, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
+    }
+  }
+  const float r = op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 2));
+  return op(r, __shfl_xor_sync(0xffffffffu, r, 1));
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -154,6 +175,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
   asm volatile(
