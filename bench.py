@@ -51,6 +51,13 @@ def load_peaks():
             "source": "fallback (B200_PROFILING.md: MEASURED_PEAKS.json absent)"}
 
 
+def load_traffic():
+    """DRAM bytes per launch of each dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json); empty if absent."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(path)) if os.path.exists(path) else {}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -292,6 +299,10 @@ def run_ours(args):
                 "unit": "TFLOP/s", "frac": round(att_tflops / peak_t, 4), "traffic": None,
                 "share_of_step": round(t_att / (t_sel + t_att), 3)}
     roof["peak_source"] = peaks["source"]
+    traffic = load_traffic()
+    if roof["kernel"] in traffic:
+        roof["traffic"] = traffic[roof["kernel"]]["bytes_per_launch"]
+        roof["traffic_note"] = "bytes per launch (one layer), " + traffic["source"]
     roof["stage1_ms_per_step"] = round(t_sel, 3)
     roof["stage2_ms_per_step"] = round(t_att, 3)
     roof["stage1_tflops"] = round(sel_tflops, 2)
@@ -505,7 +516,10 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
             "tokens_per_s": round(S * world / (step_ms / 1e3), 1),
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
-                         "peak_source": peaks["source"], "algorithmic_bytes_per_step": int(bytes_step)},
+                         "peak_source": peaks["source"], "algorithmic_bytes_per_step": int(bytes_step),
+                         "traffic": load_traffic().get("decode_cluster_kernel", {}).get("bytes_per_launch"),
+                         "traffic_note": "DRAM bytes per layer launch (ncu); algorithmic per layer = "
+                                         f"{bytes_step // max(1, layers)}"},
             "e2e": {"ms_per_step": round(ms_e2e / args.steps, 4),
                     "us_per_token": round(ms_e2e / args.steps * 1e3 / (S * world), 2),
                     "h2d_bytes_per_step": int((q.numel() + kn.numel() + vn.numel()) * 2),

@@ -6,6 +6,7 @@ Drop-in for the reference's sparse-attention surface (``deskinfer.sparse``):
 hand-written sm_100a kernels in ``libinfllm2.so`` (C ABI: ``include/infllm2.h``).
 """
 
+from . import model, stages
 from .decode import DecodeBatch
 from .errors import NumericError, ValidationError
 from .sparse import (BlockizedLayerCache, KVCache, SparseAttentionConfig, TouchStats,
@@ -13,7 +14,7 @@ from .sparse import (BlockizedLayerCache, KVCache, SparseAttentionConfig, TouchS
                      partition_blocks, two_stage_attention)
 
 __all__ = [
-    "DecodeBatch", "BlockizedLayerCache", "KVCache", "NumericError", "SparseAttentionConfig", "TouchStats",
+    "model", "stages", "DecodeBatch", "BlockizedLayerCache", "KVCache", "NumericError", "SparseAttentionConfig", "TouchStats",
     "ValidationError", "blockized_cache", "build_kernels", "force_blocks",
     "kernel_range_for_block", "partition_blocks", "two_stage_attention",
 ]
