@@ -8,7 +8,8 @@ tied_lm_head; ``bundle.params``: float32 arrays named as in
 ``param_shapes``; ``bundle.lm_head``), and ``specdec.make_cache``
 (specdec.py:632-641).  Projections, RMSNorm, RoPE and the MLP run in float32
 on the GPU (torch/cuBLAS, TF32 off); the cache appends happen BEFORE
-attending (F4, model.py:434-444); ``backend="sparse"`` calls
+attending (F4, model.py:434-444); q is rounded to bf16 on both backends (the
+operator's input precision, the cache holds bf16 K/V); ``backend="sparse"`` calls
 ``two_stage_attention`` when a cache is given, otherwise the dense causal
 GQA path (F16).  Returns a ``ForwardResult`` of CUDA tensors.
 """
@@ -145,7 +146,9 @@ def forward(bundle, tokens, cache: Optional[KVCache] = None, *, backend: str = "
         q = (h @ p[lp + "attn.wq"]).reshape(n, cfg.n_q_heads, cfg.head_dim)
         k = (h @ p[lp + "attn.wk"]).reshape(n, cfg.n_kv_heads, cfg.head_dim)
         v = (h @ p[lp + "attn.wv"]).reshape(n, cfg.n_kv_heads, cfg.head_dim)
-        q = apply_rope(q, cos, sin)
+        # q enters attention in bf16 on both backends (the operator's input
+        # precision), so the dense and sparse paths see identical inputs
+        q = apply_rope(q, cos, sin).to(torch.bfloat16).float()
         k = apply_rope(k, cos, sin)
         if cache is not None:
             layer = cache.layers[i]
