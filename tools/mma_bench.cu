@@ -8,14 +8,23 @@
 
 using namespace infllm2::sm100;
 
-__global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, long long* out) {
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, long long* out, int ts) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
   if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
-  if (threadIdx.x < 32) tmem_alloc<256>(&slot);
+  if (threadIdx.x < 32) tmem_alloc<512>(&slot);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -29,8 +38,10 @@ __global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, lon
     uint32_t ph = 0;
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
-      for (int k = 0; k < group; ++k)
-        umma_f16_ss(tmem, da + ((k & 3) * 32 >> 4), db + ((k & 3) * 32 >> 4), idesc, k > 0 ? 1u : 0u);
+      for (int k = 0; k < group; ++k) {
+        if (ts) umma_ts(tmem, tmem + 256 + (k & 3) * 8, db + ((k & 3) * 32 >> 4), idesc, k > 0 ? 1u : 0u);
+        else umma_f16_ss(tmem, da + ((k & 3) * 32 >> 4), db + ((k & 3) * 32 >> 4), idesc, k > 0 ? 1u : 0u);
+      }
       umma_commit(&bar);
       mbar_wait(&bar, ph);
       ph ^= 1;
@@ -40,25 +51,26 @@ __global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, lon
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
+  if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 16;
   const int group = argc > 2 ? atoi(argv[2]) : 8;
   const int iters = argc > 3 ? atoi(argv[3]) : 2000;
+  const int ts = argc > 4 ? atoi(argv[4]) : 0;
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  bench<<<148, 128, 66 * 1024>>>(n, group, 10, d);
-  bench<<<148, 128, 66 * 1024>>>(n, group, iters, d);
+  bench<<<148, 128, 66 * 1024>>>(n, group, 10, d, ts);
+  bench<<<148, 128, 66 * 1024>>>(n, group, iters, d, ts);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += h[i];
   avg /= 148;
-  printf("N=%3d group=%2d: %.1f cycles per MMA (%.1f per group incl. commit+wait) %s\n", n, group,
+  printf("%s N=%3d group=%2d: %.1f cycles per MMA (%.1f per group incl. commit+wait) %s\n", ts ? "TS" : "SS", n, group,
          avg / (iters * (double)group), avg / iters, cudaGetErrorString(e));
   return 0;
 }
