@@ -904,7 +904,9 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       {
         // ---- merge (every piece): the global top-B lies in the union of the local lists
         float* lk = sarr;                                         // [n][2] (key, id bits)
-        int* chosen = reinterpret_cast<int*>(smem + Smem::p);    // P buffer is idle here
+        // the P buffer doubles as the chosen-id list: the forced tiles' PV must be done with it
+        if (ti > 0) mbar_wait(o_full, tp_prev);
+        int* chosen = reinterpret_cast<int*>(smem + Smem::p);
         const int n = dense ? 0 : P * I.budget;
         for (int x = tid; x < n; x += 128) {
           const float2 kv = ld_dsmem2(xcand + 2 * (x % I.budget), x / I.budget);
