@@ -426,7 +426,6 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
   const int cid = blockIdx.x / P;
   const int nseg = p.n_seq * p.hkv;
   const TableView tv = table_view(p.table, p.n_seq);
-  for (int s = threadIdx.x; s < p.n_seq; s += blockDim.x) len_s[s] = tv.len[s];
   if (threadIdx.x == 0) {
     trace(p.trace, 0);
     if (p.trace && blockIdx.x < kTraceCtas)
@@ -455,6 +454,12 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
   cluster_sync_all();                    // barrier inits visible to the cluster before any remote arrival
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: the prologue above overlaps the previous
+  // layer's tail; its q / k_new / lengths are visible past pdl_wait().
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int s = threadIdx.x; s < p.n_seq; s += blockDim.x) len_s[s] = tv.len[s];
+  __syncthreads();
 
   if (warp == 0) {
     // ============================================================ producer
@@ -1183,18 +1188,21 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t
   if (np <= 0) return INFLLM2_ERR_UNSUPPORTED;
   int ncl = max_active_clusters(np);
   if (ncl > nseg) ncl = nseg;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = np;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = getenv("INFLLM2_DECODE_NOPDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * np));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Smem::total + 1024;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   count_launch();
   if (cudaLaunchKernelEx(&cfg, decode_cluster_kernel, tq, p) != cudaSuccess) return INFLLM2_ERR_CUDA;
   return INFLLM2_OK;
