@@ -77,49 +77,64 @@ __device__ __forceinline__ void warp_best_after(float& bv, int& bb) {
 // One query's selection by one warp: forced init blocks, the `budget` best
 // candidates of rq[n_init, local_lo) by (score desc, id asc), forced local
 // blocks; written ascending with -1 padding (select_topk, sparse.py:247-277).
-// Fast path (budget <= 32): threshold T0 = budget-th largest lane maximum
-// (at least `budget` candidates reach it, so the answer lies in {r >= T0}),
-// compact that set in id order, pick `budget` from it, bitonic-sort the ids.
+// Fast path (budget <= 64): threshold T0 = budget-th largest of the lanes' top
+// one (budget <= 32) or top two (budget <= 64) values -- at least `budget`
+// candidates reach it, so the answer lies in {r >= T0} -- compact that set in
+// id order, rank it exactly, and the ballot-compacted survivors come out
+// ascending.  Iterative order statistics only when the set overflows the list
+// (massive exact ties) or budget > 64.
 __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, int lane, float* lkey, int* lid, int32_t* out,
                             double* osc, int max_sel) {
   const int lo = (int)u.n_init, hi = (int)u.local_lo;
   const int budget = (int)u.budget;
-  int chosen = INT_MAX;          // lane x < budget holds the x-th chosen id
+  int chosen0 = INT_MAX, chosen1 = INT_MAX;   // lane x holds the x-th / (32+x)-th chosen id
+  bool fast = false;
   if (budget >= u.n_free) {
     // dense regime: every candidate is selected (assembled below)
-  } else if (budget > 0 && budget <= 32) {
-    float m = -1.f;
-    {
-      int b = lo + lane;
-      for (; b + 96 < hi; b += 128) {
-        const float a0 = rq[b], a1 = rq[b + 32], a2 = rq[b + 64], a3 = rq[b + 96];
-        m = fmaxf(m, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
-      }
-      for (; b < hi; b += 32) m = fmaxf(m, rq[b]);
+  } else if (budget > 0 && budget <= 64) {
+    float m1 = -1.f, m2 = -1.f;                 // lane's two largest values
+    for (int b = lo + lane; b < hi; b += 32) {
+      const float a = rq[b];
+      if (a > m1) { m2 = m1; m1 = a; }
+      else if (a > m2) m2 = a;
     }
-    const float t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m, lane), budget - 1);
+    float t0;
+    if (budget <= 32) {
+      t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m1, lane), budget - 1);
+    } else {
+      // budget-th largest of the 64 values {m1, m2}: count values above / at least
+      int gt1 = 0, ge1 = 0, gt2 = 0, ge2 = 0;
+      for (int x = 0; x < 32; ++x) {
+        const float a = __shfl_sync(0xffffffffu, m1, x), c = __shfl_sync(0xffffffffu, m2, x);
+        gt1 += (a > m1) + (c > m1);
+        ge1 += (a >= m1) + (c >= m1);
+        gt2 += (a > m2) + (c > m2);
+        ge2 += (a >= m2) + (c >= m2);
+      }
+      const bool k1 = gt1 < budget && ge1 >= budget, k2 = gt2 < budget && ge2 >= budget;
+      const unsigned b1 = __ballot_sync(0xffffffffu, k1), b2 = __ballot_sync(0xffffffffu, k2);
+      t0 = b1 ? __shfl_sync(0xffffffffu, m1, __ffs(b1) - 1) : __shfl_sync(0xffffffffu, m2, __ffs(b2) - 1);
+    }
     int cnt = 0;
-    bool overflow = false;
     for (int base = lo; base < hi; base += 128) {
       float r4[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int b = base + 32 * u + lane;
-        r4[u] = b < hi ? rq[b] : -2.f;
+      for (int x = 0; x < 4; ++x) {
+        const int b = base + 32 * x + lane;
+        r4[x] = b < hi ? rq[b] : -2.f;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int b = base + 32 * u + lane;
-        const bool f = r4[u] >= t0;
+      for (int x = 0; x < 4; ++x) {
+        const int b = base + 32 * x + lane;
+        const bool f = r4[x] >= t0;
         const unsigned mask = __ballot_sync(0xffffffffu, f);
         const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
-        if (f && pos < kListCap - kOutCap) { lkey[pos] = r4[u]; lid[pos] = b; }
+        if (f && pos < kListCap - kOutCap) { lkey[pos] = r4[x]; lid[pos] = b; }
         cnt += __popc(mask);
       }
     }
-    overflow = cnt > kListCap - kOutCap;
     __syncwarp();
-    if (!overflow) {
+    if (cnt <= kListCap - kOutCap) {
       // rank every listed candidate against the whole list (no dependent
       // chains), keep rank < budget; the list is in id order, so a ballot
       // compaction emits the chosen ids already ascending.
@@ -131,6 +146,7 @@ __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, i
           const float rk = lkey[x];
           const int bk = lid[x];
           int rank = 0;
+#pragma unroll 4
           for (int f = 0; f < cnt; ++f) rank += better(lkey[f], lid[f], rk, bk) ? 1 : 0;
           keep = rank < budget;
         }
@@ -140,27 +156,14 @@ __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, i
         taken += __popc(mask);
       }
       __syncwarp();
-      chosen = lane < budget ? lid[kListCap - kOutCap + lane] : INT_MAX;
+      chosen0 = lane < budget ? lid[kListCap - kOutCap + lane] : INT_MAX;
+      chosen1 = lane + 32 < budget ? lid[kListCap - kOutCap + 32 + lane] : INT_MAX;
       __syncwarp();
-    } else {
-      float pv = INFINITY;
-      int pb = -1;
-      for (int it = 0; it < budget; ++it) {
-        float bv = -1.f;
-        int bb = -1;
-        for (int b = lo + lane; b < hi; b += 32) {
-          const float r = rq[b];
-          if ((pb < 0 || better(pv, pb, r, b)) && (bb < 0 || better(r, b, bv, bb))) { bv = r; bb = b; }
-        }
-        warp_best_after(bv, bb);
-        if (lane == it) chosen = bb;
-        pv = bv;
-        pb = bb;
-      }
-      chosen = warp_sort_asc(chosen, lane);
+      fast = true;
     }
-  } else if (budget > 32) {
-    // rare large budgets: iterative order-statistics over the whole range
+  }
+  if (budget < u.n_free && budget > 0 && !fast) {
+    // rare: iterative order statistics over the whole range (massive ties or budget > 64)
     float pv = INFINITY;
     int pb = -1;
     for (int it = 0; it < budget; ++it) {
@@ -194,7 +197,7 @@ __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, i
     else if (x < lo + n_ch) {
       const int c = x - lo;
       if (budget >= u.n_free) id = lo + c;
-      else if (budget <= 32) id = -2;  // filled from registers below
+      else if (fast) id = -2;  // filled from registers below
       else id = __float_as_int(lkey[c]);
     } else if (x < lo + n_ch + n_loc) id = (int)u.local_lo + (x - lo - n_ch);
     if (id != -2) {
@@ -202,11 +205,14 @@ __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, i
       if (osc) osc[x] = id >= 0 ? (double)rq[id] : 0.0;
     }
   }
-  if (budget < u.n_free && budget > 0 && budget <= 32) {
-    // lane c holds the c-th smallest chosen id
+  if (fast) {
     if (lane < budget) {
-      out[lo + lane] = chosen;
-      if (osc) osc[lo + lane] = (double)rq[chosen];
+      out[lo + lane] = chosen0;
+      if (osc) osc[lo + lane] = (double)rq[chosen0];
+    }
+    if (lane + 32 < budget) {
+      out[lo + 32 + lane] = chosen1;
+      if (osc) osc[lo + 32 + lane] = (double)rq[chosen1];
     }
   }
 }
