@@ -53,14 +53,32 @@ constexpr uint32_t kQBytes = 2 * kG * 128;              // 4 KB (two 64-d halves
 constexpr uint32_t kPBytes = 2 * kRowsT * kG * 2;       // 8 KB: P_hi and P_lo (bf16 each)
 constexpr uint32_t kPHalf = kRowsT * kG * 2;            // 4 KB
 
-struct Smem {
-  static constexpr uint32_t kv = 0;
-  static constexpr uint32_t q = kv + kStages * kStageBytes;     // 2 buffers
-  static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
-  static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
-  static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
-  static constexpr uint32_t bars = red + 8 * 16 * 4;
-  static constexpr uint32_t total = bars + 40 * 8;
+// Per-geometry constants: G heads per KV group (16 or 8), head dim D (128 or
+// 64).  MiniCPM4-8B is (16, 128), MiniCPM4-0.5B (8, 64).  Tiles stay 128 rows;
+// a D = 64 tile is one 128-B swizzle half, so the ring holds twice the stages.
+template <int G, int D>
+struct AttCfg {
+  static constexpr int kDH = D / 64;                              // 64-d halves per row
+  static constexpr uint32_t kTileBytes = kDH * kHalfBytes;        // K or V tile
+  static constexpr uint32_t kStageBytes = 2 * kTileBytes;
+  static constexpr int kStages = 3 * (128 / D);
+  static constexpr uint32_t kQBytes = kDH * G * 128;
+  static constexpr uint32_t kPHalf = kRowsT * G * 2;
+  static constexpr uint32_t kPBytes = 2 * kPHalf;
+  static constexpr uint32_t kColO = kSlots * G;                   // O^T buffers at [kColO, kColO + 2G)
+  static constexpr uint32_t kTmemCols = (kSlots + 2) * G <= 64 ? 64 : 128;
+  static constexpr int kSH = G / 2;                               // heads per softmax thread
+  struct Smem {
+    static constexpr uint32_t kv = 0;
+    // D = 64: PV runs M = 128 over a half-width V tile, so the last stage's V
+    // operand spans kHalfBytes past the ring: pad, never read back
+    static constexpr uint32_t q = kv + kStages * kStageBytes + (kDH == 1 ? kHalfBytes : 0);   // 2 buffers
+    static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
+    static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
+    static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
+    static constexpr uint32_t bars = red + 8 * 16 * 4;
+    static constexpr uint32_t total = bars + 48 * 8;
+  };
 };
 
 struct Params {
@@ -170,14 +188,27 @@ struct SelPrefetch {
 };
 
 
+template <int G, int D>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  using C = AttCfg<G, D>;
+  using Smem = typename C::Smem;
+  constexpr int kG = G;
+  constexpr int kD = D;
+  constexpr int kStages = C::kStages;
+  constexpr uint32_t kTileBytes = C::kTileBytes;
+  constexpr uint32_t kStageBytes = C::kStageBytes;
+  constexpr uint32_t kQBytes = C::kQBytes;
+  constexpr uint32_t kPBytes = C::kPBytes;
+  constexpr uint32_t kPHalf = C::kPHalf;
+  constexpr uint32_t kColO = C::kColO;
+  constexpr int kSH = C::kSH;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
-  uint64_t* kv_full = bars;               // [3]
-  uint64_t* kv_empty = bars + 3;          // [3]
+  uint64_t* kv_full = bars + 38;          // [kStages <= 6]
+  uint64_t* kv_empty = bars + 44;         // [kStages <= 6]
   uint64_t* q_full = bars + 6;            // [2]
   uint64_t* q_empty = bars + 8;           // [2]
   uint64_t* s_full = bars + 28;           // [kSlots]
@@ -194,7 +225,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 3; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+    for (int i = 0; i < kStages; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -211,7 +242,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
   }
-  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
@@ -246,8 +277,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         mbar_wait(q_empty + qb, q_par);
         mbar_arrive_expect_tx(q_full + qb, kQBytes);
         uint8_t* qd = smem + Smem::q + qb * kQBytes;
-        tma_load_3d(qd, &tm_q, q_full + qb, 0, grp * kG, (int)i);
-        tma_load_3d(qd + kQBytes / 2, &tm_q, q_full + qb, 64, grp * kG, (int)i);
+#pragma unroll
+        for (int hh = 0; hh < C::kDH; ++hh) tma_load_3d(qd + hh * kG * 128, &tm_q, q_full + qb, 64 * hh, grp * kG, (int)i);
       }
       for (int c = c0; c < c1; ++c) {
         const int nt = (nb - 2 * c) >= 2 ? 2 : 1;
@@ -255,16 +286,17 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         if (lane == 0) {
           mbar_wait(kv_empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(kv_full + stage, nt * 4 * (kM * 128));
+          mbar_arrive_expect_tx(kv_full + stage, nt * 2 * C::kDH * (kM * 128));
           uint8_t* kd = smem + Smem::kv + stage * kStageBytes;
           uint8_t* vd = kd + kTileBytes;
           for (int x = 0; x < nt; ++x) {
             const int row0 = (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
-            tma_load_3d(kd + off, mk, kv_full + stage, 0, row0, grp);
-            tma_load_3d(kd + kHalfBytes + off, mk, kv_full + stage, 64, row0, grp);
-            tma_load_3d(vd + off, mv, kv_full + stage, 0, row0, grp);
-            tma_load_3d(vd + kHalfBytes + off, mv, kv_full + stage, 64, row0, grp);
+#pragma unroll
+            for (int hh = 0; hh < C::kDH; ++hh) {
+              tma_load_3d(kd + hh * kHalfBytes + off, mk, kv_full + stage, 64 * hh, row0, grp);
+              tma_load_3d(vd + hh * kHalfBytes + off, mv, kv_full + stage, 64 * hh, row0, grp);
+            }
           }
         }
         __syncwarp();
@@ -307,7 +339,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
-            const uint32_t qoff = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+            const uint32_t qoff = (k >> 2) * (kG * 128) + (k & 3) * 32;
             umma_f16_ss(tmem + slot * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk, k > 0 ? 1u : 0u);
           }
           umma_commit(s_full + slot);
@@ -346,14 +378,16 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (elect_one()) {
           const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + stage * kStageBytes + kTileBytes),
                                              kHalfBytes, 1024);
-          const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 256, 128);
+          // P^T (K = rows, N = heads, no swizzle): 8-row K groups of 16*G bytes, 8-head groups 128 B apart
+          const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 16 * kG, 128);
           const uint32_t ocol = tmem + kColO + ob * kG;
           const uint32_t acc0 = c > c0 ? 1u : 0u;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (k < ksteps) {
-              umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + (k * 512 >> 4), idesc_pv, (acc0 | k) ? 1u : 0u);
-              if (p.p_split) umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + ((kPHalf + k * 512) >> 4), idesc_pv, 1u);
+              umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + (k * 32 * kG >> 4), idesc_pv, (acc0 | k) ? 1u : 0u);
+              if (p.p_split)
+                umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + ((kPHalf + k * 32 * kG) >> 4), idesc_pv, 1u);
             }
           }
           umma_commit(kv_empty + stage);
@@ -371,7 +405,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     // first four take heads 0..7, the others heads 8..15 of every row.
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    const int h0 = 8 * half;
+    const int h0 = kSH * half;
     const int ws = warp - 2;                           // scratch row
     const int row = quad * 32 + lane;                  // tile row == TMEM lane
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
@@ -393,16 +427,16 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
-      float mrun[8], lsum[8], lsx[8];     // lsum: weights as used by PV; lsx: unrounded (LSE)
+      float mrun[kSH], lsum[kSH], lsx[kSH];     // lsum: weights as used by PV; lsx: unrounded (LSE)
 #pragma unroll
-      for (int h = 0; h < 8; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
+      for (int h = 0; h < kSH; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
       for (int c = c0; c < c1; ++c) {
         const int sslot = tcount % kSlots;
         mbar_wait(s_full + sslot, (tcount / kSlots) & 1);
         ++tcount;
         tc_fence_after();
-        float z[8];
-        tmem_ld8(tmem + lane_base + sslot * kG + h0, z);
+        float z[kSH];
+        tmem_ld_n<kSH>(tmem + lane_base + sslot * kG + h0, z);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -412,13 +446,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         bool valid = (2 * c + x) < nb;
         if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
 #pragma unroll
-        for (int h = 0; h < 8; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
+        for (int h = 0; h < kSH; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
         // running max: exact on the first tile, rescale later only if z > M + 8
         bool need = (c == c0);
         if (c > c0) {
           bool over = false;
 #pragma unroll
-          for (int h = 0; h < 8; ++h) over |= z[h] > mrun[h] + 8.f;
+          for (int h = 0; h < kSH; ++h) over |= z[h] > mrun[h] + 8.f;
           const unsigned any = __ballot_sync(0xffffffffu, over);
           if (lane == 0) red[ws * 16] = any ? 1.f : 0.f;
           named_bar_sync(2, 256);
@@ -430,17 +464,17 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         }
         if (need) {
           {
-            float zz[8];
+            float zz[kSH];
 #pragma unroll
-            for (int h = 0; h < 8; ++h) zz[h] = z[h];
-            const float v = warp_reduce8(zz, lane, [](float a, float b) { return fmaxf(a, b); });
-            if ((lane & 3) == 0) red[ws * 16 + reduce_head8(lane)] = v;
+            for (int h = 0; h < kSH; ++h) zz[h] = z[h];
+            const float v = warp_reduce_n<kSH>(zz, lane, [](float a, float b) { return fmaxf(a, b); });
+            if (reduce_writer_n<kSH>(lane)) red[ws * 16 + reduce_head_n<kSH>(lane)] = v;
           }
           named_bar_sync(2, 256);
-          float corr[8];
+          float corr[kSH];
           bool any_corr = false;
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
+          for (int h = 0; h < kSH; ++h) {
             const int hb = 4 * half;                    // this half's four warps: scratch rows hb..hb+3
             const float tm = fmaxf(fmaxf(red[(hb + 0) * 16 + h], red[(hb + 1) * 16 + h]),
                                    fmaxf(red[(hb + 2) * 16 + h], red[(hb + 3) * 16 + h]));
@@ -457,12 +491,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             // PV(c-1), whose completion is the next phase of p_empty[its buffer]
             mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
             tc_fence_after();
-            float o[8];
-            tmem_ld8(tmem + lane_base + kColO + ob * kG + h0, o);
+            float o[kSH];
+            tmem_ld_n<kSH>(tmem + lane_base + kColO + ob * kG + h0, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int h = 0; h < 8; ++h) o[h] *= corr[h];
-            tmem_st8(tmem + lane_base + kColO + ob * kG + h0, o);
+            for (int h = 0; h < kSH; ++h) o[h] *= corr[h];
+            tmem_st_n<kSH>(tmem + lane_base + kColO + ob * kG + h0, o);
             tmem_wait_st();
             tc_fence_before();
           }
@@ -474,9 +508,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         // weights, so O = sum P~ V / sum P~ stays a convex combination (error
         // ~2^-9 |V| / sqrt(rows)).  p_split: P also as a bf16 lo part (second
         // PV MMA), ~16-bit weights, for callers that want 1e-5 outputs.
-        uint32_t phi[4], plo[4];
+        uint32_t phi[kSH / 2], plo[kSH / 2];
 #pragma unroll
-        for (int h = 0; h < 8; h += 2) {
+        for (int h = 0; h < kSH; h += 2) {
           const float a = ex2(z[h] - mrun[h]);
           const float b = ex2(z[h + 1] - mrun[h + 1]);
           const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
@@ -489,9 +523,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           plo[h / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
         }
         uint8_t* pb = smem + Smem::p + pbuf * kPBytes;
-        const uint32_t base = (row >> 3) * 256 + (row & 7) * 16 + 128 * half;
-        *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
-        if (p.p_split) *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
+        // P^T core matrices: 8 rows x 8 heads (128 B), 8-row groups 16*G bytes apart
+        const uint32_t base = (row >> 3) * (16 * kG) + (row & 7) * 16 + 128 * (h0 >> 3) + 2 * (h0 & 7);
+        if constexpr (kSH == 8) {
+          *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
+          if (p.p_split) *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
+        } else {
+          *reinterpret_cast<uint2*>(pb + base) = make_uint2(phi[0], phi[1]);
+          if (p.p_split) *reinterpret_cast<uint2*>(pb + kPHalf + base) = make_uint2(plo[0], plo[1]);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + pbuf);
@@ -501,17 +541,17 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(st_empty + ob, ((it >> 1) & 1) ^ 1);
       float* st = stats + ob * 9 * 16;
       {
-        const float v = warp_reduce8(lsum, lane, [](float a, float b) { return a + b; });
-        const float vx = warp_reduce8(lsx, lane, [](float a, float b) { return a + b; });
-        if ((lane & 3) == 0) {
-          st[quad * 16 + h0 + reduce_head8(lane)] = v;
-          st[80 + quad * 16 + h0 + reduce_head8(lane)] = vx;
+        const float v = warp_reduce_n<kSH>(lsum, lane, [](float a, float b) { return a + b; });
+        const float vx = warp_reduce_n<kSH>(lsx, lane, [](float a, float b) { return a + b; });
+        if (reduce_writer_n<kSH>(lane)) {
+          st[quad * 16 + h0 + reduce_head_n<kSH>(lane)] = v;
+          st[80 + quad * 16 + h0 + reduce_head_n<kSH>(lane)] = vx;
         }
       }
-      if (quad == 0 && lane < 8) {
+      if (quad == 0 && lane < kSH) {
         float mine = mrun[0];
 #pragma unroll
-        for (int h = 1; h < 8; ++h) mine = (lane == h) ? mrun[h] : mine;
+        for (int h = 1; h < kSH; ++h) mine = (lane == h) ? mrun[h] : mine;
         st[64 + h0 + lane] = mine;
       }
       __syncwarp();
@@ -547,7 +587,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(st_full + ob, par);
       tc_fence_after();
       float o[kG];
-      tmem_ld16(tmem + lane_base + kColO + ob * kG, o);
+      tmem_ld_n<kG>(tmem + lane_base + kColO + ob * kG, o);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
@@ -573,7 +613,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         continue;
       }
       const int64_t obase = (i * p.hq + (int64_t)grp * kG) * kD + d;
-      if (p.out_f32) {
+      if (d >= kD) {
+        // O^T lanes >= D (D = 64 runs PV with M = 128 over a half-width V tile): unused
+      } else if (p.out_f32) {
         float* out = static_cast<float*>(p.out);
 #pragma unroll
         for (int h = 0; h < kG; ++h) out[obase + h * kD] = o[h] / l[h];
@@ -591,7 +633,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<128>(tmem);
+  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
 // Merge split-K partials of each (row, group) item: O = sum_p O_p 2^(m_p - M) /
@@ -679,8 +721,9 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
   const uint32_t box[3] = {64, (uint32_t)kG, 1};
   if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
-  const size_t smem = Smem::total + 1024;
-  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = AttCfg<16, 128>::Smem::total + 1024;
+  cudaError_t e =
+      cudaFuncSetAttribute(attend_tc_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t items = n_seq * hkv * p.parts;
   int dev = 0, sms = kNumSMs;
@@ -697,7 +740,7 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   count_launch();
-  e = cudaLaunchKernelEx(&cfg, attend_tc_kernel, tq, tq, tq, p);
+  e = cudaLaunchKernelEx(&cfg, attend_tc_kernel<16, 128>, tq, tq, tq, p);
   if (e != cudaSuccess) return e;
   if (split_ws) {
     cfg.gridDim = dim3((unsigned)(n_seq * hkv));
@@ -719,9 +762,49 @@ static int group_major_enabled() {
   return v;
 }
 
+template <int G, int D>
+static cudaError_t launch_attend_prefill(const CallShape& cs, const void* q, int64_t q_row_stride,
+                                         const void* k_cache, const void* v_cache, int64_t cap, const Params& p,
+                                         cudaStream_t stream) {
+  CUtensorMap tq, tk, tv;
+  {
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.hq, (uint64_t)cs.n};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};
+    const uint32_t box[3] = {64, (uint32_t)G, 1};
+    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.cache_len, (uint64_t)cs.hkv};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)cap * D * 2};
+    const uint32_t box[3] = {64, (uint32_t)kM, 1};
+    if (!encode_tmap_3d_bf16(&tk, k_cache, dims, strides, box)) return cudaErrorInvalidValue;
+    if (!encode_tmap_3d_bf16(&tv, v_cache, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  const size_t smem = AttCfg<G, D>::Smem::total + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<G, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = cs.n * cs.hkv;
+  static const int ctas_cap = [] {
+    const char* e = getenv("INFLLM2_ATTEND_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (ctas_cap > 0 && ctas_cap < sms) sms = ctas_cap;
+  const int grid = (int)(items < sms ? items : sms);
+  count_launch();
+  attend_tc_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
 bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
   if (!tc_kernels_enabled()) return false;
-  if (cs.group != kG || cs.d != kD || g.block_size != kM) return false;
+  const bool shape_ok = (cs.group == 16 && cs.d == 128) || (cs.group == 8 && cs.d == 64);
+  if (!shape_ok || g.block_size != kM) return false;
   if (cs.max_sel > kMaxSel) return false;
   return cs.n > 0;
 }
@@ -748,39 +831,8 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.parts = 1;
   p.part_o = nullptr;
   p.part_ml = nullptr;
-  CUtensorMap tq, tk, tv;
-  {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)cs.n};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)q_row_stride * 2};
-    const uint32_t box[3] = {64, (uint32_t)kG, 1};
-    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
-  }
-  {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.cache_len, (uint64_t)cs.hkv};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)cap * kD * 2};
-    const uint32_t box[3] = {64, (uint32_t)kM, 1};
-    if (!encode_tmap_3d_bf16(&tk, k_cache, dims, strides, box)) return cudaErrorInvalidValue;
-    if (!encode_tmap_3d_bf16(&tv, v_cache, dims, strides, box)) return cudaErrorInvalidValue;
-  }
-  const size_t smem = Smem::total + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  int dev = 0, sms = kNumSMs;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t items = cs.n * cs.hkv;
-  static const int ctas_cap = [] {
-    const char* e = getenv("INFLLM2_ATTEND_CTAS");
-    return e ? atoi(e) : 0;
-  }();
-  if (ctas_cap > 0 && ctas_cap < sms) sms = ctas_cap;
-  const int grid = (int)(items < sms ? items : sms);
-  count_launch();
-  attend_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
-  return cudaGetLastError();
+  if (cs.group == 8 && cs.d == 64) return launch_attend_prefill<8, 64>(cs, q, q_row_stride, k_cache, v_cache, cap, p, stream);
+  return launch_attend_prefill<16, 128>(cs, q, q_row_stride, k_cache, v_cache, cap, p, stream);
 }
 
 }  // namespace infllm2

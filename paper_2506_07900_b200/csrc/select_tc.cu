@@ -62,16 +62,27 @@ constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 
 constexpr uint32_t kMuStageBytes = 4 * kMuHalfBytes;       // hi h0,h1, lo h0,h1 = 64 KB
 constexpr int kSTileLd = kNT + 4;                          // [carry | 128 kernels] + pad
 
-struct SmemLayout {
-  static constexpr uint32_t q = 0;
-  static constexpr uint32_t mu = q + kQBytes;
-  static constexpr uint32_t stile = mu + kStages * kMuStageBytes;          // float [kQ][kSTileLd]
-  static constexpr uint32_t lse2 = stile + kQ * kSTileLd * 4;              // float [kRows]
-  static constexpr uint32_t bars = lse2 + kRows * 4;                       // uint64 [..]
-  static constexpr uint32_t topk = bars + 24 * 8;                          // per top-k warp lists
-  static constexpr uint32_t topk_per_warp = kListCap * 8;
-  static constexpr uint32_t total = topk + kTopkWarps * topk_per_warp + 16;
+// Per-geometry constants: G heads per KV group, head dim D; a unit is always
+// 256 (query, head) rows, i.e. kQ = 256 / G query positions (16 for the 8B
+// shape, 32 for MiniCPM4-0.5B's G = 8, D = 64).
+template <int G, int D>
+struct SelCfg {
+  static constexpr int kQ = kRows / G;
+  static constexpr int kDH = D / 64;
+  static constexpr uint32_t kQBytes = kRows * D * 2;
+  static constexpr uint32_t kMuStageBytes = 2 * kDH * kMuHalfBytes;   // hi halves, then lo halves
+  struct Smem {
+    static constexpr uint32_t q = 0;
+    static constexpr uint32_t mu = q + kQBytes;
+    static constexpr uint32_t stile = mu + kStages * kMuStageBytes;   // float [kQ][kSTileLd]
+    static constexpr uint32_t lse2 = stile + kQ * kSTileLd * 4;       // float [kRows]
+    static constexpr uint32_t bars = lse2 + kRows * 4;                // uint64 [..]
+    static constexpr uint32_t topk = bars + 24 * 8;                   // per top-k warp lists
+    static constexpr uint32_t topk_per_warp = kListCap * 8;
+    static constexpr uint32_t total = topk + kTopkWarps * topk_per_warp + 16;
+  };
 };
+
 
 struct Params {
   int64_t n, start, cache_len, nk_total;
@@ -85,19 +96,23 @@ struct Params {
   float* rbuf;                    // [grid][2][kQ][nb_cap]  block scores, double-buffered per unit
   int64_t nb_cap;
   float zscale;                   // log2(e)/sqrt(D)
+  int kq;                         // query positions per unit (256 / G)
 };
 
 // unit index -> (t0, group); heaviest (largest t0) units first
 __device__ __forceinline__ void unit_coords(const Params& p, int64_t u, int64_t* t0, int* grp) {
   const int64_t tile = p.units_per_group - 1 - u / p.hkv;
   *grp = (int)(u % p.hkv);
-  *t0 = p.first_t0 + tile * kQ;
+  *t0 = p.first_t0 + tile * p.kq;
 }
 
-__device__ __forceinline__ int64_t unit_nk(const Params& p, int64_t t0) {
-  int64_t nk = t0 / 16 + 1;
+// kernel count of query position t (sparse.py:426)
+__device__ __forceinline__ int64_t pos_nk(const Params& p, int64_t t) {
+  int64_t nk = t / 16 + 1;
   return nk < p.nk_total ? nk : p.nk_total;
 }
+// largest kernel count in the unit (its last query)
+__device__ __forceinline__ int64_t unit_nk(const Params& p, int64_t t0) { return pos_nk(p, t0 + p.kq - 1); }
 
 __device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t nk) {
   const int64_t qb = t0 / p.m;
@@ -106,9 +121,17 @@ __device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t n
   return (int)((need + kNT - 1) / kNT);
 }
 
+template <int G, int D>
 __global__ void __launch_bounds__(kThreads, 1)
 select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_hi,
                  const __grid_constant__ CUtensorMap tm_lo, const Params p) {
+  using C = SelCfg<G, D>;
+  using SmemLayout = typename C::Smem;
+  constexpr int kQ = C::kQ;
+  constexpr int kG = G;
+  constexpr int kD = D;
+  constexpr uint32_t kQBytes = C::kQBytes;
+  constexpr uint32_t kMuStageBytes = C::kMuStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sq = smem + SmemLayout::q;
@@ -164,17 +187,18 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         q_phase ^= 1;
         mbar_arrive_expect_tx(q_full, kQBytes);
         const int i0 = (int)(t0 - p.start);
-        tma_load_3d(sq, &tm_q, q_full, 0, grp * kG, i0);
-        tma_load_3d(sq + kQBytes / 2, &tm_q, q_full, 64, grp * kG, i0);
+#pragma unroll
+        for (int hh = 0; hh < C::kDH; ++hh) tma_load_3d(sq + hh * (kRows * 128), &tm_q, q_full, 64 * hh, grp * kG, i0);
         for (int pass = 0; pass < 2; ++pass) {
           for (int c = 0; c < tiles; ++c) {
             mbar_wait(mu_empty + stage, phase ^ 1);
             uint8_t* dst = smu + stage * kMuStageBytes;
             mbar_arrive_expect_tx(mu_full + stage, kMuStageBytes);
-            tma_load_3d(dst, &tm_hi, mu_full + stage, 0, c * kNT, grp);
-            tma_load_3d(dst + kMuHalfBytes, &tm_hi, mu_full + stage, 64, c * kNT, grp);
-            tma_load_3d(dst + 2 * kMuHalfBytes, &tm_lo, mu_full + stage, 0, c * kNT, grp);
-            tma_load_3d(dst + 3 * kMuHalfBytes, &tm_lo, mu_full + stage, 64, c * kNT, grp);
+#pragma unroll
+            for (int hh = 0; hh < C::kDH; ++hh) {
+              tma_load_3d(dst + hh * kMuHalfBytes, &tm_hi, mu_full + stage, 64 * hh, c * kNT, grp);
+              tma_load_3d(dst + (C::kDH + hh) * kMuHalfBytes, &tm_lo, mu_full + stage, 64 * hh, c * kNT, grp);
+            }
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
@@ -207,11 +231,11 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const uint32_t mu_s = mu_addr + stage * kMuStageBytes;
             const uint32_t d0 = tmem + buf * 256;
             for (int part = 0; part < 2; ++part) {           // hi, then lo
-              const uint32_t mu_p = mu_s + part * 2 * kMuHalfBytes;
+              const uint32_t mu_p = mu_s + part * C::kDH * kMuHalfBytes;
               for (int k = 0; k < kD / 16; ++k) {
                 const uint32_t koff = (k >> 2) * 0 + (k & 3) * 32;
                 const uint32_t mu_k = mu_p + (k >> 2) * kMuHalfBytes + koff;
-                const uint32_t q_k = q_addr + (k >> 2) * (kQBytes / 2) + koff;
+                const uint32_t q_k = q_addr + (k >> 2) * (kRows * 128) + koff;
                 const uint32_t acc = (part | k) ? 1u : 0u;
                 if (pass == 0) {
                   umma_f16_ss(d0, sdesc_k_sw128(q_k), sdesc_k_sw128(mu_k), idesc1, acc);
@@ -256,13 +280,15 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       // independent partial sums; masking only on the tail tile.
       {
         const int row = half * 128 + quad * 32 + lane;
+        const int64_t nk_row = pos_nk(p, t0 + row / kG);    // rows of one query share its kernel count
+        const int64_t nk_min = pos_nk(p, t0);
         float mrun = -INFINITY, srun = 0.f;
         for (int c = 0; c < tiles; ++c) {
           mbar_wait(acc_full + buf, acc_phase[buf]);
           acc_phase[buf] ^= 1;
           tc_fence_after();
           const int64_t jbase = (int64_t)c * kNT;
-          const bool tail = jbase + kNT > nk;
+          const bool tail = jbase + kNT > nk_min;
 #pragma unroll 1
           for (int ch = 0; ch < 4; ch += 2) {
             float v[64];
@@ -273,7 +299,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             if (tail) {
               const int64_t j0 = jbase + ch * 32;
 #pragma unroll
-              for (int x = 0; x < 64; ++x) v[x] = (j0 + x < nk) ? v[x] : -INFINITY;
+              for (int x = 0; x < 64; ++x) v[x] = (j0 + x < nk_row) ? v[x] : -INFINITY;
             }
             float m4[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
@@ -305,24 +331,27 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         acc_phase[buf] ^= 1;
         tc_fence_after();
         const int jl = quad * 32 + lane;
-        const bool live = (int64_t)c * kNT + jl < nk;
+        const int64_t jg = (int64_t)c * kNT + jl;               // this thread's kernel
+        constexpr int kQC = 64 / kG;                             // queries per 64-column chunk
+        constexpr int kQH = 128 / kG;                            // queries per column half
 #pragma unroll 1
-        for (int qq = 0; qq < 8; qq += 4) {
+        for (int qq = 0; qq < kQH; qq += kQC) {
           float v[64];
-          const uint32_t col = tmem + lane_base + buf * 256 + (half * 8 + qq) * 16;
+          const uint32_t col = tmem + lane_base + buf * 256 + (half * kQH + qq) * kG;
           tmem_ld32(col, *reinterpret_cast<float(*)[32]>(v));
           tmem_ld32(col + 32, *reinterpret_cast<float(*)[32]>(v + 32));
           tmem_wait_ld();
 #pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            const int qi = half * 8 + qq + u4;
+          for (int u4 = 0; u4 < kQC; ++u4) {
+            const int qi = half * kQH + qq + u4;
             const float* l2 = lse2 + qi * kG;
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll
             for (int h = 0; h < kG; h += 2) {
-              a0 += ex2(fmaf(v[u4 * 16 + h], p.zscale, -l2[h]));
-              a1 += ex2(fmaf(v[u4 * 16 + h + 1], p.zscale, -l2[h + 1]));
+              a0 += ex2(fmaf(v[u4 * kG + h], p.zscale, -l2[h]));
+              a1 += ex2(fmaf(v[u4 * kG + h + 1], p.zscale, -l2[h + 1]));
             }
+            const bool live = jg < pos_nk(p, t0 + qi);
             stile[qi * kSTileLd + 1 + jl] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
           }
         }
@@ -437,20 +466,70 @@ bool tc_kernels_enabled() {
   return on;
 }
 
+static bool tc_select_shape(const CallShape& cs, int* kq) {
+  if (cs.group == 16 && cs.d == 128) { *kq = 16; return true; }
+  if (cs.group == 8 && cs.d == 64) { *kq = 32; return true; }
+  return false;
+}
+
 bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool have_split_means) {
   if (!have_split_means || !tc_kernels_enabled()) return false;
-  if (cs.group != kG || cs.d != kD) return false;
+  int kq;
+  if (!tc_select_shape(cs, &kq)) return false;
   if (g.kernel_stride != 16 || g.kernel_size != 32) return false;
-  if (g.block_size % 16 != 0 || kNT % (g.block_size / 16) != 0) return false;
+  // every query of a unit (kq consecutive positions) must share the candidate blocks
+  if (g.block_size % kq != 0 || kNT % (g.block_size / 16) != 0) return false;
   if (g.top_k + g.n_init_blocks + g.n_local_blocks > 80) return false;
   if (cs.nk_total < 1) return false;
   return true;
 }
 
 size_t tc_select_workspace(const infllm2_geometry& g, const CallShape& cs, int) {
-  if (cs.group != kG || cs.d != kD) return 0;
+  int kq;
+  if (!tc_select_shape(cs, &kq)) return 0;
   const int64_t nb_cap = cs.cache_len / g.block_size + 2;
-  return (size_t)kNumSMs * 2 * kQ * nb_cap * sizeof(float);
+  return (size_t)kNumSMs * 2 * kq * nb_cap * sizeof(float);
+}
+
+template <int G, int D>
+static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64_t q_row_stride, const void* means_hi,
+                                       const void* means_lo, int64_t means_cap, Params& p, void* ws, size_t ws_bytes,
+                                       cudaStream_t stream) {
+  using C = SelCfg<G, D>;
+  constexpr int kQ = C::kQ;
+  p.kq = kQ;
+  p.first_t0 = cs.start / kQ * kQ;
+  const int64_t last = cs.start + cs.n - 1;
+  p.units_per_group = (last - p.first_t0) / kQ + 1;
+  p.n_units = p.units_per_group * cs.hkv;
+  p.zscale = 1.4426950408889634f / sqrtf((float)D);
+  const int grid = tc_grid(p.n_units);
+  if ((size_t)grid * 2 * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
+  p.rbuf = static_cast<float*>(ws);
+  CUtensorMap tq, thi, tlo;
+  {
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.hq, (uint64_t)cs.n};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};
+    const uint32_t box[3] = {64, (uint32_t)G, (uint32_t)kQ};
+    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)means_cap, (uint64_t)cs.hkv};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)means_cap * D * 2};
+    const uint32_t box[3] = {64, (uint32_t)kNT, 1};
+    if (!encode_tmap_3d_bf16(&thi, means_hi, dims, strides, box)) return cudaErrorInvalidValue;
+    if (!encode_tmap_3d_bf16(&tlo, means_lo, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  const size_t smem = C::Smem::total + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<G, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  count_launch();
+  select_tc_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, thi, tlo, p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
@@ -470,42 +549,12 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.n_init = g.n_init_blocks;
   p.n_local = g.n_local_blocks;
   p.consume = g.forced_consume_budget;
-  p.first_t0 = cs.start / kQ * kQ;
-  const int64_t last = cs.start + cs.n - 1;
-  p.units_per_group = (last - p.first_t0) / kQ + 1;
-  p.n_units = p.units_per_group * cs.hkv;
   p.selection = selection;
   p.sel_scores = sel_scores;
   p.nb_cap = cs.cache_len / g.block_size + 2;
-  p.zscale = 1.4426950408889634f / sqrtf((float)kD);
-  const int grid = tc_grid(p.n_units);
-  if ((size_t)grid * 2 * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
-  p.rbuf = static_cast<float*>(ws);
-
-  CUtensorMap tq, thi, tlo;
-  {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)cs.n};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)q_row_stride * 2};
-    const uint32_t box[3] = {64, (uint32_t)kG, (uint32_t)kQ};
-    if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
-  }
-  {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)means_cap, (uint64_t)cs.hkv};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)means_cap * kD * 2};
-    const uint32_t box[3] = {64, (uint32_t)kNT, 1};
-    if (!encode_tmap_3d_bf16(&thi, means_hi, dims, strides, box)) return cudaErrorInvalidValue;
-    if (!encode_tmap_3d_bf16(&tlo, means_lo, dims, strides, box)) return cudaErrorInvalidValue;
-  }
-  const size_t smem = SmemLayout::total + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  count_launch();
-  select_tc_kernel<<<grid, kThreads, smem, stream>>>(tq, thi, tlo, p);
-  return cudaGetLastError();
+  if (cs.group == 8 && cs.d == 64)
+    return launch_select_shape<8, 64>(cs, q, q_row_stride, means_hi, means_lo, means_cap, p, ws, ws_bytes, stream);
+  return launch_select_shape<16, 128>(cs, q, q_row_stride, means_hi, means_lo, means_cap, p, ws, ws_bytes, stream);
 }
 
 }  // namespace infllm2

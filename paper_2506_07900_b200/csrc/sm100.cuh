@@ -118,6 +118,35 @@ __device__ __forceinline__ float warp_reduce8(float (&v)[8], int lane, Op op) {
   return op(r, __shfl_xor_sync(0xffffffffu, r, 1));
 }
 
+// N-value versions (N in {4, 8, 16}): lane l ends with the warp-wide reduction
+// of head reduce_head_n<N>(l); lanes sharing bits 4..(5-log2 N) agree.
+template <int N>
+__device__ __forceinline__ int reduce_head_n(int lane) {
+  int h = 0;
+#pragma unroll
+  for (int b = 0, w = N; w > 1; ++b, w >>= 1) h = 2 * h + ((lane >> (4 - b)) & 1);
+  return h;
+}
+template <int N>
+__device__ __forceinline__ bool reduce_writer_n(int lane) { return (lane & (32 / N - 1)) == 0; }
+template <int N, typename Op>
+__device__ __forceinline__ float warp_reduce_n(float (&v)[N], int lane, Op op) {
+#pragma unroll
+  for (int w = N / 2, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (int off = 16 / N; off >= 1; off >>= 1) r = op(r, __shfl_xor_sync(0xffffffffu, r, off));
+  return r;
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -186,6 +215,17 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float (&v)[4]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]));
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
   asm volatile(
@@ -193,6 +233,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float (&v)[N]) {
+  if constexpr (N == 4) tmem_ld4(taddr, v);
+  else if constexpr (N == 8) tmem_ld8(taddr, v);
+  else tmem_ld16(taddr, v);
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_n(uint32_t taddr, const float (&v)[N]) {
+  if constexpr (N == 4) tmem_st4(taddr, v);
+  else if constexpr (N == 8) tmem_st8(taddr, v);
+  else tmem_st16(taddr, v);
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // Make this thread's generic-proxy shared-memory writes visible to the async

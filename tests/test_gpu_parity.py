@@ -140,13 +140,16 @@ def test_touch_stats_and_traces_match_reference_counts():
     np.testing.assert_allclose(t["scores_topk"], z["scores_topk"][1500, 1, :len(t["selected"])], rtol=1e-5)
 
 
+@pytest.mark.parametrize("shape", [(32, 2, 128), (16, 2, 64)], ids=["8B", "0.5B"])
 @pytest.mark.parametrize("length,topk", [(8192, 16), (6000, 64), (4096, 8), (5000, 32)])
-def test_random_vs_oracle_sampled_rows(length, topk):
-    """Larger caches than the fixtures: GPU vs oracle (f64 dots) on sampled rows."""
+def test_random_vs_oracle_sampled_rows(length, topk, shape):
+    """Larger caches than the fixtures: GPU vs oracle (f64 dots) on sampled rows,
+    for the MiniCPM4-8B attention shape and the 0.5B one (G = 8, D = 64)."""
+    hq, hkv, d = shape
     geom = O.Geometry(top_k=topk)
     cfg = P.SparseAttentionConfig(top_k=topk)
-    q, k, v = make_qkv(1234 + length, length, length, 32, 2, 128)
-    layer = P.BlockizedLayerCache(2, 128, cfg, capacity=length)
+    q, k, v = make_qkv(1234 + length, length, length, hq, hkv, d)
+    layer = P.BlockizedLayerCache(hkv, d, cfg, capacity=length)
     layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     o, s, l = P.two_stage_attention(torch.from_numpy(q).cuda(), layer, cfg, 0, return_selection=True,
                                     return_lse=True, out_dtype=torch.float32)
@@ -249,3 +252,22 @@ def test_numpy_compat_adapter_matches_reference(name):
     for t in traces:
         j = pos_of[t["query_pos"] - meta["start"]]
         assert t["selected"] == [int(b) for b in z["selection"][j, t["group"]] if b >= 0]
+
+
+def test_small_model_shape_chunks_and_verifier():
+    """MiniCPM4-0.5B attention geometry (G = 8, D = 64) on the tensor-core path:
+    a chunk starting off the 32-position unit grid equals the same rows of the
+    whole prefill (selections bitwise, F12), and the tensor-core selections equal
+    the float64 verifier's."""
+    cfg = P.SparseAttentionConfig(top_k=16)
+    q, k, v = make_qkv(505, 3000, 3000, 16, 2, 64)
+    layer = P.BlockizedLayerCache(2, 64, cfg, capacity=3000)
+    layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd = torch.from_numpy(q).cuda()
+    o, s = P.two_stage_attention(qd, layer, cfg, 0, return_selection=True, out_dtype=torch.float32)
+    o2, s2 = P.two_stage_attention(qd[1001:1778], layer, cfg, 1001, return_selection=True, out_dtype=torch.float32)
+    assert torch.equal(s[1001:1778], s2)
+    assert (o[1001:1778] - o2).abs().max().item() < 1e-6
+    o3, s3 = P.two_stage_attention(qd, layer, cfg, 0, return_selection=True, out_dtype=torch.float32, exact=True)
+    assert torch.equal(s, s3)
+    assert bool(((o - o3).abs() <= 2e-3 + 2e-2 * o3.abs()).all())     # bf16 softmax weights (DESIGN §4 K3p)
