@@ -358,7 +358,7 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
                         start_position: int, *, stats: Optional[TouchStats] = None,
                         traces: Optional[list] = None, return_selection: bool = False,
                         return_lse: bool = False, out_dtype: Optional[torch.dtype] = None,
-                        exact: bool = False, split_p: bool = False):
+                        exact: bool = False, split_p: bool = False, check_finite: bool = False):
     """Block-sparse attention for ``q`` of shape (n, n_q_heads, head_dim).
 
     Same semantics as the reference (sparse.py:387-468): row i sits at
@@ -368,6 +368,9 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     int32 selection (n, HKV, max_selected; ascending, -1 padded) and/or the
     float32 LSE (n, HQ) when requested.  ``exact=True`` forces the float64
     CUDA-core scorer (the verifier) instead of the tensor-core one.
+    ``check_finite=True`` reproduces the reference's ``NumericError`` for
+    non-finite queries or kernel means (sparse.py:176-177); it costs a device
+    synchronisation, so it is opt-in.
     ``split_p=True`` makes the tensor-core stage 2 carry the softmax weights as
     bf16 hi + lo (outputs ~1e-5 of the float64 reference instead of ~1e-4, at
     ~1.3x the stage-2 cost); the default uses bf16 weights.
@@ -385,6 +388,9 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
         raise ValidationError(f"query position {start + n - 1} beyond cache length {layer.length}")
     dev = layer.device
     out_dtype = out_dtype or (q.dtype if q.dtype in (torch.float32, torch.bfloat16) else torch.bfloat16)
+    if check_finite and n:
+        if not (bool(torch.isfinite(q).all()) and bool(torch.isfinite(layer.fine_means).all())):
+            raise NumericError("non-finite values in kernel scoring")
     qb = q.to(device=dev, dtype=torch.bfloat16)
     if qb.stride(2) != 1 or qb.stride(1) != d:
         qb = qb.contiguous()

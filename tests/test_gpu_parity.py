@@ -271,3 +271,16 @@ def test_small_model_shape_chunks_and_verifier():
     o3, s3 = P.two_stage_attention(qd, layer, cfg, 0, return_selection=True, out_dtype=torch.float32, exact=True)
     assert torch.equal(s, s3)
     assert bool(((o - o3).abs() <= 2e-3 + 2e-2 * o3.abs()).all())     # bf16 softmax weights (DESIGN §4 K3p)
+
+
+def test_check_finite_raises_numeric_error():
+    """check_finite=True mirrors the reference's NumericError (sparse.py:176-177)."""
+    cfg = P.SparseAttentionConfig(top_k=8)
+    q, k, v = make_qkv(9, 512, 4, 32, 2, 128)
+    layer = P.BlockizedLayerCache(2, 128, cfg)
+    layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd = torch.from_numpy(q).cuda()
+    P.two_stage_attention(qd, layer, cfg, 508, check_finite=True)      # finite: fine
+    qd[1, 3, 7] = float("nan")
+    with pytest.raises(P.NumericError):
+        P.two_stage_attention(qd, layer, cfg, 508, check_finite=True)
