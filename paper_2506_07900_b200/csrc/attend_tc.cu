@@ -41,7 +41,7 @@ constexpr int kD = 128;
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
 constexpr int kStages = 3;
-constexpr int kThreads = 480;          // 0 TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue
+constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
 constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to 4 tiles ahead of softmax)
 constexpr uint32_t kColO = kSlots * 16;  // O^T columns [kColO, kColO + 32)
 constexpr int kMaxSel = 80;
@@ -77,7 +77,7 @@ struct AttCfg {
     static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
     static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
     static constexpr uint32_t bars = red + 8 * 16 * 4;
-    static constexpr uint32_t total = bars + 48 * 8;
+    static constexpr uint32_t total = bars + 64 * 8;
   };
 };
 
@@ -207,8 +207,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
-  uint64_t* kv_full = bars + 38;          // [kStages <= 6]
-  uint64_t* kv_empty = bars + 44;         // [kStages <= 6]
+  // K and V have separate rings: a K stage frees as soon as its QK is done, so
+  // QK runs ahead of the softmax / PV chain instead of waiting for PV to free
+  // a shared K+V stage
+  uint64_t* k_full = bars + 38;           // [kStages <= 6]
+  uint64_t* k_empty = bars + 44;
+  uint64_t* v_full = bars + 50;
+  uint64_t* v_empty = bars + 56;
   uint64_t* q_full = bars + 6;            // [2]
   uint64_t* q_empty = bars + 8;           // [2]
   uint64_t* s_full = bars + 28;           // [kSlots]
@@ -225,7 +230,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -251,8 +261,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   pdl_wait();                             // no-op unless launched as a dependent
   const int64_t items = p.n * p.hkv * p.parts;   // work units (item, part)
 
-  if (warp == 0) {
-    // -------------------------------------------------------------- producer
+  if (warp == 0 || warp == 15) {
+    // -------------------------------------------------------------- producers
+    // warp 0: Q + K tiles into the K ring; warp 15: V tiles into the V ring
+    const bool is_k = warp == 0;
+    uint64_t* ring_full = is_k ? k_full : v_full;
+    uint64_t* ring_empty = is_k ? k_empty : v_empty;
+    uint8_t* ring = smem + Smem::kv + (is_k ? 0 : kStages * kTileBytes);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -265,6 +280,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int64_t pos = item_pos(p, i);
       const CUtensorMap* mk = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i : &tm_k;
       const CUtensorMap* mv = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i + 1 : &tm_v;
+      const CUtensorMap* mm = is_k ? mk : mv;
       const SelRow sr = pf.take(p, w, items, pos, lane);
       const int nb = sr.nb;
       int c0, c1;
@@ -273,7 +289,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int qb = it & 1;
       const uint32_t q_par = ((it >> 1) & 1) ^ 1;
       ++it;
-      if (lane == 0) {
+      if (is_k && lane == 0) {
         mbar_wait(q_empty + qb, q_par);
         mbar_arrive_expect_tx(q_full + qb, kQBytes);
         uint8_t* qd = smem + Smem::q + qb * kQBytes;
@@ -285,18 +301,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int b0 = sr.get(2 * c);
         const int b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         if (lane == 0) {
-          mbar_wait(kv_empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(kv_full + stage, nt * 2 * C::kDH * (kM * 128));
-          uint8_t* kd = smem + Smem::kv + stage * kStageBytes;
-          uint8_t* vd = kd + kTileBytes;
+          mbar_wait(ring_empty + stage, phase ^ 1);
+          mbar_arrive_expect_tx(ring_full + stage, nt * C::kDH * (kM * 128));
+          uint8_t* dst = ring + stage * kTileBytes;
           for (int x = 0; x < nt; ++x) {
             const int row0 = (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
 #pragma unroll
-            for (int hh = 0; hh < C::kDH; ++hh) {
-              tma_load_3d(kd + hh * kHalfBytes + off, mk, kv_full + stage, 64 * hh, row0, grp);
-              tma_load_3d(vd + hh * kHalfBytes + off, mv, kv_full + stage, 64 * hh, row0, grp);
-            }
+            for (int hh = 0; hh < C::kDH; ++hh)
+              tma_load_3d(dst + hh * kHalfBytes + off, mm, ring_full + stage, 64 * hh, row0, grp);
           }
         }
         __syncwarp();
@@ -331,17 +344,18 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const uint64_t dq = sdesc_k_sw128(smem_u32(smem + Smem::q + qb * kQBytes));
       for (int c = c0; c < c1; ++c, ++tcount) {
         const int slot = tcount % kSlots;
-        mbar_wait(kv_full + stage, phase);
+        mbar_wait(k_full + stage, phase);
         mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t dk = sdesc_k_sw128(smem_u32(smem + Smem::kv + stage * kStageBytes));
+          const uint64_t dk = sdesc_k_sw128(smem_u32(smem + Smem::kv + stage * kTileBytes));
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
             const uint32_t qoff = (k >> 2) * (kG * 128) + (k & 3) * 32;
             umma_f16_ss(tmem + slot * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk, k > 0 ? 1u : 0u);
           }
+          umma_commit(k_empty + stage);                // K tile consumed: its stage may refill
           umma_commit(s_full + slot);
           if (c == c1 - 1) umma_commit(q_empty + qb);
         }
@@ -354,6 +368,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     // -------------------------------------------------------------- PV issuer
     const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
     int stage = 0;
+    uint32_t vphase = 0;
     uint32_t pcount = 0;
     int it = 0;
     SelPrefetch pf;
@@ -371,12 +386,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int ob = it & 1;
       for (int c = c0; c < c1; ++c, ++pcount) {
         const int pbuf = pcount & 1;
+        mbar_wait(v_full + stage, vphase);
         mbar_wait(p_full + pbuf, (pcount >> 1) & 1);
         if (c == c0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
         if (elect_one()) {
-          const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + stage * kStageBytes + kTileBytes),
+          const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + (kStages + stage) * kTileBytes),
                                              kHalfBytes, 1024);
           // P^T (K = rows, N = heads, no swizzle): 8-row K groups of 16*G bytes, 8-head groups 128 B apart
           const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 16 * kG, 128);
@@ -390,12 +406,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
                 umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + ((kPHalf + k * 32 * kG) >> 4), idesc_pv, 1u);
             }
           }
-          umma_commit(kv_empty + stage);
+          umma_commit(v_empty + stage);
           umma_commit(p_empty + pbuf);
           if (c == c1 - 1) umma_commit(o_full + ob);
         }
         __syncwarp();
-        if (++stage == kStages) stage = 0;
+        if (++stage == kStages) { stage = 0; vphase ^= 1; }
       }
       ++it;
     }

@@ -17,7 +17,7 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
-__global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, long long* out, int ts) {
+__global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, long long* out, int ts, int nowait) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(128, 1) bench(int n, int group, int iters, lon
         else umma_f16_ss(tmem, da + ((k & 3) * 32 >> 4), db + ((k & 3) * 32 >> 4), idesc, k > 0 ? 1u : 0u);
       }
       umma_commit(&bar);
-      mbar_wait(&bar, ph);
+      if (!nowait || it == iters - 1) {
+        mbar_wait(&bar, ph);
+      }
       ph ^= 1;
     }
     t1 = clock64();
@@ -59,18 +61,19 @@ int main(int argc, char** argv) {
   const int group = argc > 2 ? atoi(argv[2]) : 8;
   const int iters = argc > 3 ? atoi(argv[3]) : 2000;
   const int ts = argc > 4 ? atoi(argv[4]) : 0;
+  const int nowait = argc > 5 ? atoi(argv[5]) : 0;
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  bench<<<148, 128, 66 * 1024>>>(n, group, 10, d, ts);
-  bench<<<148, 128, 66 * 1024>>>(n, group, iters, d, ts);
+  bench<<<148, 128, 66 * 1024>>>(n, group, 10, d, ts, nowait);
+  bench<<<148, 128, 66 * 1024>>>(n, group, iters, d, ts, nowait);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += h[i];
   avg /= 148;
-  printf("%s N=%3d group=%2d: %.1f cycles per MMA (%.1f per group incl. commit+wait) %s\n", ts ? "TS" : "SS", n, group,
+  printf("%s%s N=%3d group=%2d: %.1f cycles per MMA (%.1f per group incl. commit+wait) %s\n", ts ? "TS" : "SS", nowait ? " nowait" : "", n, group,
          avg / (iters * (double)group), avg / iters, cudaGetErrorString(e));
   return 0;
 }
