@@ -41,6 +41,9 @@ constexpr int kD = 128;
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
 constexpr int kStages = 3;
+#ifndef ATT_KSTAGES
+#define ATT_KSTAGES 3
+#endif
 constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
 constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to 4 tiles ahead of softmax)
 constexpr uint32_t kColO = kSlots * 16;  // O^T columns [kColO, kColO + 32)
@@ -61,7 +64,10 @@ struct AttCfg {
   static constexpr int kDH = D / 64;                              // 64-d halves per row
   static constexpr uint32_t kTileBytes = kDH * kHalfBytes;        // K or V tile
   static constexpr uint32_t kStageBytes = 2 * kTileBytes;
-  static constexpr int kStages = 3 * (128 / D);
+  static constexpr int kStages = 3 * (128 / D);                   // K + V stage pairs of smem
+  static constexpr int kKStages = ATT_KSTAGES * (128 / D);        // K ring depth
+  static constexpr int kVStages = 2 * kStages - kKStages;         // V ring depth
+  static_assert(kKStages <= 8 && kVStages <= 8 && kKStages >= 1 && kVStages >= 1, "ring depths");
   static constexpr uint32_t kQBytes = kDH * G * 128;
   static constexpr uint32_t kPHalf = kRowsT * G * 2;
   static constexpr uint32_t kPBytes = 2 * kPHalf;
@@ -72,12 +78,12 @@ struct AttCfg {
     static constexpr uint32_t kv = 0;
     // D = 64: PV runs M = 128 over a half-width V tile, so the last stage's V
     // operand spans kHalfBytes past the ring: pad, never read back
-    static constexpr uint32_t q = kv + kStages * kStageBytes + (kDH == 1 ? kHalfBytes : 0);   // 2 buffers
+    static constexpr uint32_t q = kv + (kKStages + kVStages) * kTileBytes + (kDH == 1 ? kHalfBytes : 0);   // 2 buffers
     static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
     static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
     static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
     static constexpr uint32_t bars = red + 8 * 16 * 4;
-    static constexpr uint32_t total = bars + 64 * 8;
+    static constexpr uint32_t total = bars + 72 * 8;
   };
 };
 
@@ -210,10 +216,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   // K and V have separate rings: a K stage frees as soon as its QK is done, so
   // QK runs ahead of the softmax / PV chain instead of waiting for PV to free
   // a shared K+V stage
-  uint64_t* k_full = bars + 38;           // [kStages <= 6]
-  uint64_t* k_empty = bars + 44;
-  uint64_t* v_full = bars + 50;
-  uint64_t* v_empty = bars + 56;
+  uint64_t* k_full = bars + 38;           // [kKStages <= 8]
+  uint64_t* k_empty = bars + 46;
+  uint64_t* v_full = bars + 54;           // [kVStages <= 8]
+  uint64_t* v_empty = bars + 62;
   uint64_t* q_full = bars + 6;            // [2]
   uint64_t* q_empty = bars + 8;           // [2]
   uint64_t* s_full = bars + 28;           // [kSlots]
@@ -230,12 +236,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(k_full + i, 1);
-      mbar_init(k_empty + i, 1);
-      mbar_init(v_full + i, 1);
-      mbar_init(v_empty + i, 1);
-    }
+    for (int i = 0; i < C::kKStages; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
+    for (int i = 0; i < C::kVStages; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -267,7 +269,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     const bool is_k = warp == 0;
     uint64_t* ring_full = is_k ? k_full : v_full;
     uint64_t* ring_empty = is_k ? k_empty : v_empty;
-    uint8_t* ring = smem + Smem::kv + (is_k ? 0 : kStages * kTileBytes);
+    uint8_t* ring = smem + Smem::kv + (is_k ? 0 : C::kKStages * kTileBytes);
+    const int nstages = is_k ? C::kKStages : C::kVStages;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -313,7 +316,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           }
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++stage == nstages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -360,7 +363,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           if (c == c1 - 1) umma_commit(q_empty + qb);
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++stage == C::kKStages) { stage = 0; phase ^= 1; }
       }
       ++it;
     }
@@ -392,7 +395,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         tc_fence_after();
         const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
         if (elect_one()) {
-          const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + (kStages + stage) * kTileBytes),
+          const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + (C::kKStages + stage) * kTileBytes),
                                              kHalfBytes, 1024);
           // P^T (K = rows, N = heads, no swizzle): 8-row K groups of 16*G bytes, 8-head groups 128 B apart
           const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 16 * kG, 128);
@@ -411,7 +414,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           if (c == c1 - 1) umma_commit(o_full + ob);
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; vphase ^= 1; }
+        if (++stage == C::kVStages) { stage = 0; vphase ^= 1; }
       }
       ++it;
     }
