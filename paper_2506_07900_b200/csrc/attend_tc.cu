@@ -45,7 +45,7 @@ constexpr int kStages = 3;
 #define ATT_KSTAGES 3
 #endif
 constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
-constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to 4 tiles ahead of softmax)
+constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to kSlots tiles ahead of softmax)
 constexpr uint32_t kColO = kSlots * 16;  // O^T columns [kColO, kColO + 32)
 constexpr int kMaxSel = 80;
 
@@ -83,7 +83,7 @@ struct AttCfg {
     static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
     static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
     static constexpr uint32_t bars = red + 8 * 16 * 4;
-    static constexpr uint32_t total = bars + 72 * 8;
+    static constexpr uint32_t total = bars + 88 * 8;
   };
 };
 
@@ -222,8 +222,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   uint64_t* v_empty = bars + 62;
   uint64_t* q_full = bars + 6;            // [2]
   uint64_t* q_empty = bars + 8;           // [2]
-  uint64_t* s_full = bars + 28;           // [kSlots]
-  uint64_t* s_empty = bars + 32;          // [kSlots]
+  uint64_t* s_full = bars + 70;           // [kSlots <= 8]
+  uint64_t* s_empty = bars + 78;          // [kSlots <= 8]
   uint64_t* p_full = bars + 14;           // [2]
   uint64_t* p_empty = bars + 16;          // [2]
   uint64_t* o_full = bars + 18;           // [2]
