@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .errors import ValidationError
-from .sparse import BlockizedLayerCache, SparseAttentionConfig, _ptr, _stream
+from .sparse import BlockizedLayerCache, SparseAttentionConfig, _ptr, _stream, two_stage_attention
 
 
 class DecodeBatch:
@@ -64,6 +64,34 @@ class DecodeBatch:
                                                         _stream(self.device)), "decode table")
         self._sig = sig
 
+    def _fused_ok(self, hq: int, hkv: int, d: int) -> bool:
+        """The batched decode kernels cover G = 16, D = 128 (MiniCPM4-8B); other
+        head geometries step each sequence through the prefill kernels."""
+        return hkv > 0 and hq // hkv == 16 and hq % hkv == 0 and d == 128
+
+    def _step_per_sequence(self, q, k_new, v_new, return_selection, return_lse, out_dtype, bookkeep):
+        """One decode step per sequence with the (n = 1) prefill kernels — same
+        semantics (append, then attend the new row, model.py:434-444)."""
+        if not bookkeep:
+            raise ValidationError("graph replay (bookkeep=False) needs the batched decode kernels (G = 16, D = 128)")
+        outs, sels, lses = [], [], []
+        for i, layer in enumerate(self.layers):
+            layer.append(k_new[i:i + 1], v_new[i:i + 1])
+            res = two_stage_attention(q[i:i + 1], layer, self.config, layer.length - 1, return_selection=True,
+                                      return_lse=True, out_dtype=out_dtype)
+            outs.append(res[0])
+            sels.append(res[1])
+            lses.append(res[2])
+        out = torch.cat(outs)
+        if return_selection or return_lse:
+            ret = (out,)
+            if return_selection:
+                ret += (torch.cat(sels),)
+            if return_lse:
+                ret += (torch.cat(lses),)
+            return ret
+        return out
+
     def reserve(self, extra_tokens: int) -> None:
         """Preallocate room for `extra_tokens` more decode steps (no reallocation,
         hence no table rebuild, while they run — required for graph capture)."""
@@ -97,6 +125,8 @@ class DecodeBatch:
             raise ValidationError("decode step shapes must be q (S, HQ, D), k/v (S, HKV, D)")
         if hq % l0.n_kv_heads:
             raise ValidationError("query heads not divisible by KV heads")
+        if not self._fused_ok(hq, l0.n_kv_heads, l0.head_dim):
+            return self._step_per_sequence(q, k_new, v_new, return_selection, return_lse, out_dtype, bookkeep)
         self._ensure()
         dev = self.device
         qb = q.to(device=dev, dtype=torch.bfloat16).contiguous()

@@ -127,3 +127,30 @@ def test_fused_decode_matches_five_launch_path(lengths, monkeypatch):
         assert torch.equal(a.values.contiguous(), b.values.contiguous())
         assert digest(_means(a.fine_means)) == digest(_means(b.fine_means))
         assert digest(_means(a.coarse_means)) == digest(_means(b.coarse_means))
+
+
+def test_decode_batch_small_model_shape():
+    """MiniCPM4-0.5B geometry (G = 8, D = 64): DecodeBatch steps each sequence
+    through the prefill kernels; equals an independently built cache."""
+    cfg = P.SparseAttentionConfig(top_k=16)
+    lengths = [1500, 3001]
+    full = [make_qkv(91 + i, L + 3, 3, 16, 2, 64) for i, L in enumerate(lengths)]
+    layers = []
+    for (q, k, v), L in zip(full, lengths):
+        layer = P.BlockizedLayerCache(2, 64, cfg)
+        layer.append(torch.from_numpy(k[:L]).cuda(), torch.from_numpy(v[:L]).cuda())
+        layers.append(layer)
+    batch = P.DecodeBatch(layers, cfg)
+    for st in range(3):
+        qs = torch.stack([torch.from_numpy(f[0][st]) for f in full]).cuda()
+        ks = torch.stack([torch.from_numpy(f[1][L + st]) for f, L in zip(full, lengths)]).cuda()
+        vs = torch.stack([torch.from_numpy(f[2][L + st]) for f, L in zip(full, lengths)]).cuda()
+        out, sel = batch.step(qs, ks, vs, return_selection=True, out_dtype=torch.float32)
+        for i, ((q, k, v), L) in enumerate(zip(full, lengths)):
+            n_now = L + st + 1
+            ref = P.BlockizedLayerCache(2, 64, cfg)
+            ref.append(torch.from_numpy(k[:n_now]).cuda(), torch.from_numpy(v[:n_now]).cuda())
+            o2, s2 = P.two_stage_attention(qs[i:i + 1], ref, cfg, n_now - 1, return_selection=True,
+                                           out_dtype=torch.float32)
+            assert torch.equal(sel[i], s2[0])
+            assert (out[i] - o2[0]).abs().max().item() < 1e-5
