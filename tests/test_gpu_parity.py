@@ -284,3 +284,34 @@ def test_check_finite_raises_numeric_error():
     qd[1, 3, 7] = float("nan")
     with pytest.raises(P.NumericError):
         P.two_stage_attention(qd, layer, cfg, 508, check_finite=True)
+
+
+@pytest.mark.parametrize("topk", [16, 64])
+def test_full_size_128k_tensor_core_vs_float64_verifier(topk):
+    """At BASELINE's full size (131072-token cache, 8B shape): the tensor-core
+    stage 1 + stage 2 against the float64 CUDA-core verifier (exact=True) on row
+    chunks at the start, middle and end of the sequence - selections bitwise,
+    outputs within the tensor-core bar."""
+    L = 131072
+    cfg = P.SparseAttentionConfig(top_k=topk)
+    g = torch.Generator(device="cuda").manual_seed(topk)
+    k = torch.randn((L, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((L, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
+    layer = P.BlockizedLayerCache(2, 128, cfg, capacity=L)
+    layer.append(k, v)
+    for start, n in ((0, 48), (65500, 80), (L - 96, 96)):
+        q = torch.randn((n, 32, 128), generator=g, device="cuda").to(torch.bfloat16)
+        o, s, l = P.two_stage_attention(q, layer, cfg, start, return_selection=True, return_lse=True,
+                                        out_dtype=torch.float32)
+        o2, s2, l2 = P.two_stage_attention(q, layer, cfg, start, return_selection=True, return_lse=True,
+                                           out_dtype=torch.float32, exact=True)
+        assert torch.equal(s, s2), (start, int((s != s2).any(-1).sum()))
+        # bf16 softmax weights: each weight is off by <= 2^-9 relative, so a
+        # row over few keys (row 1 attends 2) can be off by 2^-9*|v0 - v1|,
+        # ~4e-3 for N(0,1) values; long rows average it away (measured <=6e-4)
+        err = (o - o2).abs()
+        assert bool((err[:64] <= 8e-3 + 2e-2 * o2[:64].abs()).all())
+        assert bool((err[64:] <= 2e-3 + 2e-2 * o2[64:].abs()).all())
+        assert (l - l2).abs().max().item() <= 1e-4
+        o3 = P.two_stage_attention(q, layer, cfg, start, out_dtype=torch.float32, split_p=True)
+        assert (o3 - o2).abs().max().item() <= 5e-5
