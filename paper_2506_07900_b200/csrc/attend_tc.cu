@@ -46,7 +46,6 @@ constexpr int kStages = 3;
 #endif
 constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
 constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to kSlots tiles ahead of softmax)
-constexpr uint32_t kColO = kSlots * 16;  // O^T columns [kColO, kColO + 32)
 constexpr int kMaxSel = 80;
 
 constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
@@ -71,8 +70,13 @@ struct AttCfg {
   static constexpr uint32_t kQBytes = kDH * G * 128;
   static constexpr uint32_t kPHalf = kRowsT * G * 2;
   static constexpr uint32_t kPBytes = 2 * kPHalf;
-  static constexpr uint32_t kColO = kSlots * G;                   // O^T buffers at [kColO, kColO + 2G)
-  static constexpr uint32_t kTmemCols = (kSlots + 2) * G <= 64 ? 64 : 128;
+  // Every accumulator is split in two (even / odd K-steps, summed by the
+  // reader) so consecutive MMAs never write the same TMEM columns: a dependent
+  // N = 16 chain costs ~75 cycles per MMA, two interleaved ones ~50
+  // (tools/mma_bench.cu).  S^T slot s: columns [2Gs, 2Gs + 2G); O^T buffer b:
+  // [kColO + 2Gb, kColO + 2Gb + 2G).
+  static constexpr uint32_t kColO = kSlots * 2 * G;
+  static constexpr uint32_t kTmemCols = (kSlots + 2) * 2 * G <= 64 ? 64 : (kSlots + 2) * 2 * G <= 128 ? 128 : 256;
   static constexpr int kSH = G / 2;                               // heads per softmax thread
   struct Smem {
     static constexpr uint32_t kv = 0;
@@ -356,7 +360,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
             const uint32_t qoff = (k >> 2) * (kG * 128) + (k & 3) * 32;
-            umma_f16_ss(tmem + slot * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk, k > 0 ? 1u : 0u);
+            umma_f16_ss(tmem + slot * 2 * kG + (k & 1) * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk,
+                        k > 1 ? 1u : 0u);
           }
           umma_commit(k_empty + stage);                // K tile consumed: its stage may refill
           umma_commit(s_full + slot);
@@ -399,14 +404,23 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
                                              kHalfBytes, 1024);
           // P^T (K = rows, N = heads, no swizzle): 8-row K groups of 16*G bytes, 8-head groups 128 B apart
           const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 16 * kG, 128);
-          const uint32_t ocol = tmem + kColO + ob * kG;
+          const uint32_t ocol = tmem + kColO + ob * 2 * kG;
           const uint32_t acc0 = c > c0 ? 1u : 0u;
+          if (p.p_split) {      // hi -> O_a, lo -> O_b
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            if (k < ksteps) {
-              umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + (k * 32 * kG >> 4), idesc_pv, (acc0 | k) ? 1u : 0u);
-              if (p.p_split)
-                umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + ((kPHalf + k * 32 * kG) >> 4), idesc_pv, 1u);
+            for (int k = 0; k < 8; ++k) {
+              if (k < ksteps) {
+                umma_f16_ss(ocol, dv + (k * 2048 >> 4), dp + (k * 32 * kG >> 4), idesc_pv, (acc0 | k) ? 1u : 0u);
+                umma_f16_ss(ocol + kG, dv + (k * 2048 >> 4), dp + ((kPHalf + k * 32 * kG) >> 4), idesc_pv,
+                            (acc0 | k) ? 1u : 0u);
+              }
+            }
+          } else {              // even K-steps -> O_a, odd -> O_b
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (k < ksteps)
+                umma_f16_ss(ocol + (k & 1) * kG, dv + (k * 2048 >> 4), dp + (k * 32 * kG >> 4), idesc_pv,
+                            (acc0 | (k >> 1)) ? 1u : 0u);
             }
           }
           umma_commit(v_empty + stage);
@@ -454,9 +468,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         mbar_wait(s_full + sslot, (tcount / kSlots) & 1);
         ++tcount;
         tc_fence_after();
-        float z[kSH];
-        tmem_ld_n<kSH>(tmem + lane_base + sslot * kG + h0, z);
+        float z[kSH], z2[kSH];
+        tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + h0, z);
+        tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + kG + h0, z2);
         tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < kSH; ++h) z[h] += z2[h];
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + sslot);
@@ -510,12 +527,14 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             // PV(c-1), whose completion is the next phase of p_empty[its buffer]
             mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
             tc_fence_after();
-            float o[kSH];
-            tmem_ld_n<kSH>(tmem + lane_base + kColO + ob * kG + h0, o);
+            float o[kSH], o2[kSH];
+            tmem_ld_n<kSH>(tmem + lane_base + kColO + ob * 2 * kG + h0, o);
+            tmem_ld_n<kSH>(tmem + lane_base + kColO + ob * 2 * kG + kG + h0, o2);
             tmem_wait_ld();
 #pragma unroll
-            for (int h = 0; h < kSH; ++h) o[h] *= corr[h];
-            tmem_st_n<kSH>(tmem + lane_base + kColO + ob * kG + h0, o);
+            for (int h = 0; h < kSH; ++h) { o[h] *= corr[h]; o2[h] *= corr[h]; }
+            tmem_st_n<kSH>(tmem + lane_base + kColO + ob * 2 * kG + h0, o);
+            tmem_st_n<kSH>(tmem + lane_base + kColO + ob * 2 * kG + kG + h0, o2);
             tmem_wait_st();
             tc_fence_before();
           }
@@ -605,9 +624,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(o_full + ob, par);
       mbar_wait(st_full + ob, par);
       tc_fence_after();
-      float o[kG];
-      tmem_ld_n<kG>(tmem + lane_base + kColO + ob * kG, o);
+      float o[kG], o2[kG];
+      tmem_ld_n<kG>(tmem + lane_base + kColO + ob * 2 * kG, o);
+      tmem_ld_n<kG>(tmem + lane_base + kColO + ob * 2 * kG + kG, o2);
       tmem_wait_ld();
+#pragma unroll
+      for (int h = 0; h < kG; ++h) o[h] += o2[h];
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty + ob);

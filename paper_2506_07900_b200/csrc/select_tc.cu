@@ -60,7 +60,7 @@ using topk::warp_select;
 constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
 constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 128 B)
 constexpr uint32_t kMuStageBytes = 4 * kMuHalfBytes;       // hi h0,h1, lo h0,h1 = 64 KB
-constexpr int kSTileLd = kNT + 4;                          // [carry | 128 kernels] + pad
+constexpr int kSTileLd = kNT + 4;                          // pass-2 carry scratch (>= 3*2*4*16 floats)
 
 // Per-geometry constants: G heads per KV group, head dim D; a unit is always
 // 256 (query, head) rows, i.e. kQ = 256 / G query positions (16 for the 8B
@@ -74,7 +74,7 @@ struct SelCfg {
   struct Smem {
     static constexpr uint32_t q = 0;
     static constexpr uint32_t mu = q + kQBytes;
-    static constexpr uint32_t stile = mu + kStages * kMuStageBytes;   // float [kQ][kSTileLd]
+    static constexpr uint32_t stile = mu + kStages * kMuStageBytes;   // float [3][2][4][kQH] carries
     static constexpr uint32_t lse2 = stile + kQ * kSTileLd * 4;       // float [kRows]
     static constexpr uint32_t bars = lse2 + kRows * 4;                // uint64 [..]
     static constexpr uint32_t topk = bars + 24 * 8;                   // per top-k warp lists
@@ -207,7 +207,6 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc1 = idesc_bf16_f32(128, 128);
-    const uint32_t idesc2 = idesc_bf16_f32(128, 256);
     const uint32_t q_addr = smem_u32(sq);
     const uint32_t mu_addr = smem_u32(smu);
     int stage = 0, buf = 0;
@@ -241,7 +240,12 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
                   umma_f16_ss(d0, sdesc_k_sw128(q_k), sdesc_k_sw128(mu_k), idesc1, acc);
                   umma_f16_ss(d0 + 128, sdesc_k_sw128(q_k + 128 * 128), sdesc_k_sw128(mu_k), idesc1, acc);
                 } else {
-                  umma_f16_ss(d0, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc2, acc);
+                  // N = 256 split into two independent N = 128 accumulators
+                  // (columns 0-127 / 128-255), issued alternately: a dependent
+                  // N = 256 chain costs ~190 cycles per MMA, two interleaved
+                  // N = 128 chains ~75 each (tools/mma_bench.cu)
+                  umma_f16_ss(d0, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc1, acc);
+                  umma_f16_ss(d0 + 128, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k + 128 * 128), idesc1, acc);
                 }
               }
             }
@@ -323,17 +327,32 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       named_bar_sync(1, kEpiThreads);
 
-      // ---- pass 2: group scores per kernel, block max
+      // ---- pass 2: group scores per kernel, block max.  A thread owns one
+      // kernel (TMEM lane) and kQH queries; lanes hold consecutive kernels,
+      // so block b's kernels [b*kpb - 1, (b+1)*kpb) (sparse.py:191-215: the
+      // boundary kernel is shared with block b-1) are a shuffle-reduction
+      // over kpb lanes plus the previous lane; the kernel before a warp's
+      // lane 0 comes from the neighbouring quadrant (same tile) or the
+      // previous tile through a small double-buffered smem carry.
       mbar_wait(rb_empty + (ucount & 1), ((ucount >> 1) & 1) ^ 1);
-      if (etid < kQ) stile[etid * kSTileLd] = -INFINITY;   // carry (kernel -1)
+      constexpr int kQC = 64 / kG;                             // queries per 64-column chunk
+      constexpr int kQH = 128 / kG;                            // queries per column half
+      const int kpb = p.kpb;
+      const int jl = quad * 32 + lane;
+      const bool first = (jl % kpb) == 0;
       for (int c = 0; c < tiles; ++c) {
         mbar_wait(acc_full + buf, acc_phase[buf]);
         acc_phase[buf] ^= 1;
         tc_fence_after();
-        const int jl = quad * 32 + lane;
         const int64_t jg = (int64_t)c * kNT + jl;               // this thread's kernel
-        constexpr int kQC = 64 / kG;                             // queries per 64-column chunk
-        constexpr int kQH = 128 / kG;                            // queries per column half
+        const int64_t b = jg / kpb;
+        const bool writer = first && b < n_cand;
+        // scratch: [slot][half][quad][kQH] lane-31 scores (the kernel before the
+        // next quadrant's lane 0) and lane-0 partial block maxima; three slots so
+        // tile c + 3's writes never race tile c + 1's reads
+        const int slot = c % 3;
+        float* carry = stile + (slot * 2 + half) * 8 * kQH;
+        float* part0 = carry + 4 * kQH;
 #pragma unroll 1
         for (int qq = 0; qq < kQH; qq += kQC) {
           float v[64];
@@ -341,6 +360,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           tmem_ld32(col, *reinterpret_cast<float(*)[32]>(v));
           tmem_ld32(col + 32, *reinterpret_cast<float(*)[32]>(v + 32));
           tmem_wait_ld();
+          float sc[kQC];
 #pragma unroll
           for (int u4 = 0; u4 < kQC; ++u4) {
             const int qi = half * kQH + qq + u4;
@@ -352,30 +372,49 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
               a1 += ex2(fmaf(v[u4 * kG + h + 1], p.zscale, -l2[h + 1]));
             }
             const bool live = jg < pos_nk(p, t0 + qi);
-            stile[qi * kSTileLd + 1 + jl] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
+            sc[u4] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
+          }
+          // the chunk's kQC shuffle chains are independent: issue them together
+          float r[kQC];
+#pragma unroll
+          for (int u4 = 0; u4 < kQC; ++u4) {
+            const float up = __shfl_up_sync(0xffffffffu, sc[u4], 1);
+            r[u4] = (first && lane > 0) ? fmaxf(sc[u4], up) : sc[u4];
+          }
+          // butterfly over the kpb lanes of a block: unconditional shuffles (a
+          // loop bounded by the runtime kpb costs a WARPSYNC per step)
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            if (o >= 4 && o >= kpb) break;               // uniform; kpb <= 4 never takes it
+#pragma unroll
+            for (int u4 = 0; u4 < kQC; ++u4) {
+              const float t = __shfl_xor_sync(0xffffffffu, r[u4], o);
+              r[u4] = o < kpb ? fmaxf(r[u4], t) : r[u4];
+            }
+          }
+#pragma unroll
+          for (int u4 = 0; u4 < kQC; ++u4) {
+            const int qi = half * kQH + qq + u4;
+            st_shared_if(smem_u32(carry + quad * kQH + qq + u4), sc[u4], lane == 31);
+            st_shared_if(smem_u32(part0 + quad * kQH + qq + u4), r[u4], lane == 0);
+            st_global_if(rbuf + (int64_t)qi * p.nb_cap + b, (r[u4] == -INFINITY) ? 0.f : r[u4], writer && lane > 0);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + buf);
         buf ^= 1;
-        named_bar_sync(1, kEpiThreads);
-        // blocks whose last kernel lies in this tile
-        const int bpt = kNT / p.kpb;
-        for (int x = etid; x < kQ * bpt; x += kEpiThreads) {
-          const int qi = x / bpt;
-          const int64_t b = (int64_t)c * bpt + (x - qi * bpt);
-          if (b < n_cand) {
-            const int64_t lo = b * p.kpb - 1 < 0 ? 0 : b * p.kpb - 1;
-            const int64_t hi = (b + 1) * p.kpb;
-            float r = -INFINITY;
-            for (int64_t j = lo; j < hi; ++j) r = fmaxf(r, stile[qi * kSTileLd + 1 + (int)(j - (int64_t)c * kNT)]);
-            rbuf[(int64_t)qi * p.nb_cap + b] = (r == -INFINITY) ? 0.f : r;
-          }
+        if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+        {   // lane 0's block also holds the previous kernel: lane x finishes query x
+          const float* prev = (quad > 0) ? carry + (quad - 1) * kQH
+                                         : stile + (((slot + 2) % 3) * 2 + half) * 8 * kQH + 3 * kQH;
+          const int x = lane & (kQH - 1);
+          const int64_t b0 = ((int64_t)c * kNT + quad * 32) / kpb;
+          const float pr = (quad == 0 && c == 0) ? -INFINITY : prev[x];
+          const float r = fmaxf(part0[quad * kQH + x], pr);
+          st_global_if(rbuf + (int64_t)(half * kQH + x) * p.nb_cap + b0, (r == -INFINITY) ? 0.f : r,
+                       lane < kQH && b0 < n_cand);
         }
-        named_bar_sync(1, kEpiThreads);
-        if (etid < kQ) stile[etid * kSTileLd] = stile[etid * kSTileLd + kNT];
-        named_bar_sync(1, kEpiThreads);
       }
 
       // hand the unit's block scores to the top-k warps
@@ -478,7 +517,9 @@ bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool ha
   if (!tc_select_shape(cs, &kq)) return false;
   if (g.kernel_stride != 16 || g.kernel_size != 32) return false;
   // every query of a unit (kq consecutive positions) must share the candidate blocks
-  if (g.block_size % kq != 0 || kNT % (g.block_size / 16) != 0) return false;
+  // kernels per block (a power of two dividing the 128-kernel tile) must fit
+  // in one warp: the block max is a shuffle reduction over lanes
+  if (g.block_size % kq != 0 || kNT % (g.block_size / 16) != 0 || g.block_size / 16 > 32) return false;
   if (g.top_k + g.n_init_blocks + g.n_local_blocks > 80) return false;
   if (cs.nk_total < 1) return false;
   return true;
