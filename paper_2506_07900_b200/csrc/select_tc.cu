@@ -279,9 +279,9 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int64_t qb = t0 / p.m;
       const int64_t n_cand = qb + 1;
 
-      // ---- pass 1: row LSE (log2 domain).  Two 32-column TMEM loads per
-      // wait, max on the raw accumulator (zscale > 0), FFMA+ex2 with four
-      // independent partial sums; masking only on the tail tile.
+      // ---- pass 1: row LSE (log2 domain).  Max on the raw accumulator
+      // (zscale > 0), FFMA+ex2 with four independent partial sums; masking
+      // only on the tail tile.
       {
         const int row = half * 128 + quad * 32 + lane;
         const int64_t nk_row = pos_nk(p, t0 + row / kG);    // rows of one query share its kernel count
@@ -293,30 +293,35 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           tc_fence_after();
           const int64_t jbase = (int64_t)c * kNT;
           const bool tail = jbase + kNT > nk_min;
-#pragma unroll 1
-          for (int ch = 0; ch < 4; ch += 2) {
-            float v[64];
-            tmem_ld32(tmem + lane_base + buf * 256 + half * 128 + ch * 32, *reinterpret_cast<float(*)[32]>(v));
-            tmem_ld32(tmem + lane_base + buf * 256 + half * 128 + ch * 32 + 32,
-                      *reinterpret_cast<float(*)[32]>(v + 32));
-            tmem_wait_ld();
+          // four 32-column chunks, the next chunk's TMEM load in flight while
+          // this one is reduced (tcgen05.wait::ld waits for all loads, so the
+          // wait sits after the compute)
+          const uint32_t cbase = tmem + lane_base + buf * 256 + half * 128;
+          float va[32], vb[32];
+          tmem_ld32(cbase, va);
+          tmem_wait_ld();
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            float* v = (ch & 1) ? vb : va;
+            if (ch < 3) tmem_ld32(cbase + (ch + 1) * 32, *reinterpret_cast<float(*)[32]>((ch & 1) ? va : vb));
             if (tail) {
               const int64_t j0 = jbase + ch * 32;
 #pragma unroll
-              for (int x = 0; x < 64; ++x) v[x] = (j0 + x < nk_row) ? v[x] : -INFINITY;
+              for (int x = 0; x < 32; ++x) v[x] = (j0 + x < nk_row) ? v[x] : -INFINITY;
             }
             float m4[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
-            for (int x = 4; x < 64; ++x) m4[x & 3] = fmaxf(m4[x & 3], v[x]);
+            for (int x = 4; x < 32; ++x) m4[x & 3] = fmaxf(m4[x & 3], v[x]);
             const float cmax = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * p.zscale;
             const float mnew = fmaxf(mrun, cmax);
             if (mnew != -INFINITY) {
               float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-              for (int x = 0; x < 64; ++x) a4[x & 3] += ex2(fmaf(v[x], p.zscale, -mnew));
+              for (int x = 0; x < 32; ++x) a4[x & 3] += ex2(fmaf(v[x], p.zscale, -mnew));
               srun = srun * ex2(mrun - mnew) + ((a4[0] + a4[1]) + (a4[2] + a4[3]));
               mrun = mnew;
             }
+            if (ch < 3) tmem_wait_ld();
           }
           tc_fence_before();
           __syncwarp();
@@ -335,7 +340,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       // lane 0 comes from the neighbouring quadrant (same tile) or the
       // previous tile through a small double-buffered smem carry.
       mbar_wait(rb_empty + (ucount & 1), ((ucount >> 1) & 1) ^ 1);
-      constexpr int kQC = 64 / kG;                             // queries per 64-column chunk
+      constexpr int kQC = 32 / kG;                             // queries per 32-column chunk
       constexpr int kQH = 128 / kG;                            // queries per column half
       const int kpb = p.kpb;
       const int jl = quad * 32 + lane;
@@ -353,13 +358,16 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int slot = c % 3;
         float* carry = stile + (slot * 2 + half) * 8 * kQH;
         float* part0 = carry + 4 * kQH;
-#pragma unroll 1
+        // 32-column chunks (kQC queries), next chunk's TMEM load in flight
+        const uint32_t cbase = tmem + lane_base + buf * 256 + half * kQH * kG;
+        float va[32], vb[32];
+        tmem_ld32(cbase, va);
+        tmem_wait_ld();
+#pragma unroll
         for (int qq = 0; qq < kQH; qq += kQC) {
-          float v[64];
-          const uint32_t col = tmem + lane_base + buf * 256 + (half * kQH + qq) * kG;
-          tmem_ld32(col, *reinterpret_cast<float(*)[32]>(v));
-          tmem_ld32(col + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-          tmem_wait_ld();
+          const int ch = qq / kQC;
+          float* v = (ch & 1) ? vb : va;
+          if (qq + kQC < kQH) tmem_ld32(cbase + (ch + 1) * 32, *reinterpret_cast<float(*)[32]>((ch & 1) ? va : vb));
           float sc[kQC];
 #pragma unroll
           for (int u4 = 0; u4 < kQC; ++u4) {
@@ -399,6 +407,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             st_shared_if(smem_u32(part0 + quad * kQH + qq + u4), r[u4], lane == 0);
             st_global_if(rbuf + (int64_t)qi * p.nb_cap + b, (r[u4] == -INFINITY) ? 0.f : r[u4], writer && lane > 0);
           }
+          if (qq + kQC < kQH) tmem_wait_ld();
         }
         tc_fence_before();
         __syncwarp();
