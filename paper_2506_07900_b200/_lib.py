@@ -84,11 +84,13 @@ def load() -> ctypes.CDLL:
         return _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
+            # INFLLM2_LIB_PATH: an alternative build of the same ABI (A/B timing of kernel variants)
+            path = os.environ.get("INFLLM2_LIB_PATH", LIB_PATH)
+            if not os.path.exists(path):
                 raise RuntimeError(
                     f"libinfllm2.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; "
                     "g.build()'` — there is no CPU fallback")
-            lib = ctypes.CDLL(LIB_PATH)
+            lib = ctypes.CDLL(path)
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.restype = res

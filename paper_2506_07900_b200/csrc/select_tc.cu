@@ -47,7 +47,11 @@ constexpr int kRows = kQ * kG;    // 256 (query, head) rows
 constexpr int kD = 128;
 constexpr int kNT = 128;          // kernels per tile
 constexpr int kStages = 2;
-constexpr int kEpiWarps = 8;
+#ifndef SEL_SPLIT
+#define SEL_SPLIT 1   // 2 (16 epilogue warps at 80 registers) measured ~2% slower
+#endif
+constexpr int kSplit = SEL_SPLIT;           // epilogue warps per TMEM quadrant and half
+constexpr int kEpiWarps = 8 * kSplit;
 constexpr int kTopkWarps = 4;     // dedicated selection warps (4 queries each)
 constexpr int kThreads = 32 * (2 + kEpiWarps + kTopkWarps);
 constexpr int kEpiThreads = 32 * kEpiWarps;
@@ -60,7 +64,7 @@ using topk::warp_select;
 constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
 constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 128 B)
 constexpr uint32_t kMuStageBytes = 4 * kMuHalfBytes;       // hi h0,h1, lo h0,h1 = 64 KB
-constexpr int kSTileLd = kNT + 4;                          // pass-2 carry scratch (>= 3*2*4*16 floats)
+constexpr int kSTileLd = kNT + 4;                          // epilogue scratch (see the epilogue)
 
 // Per-geometry constants: G heads per KV group, head dim D; a unit is always
 // 256 (query, head) rows, i.e. kQ = 256 / G query positions (16 for the 8B
@@ -71,10 +75,11 @@ struct SelCfg {
   static constexpr int kDH = D / 64;
   static constexpr uint32_t kQBytes = kRows * D * 2;
   static constexpr uint32_t kMuStageBytes = 2 * kDH * kMuHalfBytes;   // hi halves, then lo halves
+  static_assert(2 * kSplit * kRows + 3 * 2 * kSplit * 8 * (128 / G / kSplit) <= kQ * kSTileLd, "epilogue scratch");
   struct Smem {
     static constexpr uint32_t q = 0;
     static constexpr uint32_t mu = q + kQBytes;
-    static constexpr uint32_t stile = mu + kStages * kMuStageBytes;   // float [3][2][4][kQH] carries
+    static constexpr uint32_t stile = mu + kStages * kMuStageBytes;   // epilogue scratch
     static constexpr uint32_t lse2 = stile + kQ * kSTileLd * 4;       // float [kRows]
     static constexpr uint32_t bars = lse2 + kRows * 4;                // uint64 [..]
     static constexpr uint32_t topk = bars + 24 * 8;                   // per top-k warp lists
@@ -261,14 +266,29 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;                 // 0..7
+    // kEpiWarps = 8 * kSplit warps: groups ("subs") of four warps cover the
+    // four TMEM lane quadrants; sub = (column part, half).  More warps per
+    // SM sub-partition hide the TMEM-load / MUFU latency of each thread's
+    // chain (the epilogue, not the tensor pipe, bounds this kernel).
+    const int ew = warp - 2;                 // 0..kEpiWarps-1
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;                // pass 1: query tile; pass 2: column half
+    const int sub = ew >> 2;                 // 0..2*kSplit-1
+    const int half = sub & 1;                // pass 1: row half; pass 2: query half
+    const int cpart = sub >> 1;              // pass 1: column part; pass 2: query part
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    const int etid = ew * 32 + lane;         // 0..255
+    const int etid = ew * 32 + lane;
     int buf = 0;
     uint32_t acc_phase[2] = {0, 0};
     int ucount = 0;
+    constexpr int kQC = 32 / kG;                     // queries per 32-column chunk
+    constexpr int kQH = 128 / kG;                    // queries per column half
+    constexpr int kQS = kQH / kSplit;                // queries per sub in pass 2
+    constexpr int kCols1 = 128 / kSplit;             // pass-1 columns per thread
+    // scratch in the stile region: pass-1 partial (max, sum) per (part, row),
+    // then pass-2 carries [3 slots][subs][2][4 quads][kQS]
+    float* pm = stile;
+    float* ps = stile + kSplit * kRows;
+    float* carries = stile + 2 * kSplit * kRows;
     for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++ucount) {
       float* rbuf = p.rbuf + ((int64_t)blockIdx.x * 2 + (ucount & 1)) * kQ * p.nb_cap;
       int64_t t0;
@@ -291,19 +311,20 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           mbar_wait(acc_full + buf, acc_phase[buf]);
           acc_phase[buf] ^= 1;
           tc_fence_after();
-          const int64_t jbase = (int64_t)c * kNT;
-          const bool tail = jbase + kNT > nk_min;
-          // four 32-column chunks, the next chunk's TMEM load in flight while
-          // this one is reduced (tcgen05.wait::ld waits for all loads, so the
-          // wait sits after the compute)
-          const uint32_t cbase = tmem + lane_base + buf * 256 + half * 128;
+          const int64_t jbase = (int64_t)c * kNT + cpart * kCols1;
+          const bool tail = (int64_t)c * kNT + kNT > nk_min;
+          // 32-column chunks, the next chunk's TMEM load in flight while this
+          // one is reduced (tcgen05.wait::ld waits for all loads, so the wait
+          // sits after the compute)
+          const uint32_t cbase = tmem + lane_base + buf * 256 + half * 128 + cpart * kCols1;
           float va[32], vb[32];
           tmem_ld32(cbase, va);
           tmem_wait_ld();
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
+          for (int ch = 0; ch < kCols1 / 32; ++ch) {
             float* v = (ch & 1) ? vb : va;
-            if (ch < 3) tmem_ld32(cbase + (ch + 1) * 32, *reinterpret_cast<float(*)[32]>((ch & 1) ? va : vb));
+            if (ch + 1 < kCols1 / 32)
+              tmem_ld32(cbase + (ch + 1) * 32, *reinterpret_cast<float(*)[32]>((ch & 1) ? va : vb));
             if (tail) {
               const int64_t j0 = jbase + ch * 32;
 #pragma unroll
@@ -321,30 +342,49 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
               srun = srun * ex2(mrun - mnew) + ((a4[0] + a4[1]) + (a4[2] + a4[3]));
               mrun = mnew;
             }
-            if (ch < 3) tmem_wait_ld();
+            if (ch + 1 < kCols1 / 32) tmem_wait_ld();
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty + buf);
           buf ^= 1;
         }
-        lse2[row] = mrun + log2f(srun);
+        if constexpr (kSplit == 1) {
+          lse2[row] = mrun + log2f(srun);
+        } else {
+          pm[cpart * kRows + row] = mrun;
+          ps[cpart * kRows + row] = srun;
+        }
       }
       named_bar_sync(1, kEpiThreads);
+      if constexpr (kSplit > 1) {
+        if (etid < kRows) {
+          float m = pm[etid];
+#pragma unroll
+          for (int x = 1; x < kSplit; ++x) m = fmaxf(m, pm[x * kRows + etid]);
+          float sum = 0.f;
+#pragma unroll
+          for (int x = 0; x < kSplit; ++x) {
+            const float mx = pm[x * kRows + etid];
+            sum += (mx == -INFINITY) ? 0.f : ps[x * kRows + etid] * ex2(mx - m);
+          }
+          lse2[etid] = m + log2f(sum);
+        }
+        named_bar_sync(1, kEpiThreads);
+      }
 
       // ---- pass 2: group scores per kernel, block max.  A thread owns one
-      // kernel (TMEM lane) and kQH queries; lanes hold consecutive kernels,
+      // kernel (TMEM lane) and kQS queries; lanes hold consecutive kernels,
       // so block b's kernels [b*kpb - 1, (b+1)*kpb) (sparse.py:191-215: the
       // boundary kernel is shared with block b-1) are a shuffle-reduction
       // over kpb lanes plus the previous lane; the kernel before a warp's
       // lane 0 comes from the neighbouring quadrant (same tile) or the
-      // previous tile through a small double-buffered smem carry.
+      // previous tile through a small smem carry.
       mbar_wait(rb_empty + (ucount & 1), ((ucount >> 1) & 1) ^ 1);
-      constexpr int kQC = 32 / kG;                             // queries per 32-column chunk
-      constexpr int kQH = 128 / kG;                            // queries per column half
       const int kpb = p.kpb;
       const int jl = quad * 32 + lane;
       const bool first = (jl % kpb) == 0;
+      const int q0 = half * kQH + cpart * kQS;                 // this sub's first query
       for (int c = 0; c < tiles; ++c) {
         mbar_wait(acc_full + buf, acc_phase[buf]);
         acc_phase[buf] ^= 1;
@@ -352,37 +392,38 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int64_t jg = (int64_t)c * kNT + jl;               // this thread's kernel
         const int64_t b = jg / kpb;
         const bool writer = first && b < n_cand;
-        // scratch: [slot][half][quad][kQH] lane-31 scores (the kernel before the
-        // next quadrant's lane 0) and lane-0 partial block maxima; three slots so
-        // tile c + 3's writes never race tile c + 1's reads
+        // [slot][sub][carry | part0][quad][kQS]: lane-31 scores (the kernel
+        // before the next quadrant's lane 0) and lane-0 partial block maxima;
+        // three slots so tile c + 3's writes never race tile c + 1's reads
         const int slot = c % 3;
-        float* carry = stile + (slot * 2 + half) * 8 * kQH;
-        float* part0 = carry + 4 * kQH;
-        // 32-column chunks (kQC queries), next chunk's TMEM load in flight
-        const uint32_t cbase = tmem + lane_base + buf * 256 + half * kQH * kG;
+        float* carry = carries + (slot * 2 * kSplit + sub) * 8 * kQS;
+        float* part0 = carry + 4 * kQS;
+        const uint32_t cbase = tmem + lane_base + buf * 256 + q0 * kG;
         float va[32], vb[32];
         tmem_ld32(cbase, va);
         tmem_wait_ld();
 #pragma unroll
-        for (int qq = 0; qq < kQH; qq += kQC) {
+        for (int qq = 0; qq < kQS; qq += kQC) {
           const int ch = qq / kQC;
           float* v = (ch & 1) ? vb : va;
-          if (qq + kQC < kQH) tmem_ld32(cbase + (ch + 1) * 32, *reinterpret_cast<float(*)[32]>((ch & 1) ? va : vb));
+          if (qq + kQC < kQS) tmem_ld32(cbase + (ch + 1) * 32, *reinterpret_cast<float(*)[32]>((ch & 1) ? va : vb));
           float sc[kQC];
 #pragma unroll
           for (int u4 = 0; u4 < kQC; ++u4) {
-            const int qi = half * kQH + qq + u4;
-            const float* l2 = lse2 + qi * kG;
+            const int qi = q0 + qq + u4;
+            const uint32_t l2 = smem_u32(lse2 + qi * kG);
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-            for (int h = 0; h < kG; h += 2) {
-              a0 += ex2(fmaf(v[u4 * kG + h], p.zscale, -l2[h]));
-              a1 += ex2(fmaf(v[u4 * kG + h + 1], p.zscale, -l2[h + 1]));
+            for (int h = 0; h < kG; h += 4) {
+              const float4 l4 = lds4(l2 + h * 4);
+              a0 += ex2(fmaf(v[u4 * kG + h], p.zscale, -l4.x));
+              a1 += ex2(fmaf(v[u4 * kG + h + 1], p.zscale, -l4.y));
+              a0 += ex2(fmaf(v[u4 * kG + h + 2], p.zscale, -l4.z));
+              a1 += ex2(fmaf(v[u4 * kG + h + 3], p.zscale, -l4.w));
             }
             const bool live = jg < pos_nk(p, t0 + qi);
             sc[u4] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
           }
-          // the chunk's kQC shuffle chains are independent: issue them together
           float r[kQC];
 #pragma unroll
           for (int u4 = 0; u4 < kQC; ++u4) {
@@ -402,27 +443,32 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           }
 #pragma unroll
           for (int u4 = 0; u4 < kQC; ++u4) {
-            const int qi = half * kQH + qq + u4;
-            st_shared_if(smem_u32(carry + quad * kQH + qq + u4), sc[u4], lane == 31);
-            st_shared_if(smem_u32(part0 + quad * kQH + qq + u4), r[u4], lane == 0);
+            const int qi = q0 + qq + u4;
+            st_shared_if(smem_u32(carry + quad * kQS + qq + u4), sc[u4], lane == 31);
+            st_shared_if(smem_u32(part0 + quad * kQS + qq + u4), r[u4], lane == 0);
             st_global_if(rbuf + (int64_t)qi * p.nb_cap + b, (r[u4] == -INFINITY) ? 0.f : r[u4], writer && lane > 0);
           }
-          if (qq + kQC < kQH) tmem_wait_ld();
+          if (qq + kQC < kQS) tmem_wait_ld();
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + buf);
         buf ^= 1;
-        if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+        switch (sub) {                       // constant barrier ids (a variable id reserves all 16)
+          case 0: named_bar_sync(2, 128); break;
+          case 1: named_bar_sync(3, 128); break;
+          case 2: named_bar_sync(4, 128); break;
+          default: named_bar_sync(5, 128); break;
+        }
         {   // lane 0's block also holds the previous kernel: lane x finishes query x
-          const float* prev = (quad > 0) ? carry + (quad - 1) * kQH
-                                         : stile + (((slot + 2) % 3) * 2 + half) * 8 * kQH + 3 * kQH;
-          const int x = lane & (kQH - 1);
+          const float* prev = (quad > 0) ? carry + (quad - 1) * kQS
+                                         : carries + (((slot + 2) % 3) * 2 * kSplit + sub) * 8 * kQS + 3 * kQS;
+          const int x = lane & (kQS - 1);
           const int64_t b0 = ((int64_t)c * kNT + quad * 32) / kpb;
           const float pr = (quad == 0 && c == 0) ? -INFINITY : prev[x];
-          const float r = fmaxf(part0[quad * kQH + x], pr);
-          st_global_if(rbuf + (int64_t)(half * kQH + x) * p.nb_cap + b0, (r == -INFINITY) ? 0.f : r,
-                       lane < kQH && b0 < n_cand);
+          const float r = fmaxf(part0[quad * kQS + x], pr);
+          st_global_if(rbuf + (int64_t)(q0 + x) * p.nb_cap + b0, (r == -INFINITY) ? 0.f : r,
+                       lane < kQS && b0 < n_cand);
         }
       }
 
