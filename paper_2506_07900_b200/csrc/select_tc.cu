@@ -41,6 +41,17 @@ namespace {
 
 using namespace sm100;
 
+#ifdef SEL_PROFILE
+// per-CTA cycle counters (variant builds only, tools/build_variant.sh -DSEL_PROFILE):
+// [0] epilogue warp 2 total, [1] its acc_full waits, [2] its pass-1 time,
+// [3] MMA warp total, [4] MMA mu_full waits, [5] MMA acc_empty waits
+__device__ long long g_sel_cyc[160][8];
+#define SEL_T0(v) long long v = clock64()
+#define SEL_ADD(slot, v) (g_sel_cyc[blockIdx.x][slot] += clock64() - (v))
+#else
+#define SEL_T0(v)
+#define SEL_ADD(slot, v)
+#endif
 constexpr int kQ = 16;            // query positions per work unit
 constexpr int kG = 16;            // heads per KV group
 constexpr int kRows = kQ * kG;    // 256 (query, head) rows
@@ -102,6 +113,7 @@ struct Params {
   int64_t nb_cap;
   float zscale;                   // log2(e)/sqrt(D)
   int kq;                         // query positions per unit (256 / G)
+  int dbg;                        // INFLLM2_SELECT_DBG in -DSEL_PROFILE builds (experiments), else 0
 };
 
 // unit index -> (t0, group); heaviest (largest t0) units first
@@ -155,6 +167,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SEL_T0(t_kernel);
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
@@ -227,8 +240,12 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       q_phase ^= 1;
       for (int pass = 0; pass < 2; ++pass) {
         for (int c = 0; c < tiles; ++c) {
+          SEL_T0(tw0);
           mbar_wait(mu_full + stage, phase);
+          if (lane == 0) SEL_ADD(4, tw0);
+          SEL_T0(tw1);
           mbar_wait(acc_empty + buf, acc_phase[buf] ^ 1);
+          if (lane == 0) SEL_ADD(5, tw1);
           acc_phase[buf] ^= 1;
           tc_fence_after();
           if (elect_one()) {
@@ -299,6 +316,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int64_t qb = t0 / p.m;
       const int64_t n_cand = qb + 1;
 
+      SEL_T0(tp1);
       // ---- pass 1: row LSE (log2 domain).  Max on the raw accumulator
       // (zscale > 0), FFMA+ex2 with four independent partial sums; masking
       // only on the tail tile.
@@ -308,9 +326,12 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int64_t nk_min = pos_nk(p, t0);
         float mrun = -INFINITY, srun = 0.f;
         for (int c = 0; c < tiles; ++c) {
+          SEL_T0(tw);
           mbar_wait(acc_full + buf, acc_phase[buf]);
+          if (warp == 2 && lane == 0) SEL_ADD(1, tw);
           acc_phase[buf] ^= 1;
           tc_fence_after();
+          if (p.dbg & 4) { __syncwarp(); if (lane == 0) mbar_arrive(acc_empty + buf); buf ^= 1; continue; }
           const int64_t jbase = (int64_t)c * kNT + cpart * kCols1;
           const bool tail = (int64_t)c * kNT + kNT > nk_min;
           // 32-column chunks, the next chunk's TMEM load in flight while this
@@ -356,6 +377,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           ps[cpart * kRows + row] = srun;
         }
       }
+      if (warp == 2 && lane == 0) SEL_ADD(2, tp1);
       named_bar_sync(1, kEpiThreads);
       if constexpr (kSplit > 1) {
         if (etid < kRows) {
@@ -386,9 +408,17 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const bool first = (jl % kpb) == 0;
       const int q0 = half * kQH + cpart * kQS;                 // this sub's first query
       for (int c = 0; c < tiles; ++c) {
+        SEL_T0(tw);
         mbar_wait(acc_full + buf, acc_phase[buf]);
+        if (warp == 2 && lane == 0) SEL_ADD(1, tw);
         acc_phase[buf] ^= 1;
         tc_fence_after();
+        if (p.dbg & 2) {   // timing experiment: no pass-2 math (selection invalid)
+          __syncwarp(); if (lane == 0) mbar_arrive(acc_empty + buf); buf ^= 1;
+          if (sub == 0) named_bar_sync(2, 128); else if (sub == 1) named_bar_sync(3, 128);
+          else if (sub == 2) named_bar_sync(4, 128); else named_bar_sync(5, 128);
+          continue;
+        }
         const int64_t jg = (int64_t)c * kNT + jl;               // this thread's kernel
         const int64_t b = jg / kpb;
         const bool writer = first && b < n_cand;
@@ -492,7 +522,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       mbar_wait(rb_full + (ucount & 1), (ucount >> 1) & 1);
       for (int qi = tw; qi < kQ; qi += kTopkWarps) {
         const int64_t i = t0 + qi - p.start;
-        if (i < 0 || i >= p.n) continue;     // warp-uniform
+        if (i < 0 || i >= p.n || (p.dbg & 1)) continue;     // warp-uniform
         const int64_t item = i * p.hkv + grp;
         warp_select(rbuf + (int64_t)qi * p.nb_cap, us, lane, lkey, lid, p.selection + item * p.max_sel,
                     p.sel_scores ? p.sel_scores + item * p.max_sel : nullptr, p.max_sel);
@@ -505,6 +535,10 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   tc_fence_before();
   __syncthreads();
+#ifdef SEL_PROFILE
+  if (lane == 0 && warp == 2) SEL_ADD(0, t_kernel);
+  if (lane == 0 && warp == 1) SEL_ADD(3, t_kernel);
+#endif
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -599,6 +633,11 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
   p.units_per_group = (last - p.first_t0) / kQ + 1;
   p.n_units = p.units_per_group * cs.hkv;
   p.zscale = 1.4426950408889634f / sqrtf((float)D);
+#ifdef SEL_PROFILE
+  p.dbg = getenv("INFLLM2_SELECT_DBG") ? atoi(getenv("INFLLM2_SELECT_DBG")) : 0;   // experiments only
+#else
+  p.dbg = 0;
+#endif
   const int grid = tc_grid(p.n_units);
   if ((size_t)grid * 2 * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
   p.rbuf = static_cast<float*>(ws);
@@ -654,3 +693,13 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
 }
 
 }  // namespace infllm2
+
+extern "C" int infllm2_debug_select_cycles(long long* host, int max_entries) {
+#ifdef SEL_PROFILE
+  const int n = max_entries < 160 * 8 ? max_entries : 160 * 8;
+  return cudaMemcpyFromSymbol(host, infllm2::g_sel_cyc, sizeof(long long) * n) == cudaSuccess ? 0 : -1;
+#else
+  for (int i = 0; i < max_entries; ++i) host[i] = 0;
+  return 1;   // not a profiling build
+#endif
+}

@@ -39,6 +39,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// predicated global float max-reduction for values >= 0 (int order == float order)
+__device__ __forceinline__ void red_max_if(float* ptr, float v, bool pred) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p red.global.max.s32 [%0], %1;\n\t}" ::"l"(ptr),
+               "r"(__float_as_int(v)), "r"((int)pred)
+               : "memory");
+}
+
 // explicit shared-window vector load (a generic pointer into smem compiles to
 // LD.E, which waits on the long scoreboard)
 __device__ __forceinline__ float4 lds4(uint32_t addr) {

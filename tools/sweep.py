@@ -22,7 +22,7 @@ from paper_2506_07900_b200.sparse import _ptr, _stream, _workspace  # noqa: E402
 SHAPES = {"8B": (32, 2, 128), "0.5B": (16, 2, 64)}
 
 
-def time_layer(hq, hkv, d, L, k, reps=3):
+def time_layer(hq, hkv, d, L, k, reps=3, attend_too=True):
     cfg = P.SparseAttentionConfig(top_k=k)
     g = torch.Generator(device="cuda").manual_seed(L + k)
     q = torch.randn((L, hq, d), generator=g, device="cuda").to(torch.bfloat16)
@@ -47,6 +47,8 @@ def time_layer(hq, hkv, d, L, k, reps=3):
         _lib.check(lib.infllm2_attend(ctypes.byref(geom), _ptr(q), hq * d, L, 0, hq, hkv, d, _ptr(kc), _ptr(vc), cap, L,
                                       _ptr(sel), _ptr(out), None, 0, st), "attend")
 
+    if not attend_too:      # stage 1 only (e.g. timing experiments that leave the selection invalid)
+        attend = lambda: None  # noqa: E731
     for _ in range(2):
         select()
         attend()
