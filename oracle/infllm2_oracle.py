@@ -304,17 +304,47 @@ class OracleResult:
     scores: Optional[list] = None          # per (row, group) block scores if kept
 
 
+def approx_group_kernel_scores(q_heads: np.ndarray, means: np.ndarray, coarse: np.ndarray,
+                               geom: Geometry, dot: str) -> np.ndarray:
+    """S_j under the approx-LSE selection mode (opt-in).
+
+    The reference has no driver for this mode: ``approx_lse`` (sparse.py:292-312)
+    is its only LSE estimator.  Definition used here and by the GPU (DESIGN §4
+    K2p): head h's weights are P_hj = exp(z_hj - approx_lse(q_h, coarse[:nc_t]))
+    in float64, with nc_t = min(t // s_c + 1, L // s_c) coarse kernels (the
+    causal analogue of nk_t, sparse.py:426) passed in as ``coarse``; then the
+    group mean in head order (sparse.py:183-188).  With no coarse kernel
+    (L < s_c) the exact softmax is used.
+    """
+    if coarse.shape[0] == 0:
+        return group_kernel_scores(q_heads, means, dot)
+    z = scaled_dots(means, q_heads, dot)
+    if not np.isfinite(z).all():
+        raise OracleValidationError("non-finite values in kernel scoring")
+    per_head = np.stack([np.exp(z[h] - approx_lse(q_heads[h], coarse, geom.kernel_stride,
+                                                   geom.coarse_stride, dot))
+                         for h in range(z.shape[0])])
+    return per_head.mean(axis=0)
+
+
 def two_stage_attention(q: np.ndarray, keys: np.ndarray, values: np.ndarray,
                         fine_means: np.ndarray, geom: Geometry, start_position: int,
                         *, rows: Optional[np.ndarray] = None, dot: str = "f64",
-                        keep_scores: bool = False) -> OracleResult:
+                        keep_scores: bool = False, lse_mode: str = "exact",
+                        coarse_means: Optional[np.ndarray] = None) -> OracleResult:
     """Restatement of ``two_stage_attention`` (sparse.py:387-468).
 
     ``keys``/``values`` are the whole cache (L, HKV, D); ``fine_means`` its
     (L//s, HKV, D) float32 kernel means.  ``rows`` optionally restricts the
     computation to a subset of query rows (results for other rows are zero /
-    -1); rows are independent given the cache.
+    -1); rows are independent given the cache.  ``lse_mode="approx"``
+    (with ``coarse_means`` (L//s_c, HKV, D)) normalises stage 1 by approx_lse
+    instead of the exact softmax (see ``approx_group_kernel_scores``).
     """
+    if lse_mode not in ("exact", "approx"):
+        raise OracleValidationError(f"unknown lse_mode {lse_mode!r}")
+    if lse_mode == "approx" and coarse_means is None:
+        raise OracleValidationError("approx lse_mode needs coarse_means")
     n, hq, d = q.shape
     length, hkv, _ = keys.shape
     if hkv and hq % hkv:
@@ -340,7 +370,12 @@ def two_stage_attention(q: np.ndarray, keys: np.ndarray, values: np.ndarray,
         forced = force_blocks(n_cand, pos // m, geom.n_init_blocks, geom.n_local_blocks)
         for g in range(hkv):
             qh = q[i, g * g_size:(g + 1) * g_size, :]
-            if n_kernels > 0:
+            if n_kernels > 0 and lse_mode == "approx":
+                nc_t = min(pos // geom.coarse_stride + 1, coarse_means.shape[0])
+                gs = approx_group_kernel_scores(qh, fine_means[:n_kernels, g, :], coarse_means[:nc_t, g, :],
+                                                geom, dot)
+                bs = block_scores(gs, pos, geom)
+            elif n_kernels > 0:
                 gs = group_kernel_scores(qh, fine_means[:n_kernels, g, :], dot)
                 bs = block_scores(gs, pos, geom)
             else:
