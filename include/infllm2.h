@@ -132,6 +132,26 @@ int infllm2_select(const infllm2_geometry* g,
                    void* workspace, size_t workspace_bytes, int32_t flags,
                    infllm2_stream_t stream);
 
+/* Stage 1 in the opt-in approx-LSE mode (the paper's
+ * LSE-approximated stage 1): head h's kernel weights are
+ * exp(z_hj - approx_lse(q_h, coarse[:nc_t])) with approx_lse as in
+ * sparse.py:292-312 (logsumexp over coarse dots + ln(s_c/s)) and
+ * nc_t = min(t // s_c + 1, cache_len // s_c); the rest as infllm2_select.  The
+ * reference has no driver for this mode (it changes ~1/3 of selections, SURVEY
+ * F3); with cache_len < s_c it is infllm2_select.  coarse_means f32
+ * [HKV][coarse_cap][D]; coarse_hi/lo (bf16 split, may be NULL: CUDA-core path)
+ * as the fine pair.  Same workspace as infllm2_select. */
+int infllm2_select_approx(const infllm2_geometry* g,
+                          const void* q, int64_t q_row_stride, int64_t n, int64_t start,
+                          int32_t hq, int32_t hkv, int32_t d,
+                          const float* fine_means, const void* means_hi, const void* means_lo,
+                          int64_t means_cap,
+                          const float* coarse_means, const void* coarse_hi, const void* coarse_lo,
+                          int64_t coarse_cap, int64_t cache_len,
+                          int32_t* selection, double* sel_scores,
+                          void* workspace, size_t workspace_bytes, int32_t flags,
+                          infllm2_stream_t stream);
+
 /* Stage 2: attention over the selected blocks, causally clipped
  * (sparse_attend, sparse.py:347-384).  Writes out (n, HQ, D) and lse (n, HQ)
  * (lse may be NULL). */

@@ -50,6 +50,9 @@ SIGNATURES = {
     "infllm2_select": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,
                                       c_i32, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_sz,
                                       c_i32, c_vp]),
+    "infllm2_select_approx": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,
+                                             c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                             c_vp, c_vp, c_vp, c_sz, c_i32, c_vp]),
     "infllm2_attend": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,
                                       c_i32, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "infllm2_forward": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,

@@ -148,6 +148,33 @@ int infllm2_select(const infllm2_geometry* g, const void* q, int64_t q_row_strid
                                         sel_scores, workspace, workspace_bytes, st));
 }
 
+int infllm2_select_approx(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
+                          int64_t start, int32_t hq, int32_t hkv, int32_t d, const float* fine_means,
+                          const void* means_hi, const void* means_lo, int64_t means_cap,
+                          const float* coarse_means, const void* coarse_hi, const void* coarse_lo,
+                          int64_t coarse_cap, int64_t cache_len, int32_t* selection, double* sel_scores,
+                          void* workspace, size_t workspace_bytes, int32_t flags, infllm2_stream_t stream) {
+  CallShape cs;
+  int rc = make_shape(g, n, start, hq, hkv, d, cache_len, &cs);
+  if (rc) return rc;
+  if (n == 0) return INFLLM2_OK;
+  if (cs.nk_total > means_cap) return INFLLM2_ERR_CAPACITY;
+  const int64_t nc_total = cache_len / g->coarse_stride;
+  if (nc_total > 0 && (coarse_means == nullptr || nc_total > coarse_cap)) return INFLLM2_ERR_CAPACITY;
+  CoarseArgs ca{coarse_means, coarse_hi, coarse_lo, coarse_cap, nc_total};
+  const CoarseArgs* cp = nc_total > 0 ? &ca : nullptr;      // no coarse kernel yet: the exact softmax
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_select_supported(*g, cs, means_hi != nullptr) &&
+      (cp == nullptr || coarse_hi != nullptr)) {
+    return cuda_status(launch_select_tc(*g, cs, q, q_row_stride, fine_means, means_hi, means_lo, means_cap,
+                                        selection, sel_scores, workspace, workspace_bytes, st, cp));
+  }
+  const size_t need = select_simt_workspace(n * hkv, cs.nk_total, cs.nb_max);
+  if (workspace == nullptr || workspace_bytes < need) return INFLLM2_ERR_WORKSPACE;
+  return cuda_status(launch_select_simt(*g, cs, q, q_row_stride, fine_means, means_cap, selection,
+                                        sel_scores, workspace, workspace_bytes, st, cp));
+}
+
 int infllm2_attend(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
                    int64_t start, int32_t hq, int32_t hkv, int32_t d, const void* k_cache,
                    const void* v_cache, int64_t cap, int64_t cache_len, const int32_t* selection,

@@ -57,11 +57,21 @@ cudaError_t launch_append_kv(void* k_cache, void* v_cache, int64_t cap, int hkv,
 cudaError_t launch_compress(const void* k_cache, int64_t cap, int hkv, int d, int64_t first,
                             int64_t count, int64_t length, int p, int s, float* means,
                             void* hi, void* lo, int64_t means_cap, cudaStream_t stream);
+// Coarse kernel means (stride s_c) for the opt-in approx-LSE selection mode
+// (DESIGN §4 K2p): head weights exp(z - approx_lse) with approx_lse over the
+// nc_t = min(t // s_c + 1, nc_total) coarse kernels (sparse.py:292-312).
+struct CoarseArgs {
+  const float* means;      // f32 [HKV][cap][D]
+  const void* hi;          // bf16 split (tensor-core path)
+  const void* lo;
+  int64_t cap;
+  int64_t nc_total;        // cache_len // s_c (>= 1)
+};
 size_t select_simt_workspace(int64_t items, int64_t nk_total, int64_t nb_max);
 cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
                                int64_t q_row_stride, const float* means, int64_t means_cap,
                                int32_t* selection, double* sel_scores, void* ws, size_t ws_bytes,
-                               cudaStream_t stream);
+                               cudaStream_t stream, const CoarseArgs* coarse = nullptr);
 cudaError_t launch_attend_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
                                int64_t q_row_stride, const void* k_cache, const void* v_cache,
                                int64_t cap, const int32_t* selection, void* out, int out_f32,

@@ -37,6 +37,8 @@ struct SelectArgs {
   double* sel_scores;
   double* ws;
   int64_t ws_per_cta;  // doubles
+  const float* coarse;   // approx-LSE mode (nullptr: exact softmax)
+  int64_t coarse_cap, nc_total;
 };
 
 __device__ __forceinline__ bool better(double ra, int64_t ba, double rb, int64_t bb) {
@@ -87,12 +89,23 @@ __global__ void __launch_bounds__(kThreads) select_simt_kernel(SelectArgs a) {
     const int jl_me = tid / G;
     const float* mu_g = a.means + (int64_t)grp * a.means_cap * D;
 
+    // approx-LSE mode: pass 1 runs over the nc_t visible coarse kernels and the
+    // normaliser gains ln(s_c / s) (sparse.py:292-312)
+    int64_t nc_t = 0;
+    if (a.coarse != nullptr) {
+      nc_t = pos / a.g.coarse_stride + 1;
+      if (nc_t > a.nc_total) nc_t = a.nc_total;
+    }
+    const bool approx = nc_t > 0;
+    const float* p1_base = approx ? a.coarse + (int64_t)grp * a.coarse_cap * D : mu_g;
+    const int64_t p1_n = approx ? nc_t : nk_t;
+
     if (nk_t > 0) {
       // ---- pass 1: per-head max / sum-exp
       double mloc = -DBL_MAX, sloc = 0.0;
       if (tid < active) {
-        for (int64_t j = jl_me; j < nk_t; j += tj) {
-          const float* mu = mu_g + j * D;
+        for (int64_t j = jl_me; j < p1_n; j += tj) {
+          const float* mu = p1_base + j * D;
           const double* qh = qs + h_me * ldq;
           double dot = 0.0;
           for (int e = 0; e < D; ++e) dot = fma((double)mu[e], qh[e], dot);
@@ -115,7 +128,7 @@ __global__ void __launch_bounds__(kThreads) select_simt_kernel(SelectArgs a) {
         for (int t = tid; t < active; t += G)
           if (part_s[t] > 0.0) Ssum += part_s[t] * exp(part_m[t] - M);
         hmax[tid] = M;
-        hsum[tid] = Ssum;
+        hsum[tid] = approx ? Ssum * ((double)a.g.coarse_stride / (double)s) : Ssum;
       }
       __syncthreads();
 
@@ -237,8 +250,11 @@ size_t select_simt_workspace(int64_t items, int64_t nk_total, int64_t nb_max) {
 cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
                                int64_t q_row_stride, const float* means, int64_t means_cap,
                                int32_t* selection, double* sel_scores, void* ws, size_t ws_bytes,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, const CoarseArgs* coarse) {
   SelectArgs a;
+  a.coarse = coarse ? coarse->means : nullptr;
+  a.coarse_cap = coarse ? coarse->cap : 0;
+  a.nc_total = coarse ? coarse->nc_total : 0;
   a.g = g;
   a.q = static_cast<const __nv_bfloat16*>(q);
   a.q_row_stride = q_row_stride;

@@ -114,6 +114,12 @@ struct Params {
   float zscale;                   // log2(e)/sqrt(D)
   int kq;                         // query positions per unit (256 / G)
   int dbg;                        // INFLLM2_SELECT_DBG in -DSEL_PROFILE builds (experiments), else 0
+  // approx-LSE mode (DESIGN §4 K2p): pass 1 over the nc_t coarse kernels,
+  // LSE + log2(s_c / s); pass 2 unchanged
+  int approx;
+  int64_t nc_total;
+  int sc;
+  float lse_bias2;
 };
 
 // unit index -> (t0, group); heaviest (largest t0) units first
@@ -130,6 +136,13 @@ __device__ __forceinline__ int64_t pos_nk(const Params& p, int64_t t) {
 }
 // largest kernel count in the unit (its last query)
 __device__ __forceinline__ int64_t unit_nk(const Params& p, int64_t t0) { return pos_nk(p, t0 + p.kq - 1); }
+// coarse kernel count of query position t (approx-LSE mode)
+__device__ __forceinline__ int64_t pos_nc(const Params& p, int64_t t) {
+  const int64_t nc = t / p.sc + 1;
+  return nc < p.nc_total ? nc : p.nc_total;
+}
+// pass-1 kernel count of position t: fine kernels, or coarse ones in approx mode
+__device__ __forceinline__ int64_t pos_n1(const Params& p, int64_t t) { return p.approx ? pos_nc(p, t) : pos_nk(p, t); }
 
 __device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t nk) {
   const int64_t qb = t0 / p.m;
@@ -141,7 +154,8 @@ __device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t n
 template <int G, int D>
 __global__ void __launch_bounds__(kThreads, 1)
 select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_hi,
-                 const __grid_constant__ CUtensorMap tm_lo, const Params p) {
+                 const __grid_constant__ CUtensorMap tm_lo, const __grid_constant__ CUtensorMap tm_chi,
+                 const __grid_constant__ CUtensorMap tm_clo, const Params p) {
   using C = SelCfg<G, D>;
   using SmemLayout = typename C::Smem;
   constexpr int kQ = C::kQ;
@@ -201,6 +215,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         unit_coords(p, u, &t0, &grp);
         const int64_t nk = unit_nk(p, t0);
         const int tiles = unit_tiles(p, t0, nk);
+        const int tiles1 = p.approx ? (int)((pos_nc(p, t0 + p.kq - 1) + kNT - 1) / kNT) : tiles;
         mbar_wait(q_empty, q_phase ^ 1);
         q_phase ^= 1;
         mbar_arrive_expect_tx(q_full, kQBytes);
@@ -208,14 +223,16 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 #pragma unroll
         for (int hh = 0; hh < C::kDH; ++hh) tma_load_3d(sq + hh * (kRows * 128), &tm_q, q_full, 64 * hh, grp * kG, i0);
         for (int pass = 0; pass < 2; ++pass) {
-          for (int c = 0; c < tiles; ++c) {
+          const CUtensorMap* mh = (pass == 0 && p.approx) ? &tm_chi : &tm_hi;
+          const CUtensorMap* ml = (pass == 0 && p.approx) ? &tm_clo : &tm_lo;
+          for (int c = 0; c < (pass ? tiles : tiles1); ++c) {
             mbar_wait(mu_empty + stage, phase ^ 1);
             uint8_t* dst = smu + stage * kMuStageBytes;
             mbar_arrive_expect_tx(mu_full + stage, kMuStageBytes);
 #pragma unroll
             for (int hh = 0; hh < C::kDH; ++hh) {
-              tma_load_3d(dst + hh * kMuHalfBytes, &tm_hi, mu_full + stage, 64 * hh, c * kNT, grp);
-              tma_load_3d(dst + (C::kDH + hh) * kMuHalfBytes, &tm_lo, mu_full + stage, 64 * hh, c * kNT, grp);
+              tma_load_3d(dst + hh * kMuHalfBytes, mh, mu_full + stage, 64 * hh, c * kNT, grp);
+              tma_load_3d(dst + (C::kDH + hh) * kMuHalfBytes, ml, mu_full + stage, 64 * hh, c * kNT, grp);
             }
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
@@ -236,10 +253,11 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       unit_coords(p, u, &t0, &grp);
       const int64_t nk = unit_nk(p, t0);
       const int tiles = unit_tiles(p, t0, nk);
+      const int tiles1 = p.approx ? (int)((pos_nc(p, t0 + p.kq - 1) + kNT - 1) / kNT) : tiles;
       mbar_wait(q_full, q_phase);
       q_phase ^= 1;
       for (int pass = 0; pass < 2; ++pass) {
-        for (int c = 0; c < tiles; ++c) {
+        for (int c = 0; c < (pass ? tiles : tiles1); ++c) {
           SEL_T0(tw0);
           mbar_wait(mu_full + stage, phase);
           if (lane == 0) SEL_ADD(4, tw0);
@@ -313,6 +331,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       unit_coords(p, u, &t0, &grp);
       const int64_t nk = unit_nk(p, t0);
       const int tiles = unit_tiles(p, t0, nk);
+      const int tiles1 = p.approx ? (int)((pos_nc(p, t0 + p.kq - 1) + kNT - 1) / kNT) : tiles;
       const int64_t qb = t0 / p.m;
       const int64_t n_cand = qb + 1;
 
@@ -322,10 +341,10 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       // only on the tail tile.
       {
         const int row = half * 128 + quad * 32 + lane;
-        const int64_t nk_row = pos_nk(p, t0 + row / kG);    // rows of one query share its kernel count
-        const int64_t nk_min = pos_nk(p, t0);
+        const int64_t nk_row = pos_n1(p, t0 + row / kG);    // rows of one query share its kernel count
+        const int64_t nk_min = pos_n1(p, t0);
         float mrun = -INFINITY, srun = 0.f;
-        for (int c = 0; c < tiles; ++c) {
+        for (int c = 0; c < tiles1; ++c) {
           SEL_T0(tw);
           mbar_wait(acc_full + buf, acc_phase[buf]);
           if (warp == 2 && lane == 0) SEL_ADD(1, tw);
@@ -371,7 +390,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           buf ^= 1;
         }
         if constexpr (kSplit == 1) {
-          lse2[row] = mrun + log2f(srun);
+          lse2[row] = mrun + log2f(srun) + p.lse_bias2;
         } else {
           pm[cpart * kRows + row] = mrun;
           ps[cpart * kRows + row] = srun;
@@ -390,7 +409,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const float mx = pm[x * kRows + etid];
             sum += (mx == -INFINITY) ? 0.f : ps[x * kRows + etid] * ex2(mx - m);
           }
-          lse2[etid] = m + log2f(sum);
+          lse2[etid] = m + log2f(sum) + p.lse_bias2;
         }
         named_bar_sync(1, kEpiThreads);
       }
@@ -624,7 +643,7 @@ size_t tc_select_workspace(const infllm2_geometry& g, const CallShape& cs, int) 
 template <int G, int D>
 static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64_t q_row_stride, const void* means_hi,
                                        const void* means_lo, int64_t means_cap, Params& p, void* ws, size_t ws_bytes,
-                                       cudaStream_t stream) {
+                                       cudaStream_t stream, const CoarseArgs* coarse) {
   using C = SelCfg<G, D>;
   constexpr int kQ = C::kQ;
   p.kq = kQ;
@@ -641,7 +660,7 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
   const int grid = tc_grid(p.n_units);
   if ((size_t)grid * 2 * kQ * p.nb_cap * sizeof(float) > ws_bytes || ws == nullptr) return cudaErrorInvalidValue;
   p.rbuf = static_cast<float*>(ws);
-  CUtensorMap tq, thi, tlo;
+  CUtensorMap tq, thi, tlo, tchi, tclo;
   {
     const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.hq, (uint64_t)cs.n};
     const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};
@@ -655,6 +674,16 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
     if (!encode_tmap_3d_bf16(&thi, means_hi, dims, strides, box)) return cudaErrorInvalidValue;
     if (!encode_tmap_3d_bf16(&tlo, means_lo, dims, strides, box)) return cudaErrorInvalidValue;
   }
+  if (p.approx) {
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)coarse->cap, (uint64_t)cs.hkv};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)coarse->cap * D * 2};
+    const uint32_t box[3] = {64, (uint32_t)kNT, 1};
+    if (!encode_tmap_3d_bf16(&tchi, coarse->hi, dims, strides, box)) return cudaErrorInvalidValue;
+    if (!encode_tmap_3d_bf16(&tclo, coarse->lo, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
+    tchi = thi;
+    tclo = tlo;
+  }
   const size_t smem = C::Smem::total + 1024;
   static bool attr_set = false;
   if (!attr_set) {
@@ -663,15 +692,20 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
     attr_set = true;
   }
   count_launch();
-  select_tc_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, thi, tlo, p);
+  select_tc_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, thi, tlo, tchi, tclo, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
                              int64_t q_row_stride, const float* /*means*/, const void* means_hi,
                              const void* means_lo, int64_t means_cap, int32_t* selection,
-                             double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream) {
+                             double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream,
+                             const CoarseArgs* coarse) {
   Params p;
+  p.approx = coarse != nullptr;
+  p.nc_total = coarse ? coarse->nc_total : 0;
+  p.sc = (int)g.coarse_stride;
+  p.lse_bias2 = coarse ? log2f((float)g.coarse_stride / (float)g.kernel_stride) : 0.f;
   p.n = cs.n;
   p.start = cs.start;
   p.cache_len = cs.cache_len;
@@ -688,8 +722,10 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.sel_scores = sel_scores;
   p.nb_cap = cs.cache_len / g.block_size + 2;
   if (cs.group == 8 && cs.d == 64)
-    return launch_select_shape<8, 64>(cs, q, q_row_stride, means_hi, means_lo, means_cap, p, ws, ws_bytes, stream);
-  return launch_select_shape<16, 128>(cs, q, q_row_stride, means_hi, means_lo, means_cap, p, ws, ws_bytes, stream);
+    return launch_select_shape<8, 64>(cs, q, q_row_stride, means_hi, means_lo, means_cap, p, ws, ws_bytes, stream,
+                                      coarse);
+  return launch_select_shape<16, 128>(cs, q, q_row_stride, means_hi, means_lo, means_cap, p, ws, ws_bytes, stream,
+                                      coarse);
 }
 
 }  // namespace infllm2

@@ -10,7 +10,8 @@ size_t tc_select_workspace(const infllm2_geometry& g, const CallShape& cs, int f
 cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
                              int64_t q_row_stride, const float* means, const void* means_hi,
                              const void* means_lo, int64_t means_cap, int32_t* selection,
-                             double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream);
+                             double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream,
+                             const CoarseArgs* coarse = nullptr);
 bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs);
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
                              int64_t q_row_stride, const void* k_cache, const void* v_cache,

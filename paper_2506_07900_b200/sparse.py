@@ -191,6 +191,7 @@ class BlockizedLayerCache:
         self._nc_valid = 0
         self._k = self._v = None
         self._fine = self._fine_hi = self._fine_lo = self._coarse = None
+        self._coarse_hi = self._coarse_lo = None
         _lib.load()
         self._reserve(max(int(capacity), 0))
 
@@ -212,6 +213,8 @@ class BlockizedLayerCache:
         hi = torch.empty((h, cap // s + 1, d), dtype=torch.bfloat16, device=dev)
         lo = torch.empty_like(hi)
         coarse = torch.empty((h, cap // sc + 1, d), dtype=torch.float32, device=dev)
+        chi = torch.empty((h, cap // sc + 1, d), dtype=torch.bfloat16, device=dev)   # approx-LSE mode
+        clo = torch.empty_like(chi)
         if self._k is not None and self.length:
             k[:, :self.length].copy_(self._k[:, :self.length])
             v[:, :self.length].copy_(self._v[:, :self.length])
@@ -219,8 +222,11 @@ class BlockizedLayerCache:
             hi[:, :self._nk_valid].copy_(self._fine_hi[:, :self._nk_valid])
             lo[:, :self._nk_valid].copy_(self._fine_lo[:, :self._nk_valid])
             coarse[:, :self._nc_valid].copy_(self._coarse[:, :self._nc_valid])
+            chi[:, :self._nc_valid].copy_(self._coarse_hi[:, :self._nc_valid])
+            clo[:, :self._nc_valid].copy_(self._coarse_lo[:, :self._nc_valid])
         self._k, self._v = k, v
         self._fine, self._fine_hi, self._fine_lo, self._coarse = fine, hi, lo, coarse
+        self._coarse_hi, self._coarse_lo = chi, clo
         self._cap = cap
 
     @property
@@ -292,8 +298,8 @@ class BlockizedLayerCache:
             _ptr(self._fine_lo), self._fine.shape[1], st), "compress fine")
         _lib.check(lib.infllm2_compress(
             _ptr(self._k), self._cap, self.n_kv_heads, self.head_dim, l_old, self.length,
-            self._nc_valid, cfg.kernel_size, cfg.coarse_stride, _ptr(self._coarse), None, None,
-            self._coarse.shape[1], st), "compress coarse")
+            self._nc_valid, cfg.kernel_size, cfg.coarse_stride, _ptr(self._coarse), _ptr(self._coarse_hi),
+            _ptr(self._coarse_lo), self._coarse.shape[1], st), "compress coarse")
         self._nk_valid = self.length // cfg.kernel_stride
         self._nc_valid = self.length // cfg.coarse_stride
 
@@ -358,7 +364,8 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
                         start_position: int, *, stats: Optional[TouchStats] = None,
                         traces: Optional[list] = None, return_selection: bool = False,
                         return_lse: bool = False, out_dtype: Optional[torch.dtype] = None,
-                        exact: bool = False, split_p: bool = False, check_finite: bool = False):
+                        exact: bool = False, split_p: bool = False, check_finite: bool = False,
+                        lse: str = "exact"):
     """Block-sparse attention for ``q`` of shape (n, n_q_heads, head_dim).
 
     Same semantics as the reference (sparse.py:387-468): row i sits at
@@ -374,7 +381,15 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     ``split_p=True`` makes the tensor-core stage 2 carry the softmax weights as
     bf16 hi + lo (outputs ~1e-5 of the float64 reference instead of ~1e-4, at
     ~1.3x the stage-2 cost); the default uses bf16 weights.
+    ``lse="approx"`` is the opt-in approx-LSE selection mode (SURVEY §8f rank 4,
+    the paper's LSE-approximated stage 1): each head's kernel weights are
+    normalised by ``approx_lse`` over the coarse kernels (sparse.py:292-312)
+    instead of the exact softmax, which skips 7/8 of stage 1's first pass but
+    changes ~1/3 of the selections; the reference has no such
+    driver, so its default ``"exact"`` is what matches the reference.
     """
+    if lse not in ("exact", "approx"):
+        raise ValidationError(f"unknown lse mode {lse!r}")
     if not isinstance(q, torch.Tensor) or q.dim() != 3:
         raise ValidationError("q must be a (n, n_q_heads, head_dim) tensor")
     n, hq, d = q.shape
@@ -398,7 +413,7 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     smax = config.max_selected
     sel = torch.empty((n, hkv, smax), dtype=torch.int32, device=dev)
     out = torch.empty((n, hq, d), dtype=out_dtype, device=dev)
-    lse = torch.empty((n, hq), dtype=torch.float32, device=dev) if return_lse else None
+    lse_out = torch.empty((n, hq), dtype=torch.float32, device=dev) if return_lse else None
     sel_scores = torch.empty((n, hkv, smax), dtype=torch.float64, device=dev) if traces is not None else None
     flags = ((_lib.FLAG_EXACT_SIMT if exact else 0) | (_lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0)
              | (_lib.FLAG_P_SPLIT if split_p else 0))
@@ -406,11 +421,20 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     kc, vc, cap, fine, hi, lo, mcap = layer._device_args()
     ws_bytes = lib.infllm2_select_workspace_bytes(ctypes.byref(geom), n, hq, hkv, d, layer.length, flags)
     ws = _workspace(dev, ws_bytes)
-    if n:
+    if n and lse == "approx":
+        st = _stream(dev)
+        _lib.check(lib.infllm2_select_approx(
+            ctypes.byref(geom), _ptr(qb), qb.stride(0), n, start, hq, hkv, d, _ptr(fine), _ptr(hi), _ptr(lo), mcap,
+            _ptr(layer._coarse), _ptr(layer._coarse_hi), _ptr(layer._coarse_lo), layer._coarse.shape[1],
+            layer.length, _ptr(sel), _ptr(sel_scores), _ptr(ws), ws.numel(), flags, st), "two_stage_attention")
+        _lib.check(lib.infllm2_attend(
+            ctypes.byref(geom), _ptr(qb), qb.stride(0), n, start, hq, hkv, d, _ptr(kc), _ptr(vc), cap,
+            layer.length, _ptr(sel), _ptr(out), _ptr(lse_out), flags, st), "two_stage_attention")
+    elif n:
         _lib.check(lib.infllm2_forward(
             ctypes.byref(geom), _ptr(qb), qb.stride(0), n, start, hq, hkv, d, _ptr(kc), _ptr(vc), cap,
             layer.length, _ptr(fine), _ptr(hi), _ptr(lo), mcap, _ptr(sel), _ptr(sel_scores), _ptr(out),
-            _ptr(lse), _ptr(ws), ws.numel(), flags, _stream(dev)), "two_stage_attention")
+            _ptr(lse_out), _ptr(ws), ws.numel(), flags, _stream(dev)), "two_stage_attention")
     if stats is not None or traces is not None:
         _account(sel, sel_scores, start, layer, config, stats, traces)
     if return_selection or return_lse:
@@ -418,7 +442,7 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
         if return_selection:
             res += (sel,)
         if return_lse:
-            res += (lse,)
+            res += (lse_out,)
         return res
     return out
 
