@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-approx", action="store_true", help="skip the opt-in approx-LSE prefill line")
     ap.add_argument("--decode-seqs", type=int, default=8, help="sequences per GPU (configs[3]: 64 over 8 GPUs)")
     return ap.parse_args()
 
@@ -203,23 +204,23 @@ def run_ours(args):
         append in natural order and compress (paper_2506_07900_b200.sharding)."""
         S.fill_layer_cache(caches[layer], k_in[layer], v_in[layer], world)
 
-    def attend(layer, timed=False, outs=None):
+    def attend(layer, timed=False, outs=None, lse="exact"):
         cache = caches[layer]
         for h, (lo, hi) in enumerate(chunks):
             q = q_in[layer][h]
             if timed:
                 ev = ev_sel[2 * layer + h]
                 ev[0].record(stream)
-            o = P.two_stage_attention(q, cache, cfg, lo)
+            o = P.two_stage_attention(q, cache, cfg, lo, lse=lse)
             if timed:
                 ev[1].record(stream)
             if outs is not None:
                 outs.append(o)
 
-    def step(timed=False):
+    def step(timed=False, lse="exact"):
         for layer in range(layers):
             fill_cache(layer)
-            attend(layer, timed)
+            attend(layer, timed, lse=lse)
 
     # ---- per-kernel split (stage-1 select vs stage-2 attend) measured live via
     # the C ABI on this stream, one extra untimed pass after the timed region
@@ -309,6 +310,32 @@ def run_ours(args):
     roof["stage2_tflops"] = round(att_tflops, 2)
     roof["stage2_gather_GBps"] = round(rows2 * layers * D * 2 * 2 / (t_att / 1e3) / 1e9, 1)
 
+    # ---- secondary: the opt-in approx-LSE selection mode,
+    # same workload; not the headline (it selects differently from the reference)
+    approx = None
+    if not args.no_approx:
+        step(lse="approx")
+        barrier()
+        ta0 = torch.cuda.Event(enable_timing=True)
+        ta1 = torch.cuda.Event(enable_timing=True)
+        ta0.record(stream)
+        for _ in range(args.steps):
+            step(lse="approx")
+        ta1.record(stream)
+        barrier()
+        ms_a = ta0.elapsed_time(ta1)
+        if world > 1:
+            t = torch.tensor([ms_a], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_a = float(t.item())
+        approx = {"metric": "prefill tok/s @128K with lse='approx' (opt-in approx-LSE stage 1: pass 1 over the "
+                            "s_c=128 coarse kernels)",
+                  "value": round(seq / (ms_a / args.steps / 1e3), 1), "unit": "tok/s",
+                  "ms_per_step": round(ms_a / args.steps, 3),
+                  "note": "selection rule differs from the reference's exact softmax on ~1/3 of (row, group) "
+                          "pairs (SURVEY F3); parity pinned against fixtures composed from the reference's "
+                          "approx_lse (tests/test_approx_gpu.py)"}
+
     # ---- e2e through the public API with host buffers (pinned), H2D of every
     # layer's q/k/v shard and D2H of the last layer's output inside the region
     e2e = None
@@ -337,6 +364,7 @@ def run_ours(args):
                        "seq_len": seq, "layers": layers, "parallelism": f"query-shard x{world} (NCCL all-gather K/V)",
                        "l2": "inputs 1.2 GiB/layer x 32 layers >> 126 MB L2 (no flush needed)"},
             "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "decode": dec,
+            "approx_lse_mode": approx,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
