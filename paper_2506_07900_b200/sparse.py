@@ -189,6 +189,7 @@ class BlockizedLayerCache:
         self._cap = 0
         self._nk_valid = 0
         self._nc_valid = 0
+        self._nc_split = 0      # coarse rows whose bf16 hi/lo split is current (decode steps write f32 only)
         self._k = self._v = None
         self._fine = self._fine_hi = self._fine_lo = self._coarse = None
         self._coarse_hi = self._coarse_lo = None
@@ -292,6 +293,7 @@ class BlockizedLayerCache:
         lib = _lib.load()
         cfg = self.config
         st = _stream(self.device)
+        split_full = self._nc_split >= self._nc_valid
         _lib.check(lib.infllm2_compress(
             _ptr(self._k), self._cap, self.n_kv_heads, self.head_dim, l_old, self.length,
             self._nk_valid, cfg.kernel_size, cfg.kernel_stride, _ptr(self._fine), _ptr(self._fine_hi),
@@ -302,6 +304,18 @@ class BlockizedLayerCache:
             _ptr(self._coarse_lo), self._coarse.shape[1], st), "compress coarse")
         self._nk_valid = self.length // cfg.kernel_stride
         self._nc_valid = self.length // cfg.coarse_stride
+        self._nc_split = self._nc_valid if split_full else min(self._nc_split, self._nc_valid)
+
+    def _coarse_split(self) -> None:
+        """Bring the coarse means' bf16 hi/lo split (approx-LSE mode) up to date
+        after batched decode steps, which maintain the float32 means only."""
+        a, b = self._nc_split, self._nc_valid
+        if a < b:
+            c = self._coarse[:, a:b]
+            hi = c.to(torch.bfloat16)
+            self._coarse_hi[:, a:b].copy_(hi)
+            self._coarse_lo[:, a:b].copy_((c - hi.float()).to(torch.bfloat16))
+        self._nc_split = b
 
     def rebuild_kernels(self) -> tuple[torch.Tensor, torch.Tensor]:
         """From-scratch (fine, coarse) means, (count, HKV, D) float32 (sparse.py:135-140)."""
@@ -422,6 +436,7 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     ws_bytes = lib.infllm2_select_workspace_bytes(ctypes.byref(geom), n, hq, hkv, d, layer.length, flags)
     ws = _workspace(dev, ws_bytes)
     if n and lse == "approx":
+        layer._coarse_split()
         st = _stream(dev)
         _lib.check(lib.infllm2_select_approx(
             ctypes.byref(geom), _ptr(qb), qb.stride(0), n, start, hq, hkv, d, _ptr(fine), _ptr(hi), _ptr(lo), mcap,

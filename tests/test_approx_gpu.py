@@ -150,3 +150,27 @@ def test_approx_is_exact_without_coarse_kernels_and_validates():
     assert torch.equal(a, e)
     with pytest.raises(P.ValidationError):
         P.two_stage_attention(qd, layer, cfg, 0, lse="bogus")
+
+
+def test_approx_after_batched_decode_steps():
+    """Decode steps maintain the float32 coarse means only; the approx mode
+    re-derives their bf16 split, so a decoded cache selects like a cache built
+    from the same rows in one append (the length 2045 -> 2051 crosses a coarse
+    window)."""
+    cfg = P.SparseAttentionConfig(top_k=8)
+    L0, steps = 2045, 6
+    q, k, v = make_qkv(99, L0 + steps, 64, 32, 2, 128)
+    layer = P.BlockizedLayerCache(2, 128, cfg)
+    layer.append(torch.from_numpy(k[:L0]).cuda(), torch.from_numpy(v[:L0]).cuda())
+    batch = P.DecodeBatch([layer], cfg)
+    for st in range(steps):
+        batch.step(torch.from_numpy(q[st:st + 1]).cuda(), torch.from_numpy(k[L0 + st:L0 + st + 1]).cuda(),
+                   torch.from_numpy(v[L0 + st:L0 + st + 1]).cuda())
+    ref = P.BlockizedLayerCache(2, 128, cfg)
+    ref.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd = torch.from_numpy(q).cuda()
+    L = L0 + steps
+    a = P.two_stage_attention(qd, layer, cfg, L - 64, return_selection=True, lse="approx")[1]
+    b = P.two_stage_attention(qd, ref, cfg, L - 64, return_selection=True, lse="approx")[1]
+    assert torch.equal(a, b)
+    assert torch.equal(layer._coarse_hi[:, :L // 128], ref._coarse_hi[:, :L // 128])
