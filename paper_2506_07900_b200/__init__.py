@@ -6,15 +6,16 @@ Drop-in for the reference's sparse-attention surface (``deskinfer.sparse``):
 hand-written sm_100a kernels in ``libinfllm2.so`` (C ABI: ``include/infllm2.h``).
 """
 
-from . import model, stages
+from . import model, stages, tree
 from .decode import DecodeBatch
 from .errors import NumericError, ValidationError
+from .tree import PackedMask, tree_attention
 from .sparse import (BlockizedLayerCache, KVCache, SparseAttentionConfig, TouchStats,
                      blockized_cache, build_kernels, force_blocks, kernel_range_for_block,
                      partition_blocks, two_stage_attention)
 
 __all__ = [
-    "model", "stages", "DecodeBatch", "BlockizedLayerCache", "KVCache", "NumericError", "SparseAttentionConfig", "TouchStats",
+    "model", "stages", "tree", "DecodeBatch", "BlockizedLayerCache", "KVCache", "NumericError", "SparseAttentionConfig", "TouchStats",
     "ValidationError", "blockized_cache", "build_kernels", "force_blocks",
-    "kernel_range_for_block", "partition_blocks", "two_stage_attention",
+    "kernel_range_for_block", "partition_blocks", "two_stage_attention", "PackedMask", "tree_attention",
 ]

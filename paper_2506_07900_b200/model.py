@@ -102,6 +102,86 @@ def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, n_q_he
     return out.reshape(n, n_q_heads * d)
 
 
+def masked_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, allowed: torch.Tensor, *,
+                     n_q_heads: int, n_kv_heads: int) -> torch.Tensor:
+    """GQA with an explicit (n, m) visibility mask (model.py:194-226): float32
+    dots, float64 softmax and weighted sum; q (n, HQ*D), k/v (m, HKV*D)."""
+    n, m = q.shape[0], k.shape[0]
+    if not bool(allowed.any(dim=1).all()):
+        raise ValidationError("every query must see at least one key")
+    if not (bool(torch.isfinite(q).all()) and bool(torch.isfinite(k).all()) and bool(torch.isfinite(v).all())):
+        raise NumericError("non-finite values in attention inputs")
+    d = q.shape[1] // n_q_heads
+    g = n_q_heads // n_kv_heads
+    q3 = q.float().reshape(n, n_q_heads, d)
+    k3 = k.float().reshape(m, n_kv_heads, d)
+    v3 = v.double().reshape(m, n_kv_heads, d)
+    scale = float(np.float32(1.0 / np.sqrt(d)))
+    out = torch.empty((n, n_q_heads, d), dtype=torch.float32, device=q.device)
+    for h in range(n_q_heads):
+        s = ((q3[:, h, :] @ k3[:, h // g, :].T) * scale).double()
+        s = s.masked_fill(~allowed, float("-inf"))
+        out[:, h, :] = (torch.softmax(s, dim=-1) @ v3[:, h // g, :]).float()
+    return out.reshape(n, n_q_heads * d)
+
+
+def forward_tree(bundle, cache: KVCache, tokens, depths, mask, *, backend: str = "dense",
+                 sparse_config: Optional[SparseAttentionConfig] = None) -> ForwardResult:
+    """Score every node of a draft tree in one pass without touching the cache
+    (specdec.py:565-625): node i at position ``cache.length + depths[i] - 1``
+    sees every cached row plus its ancestor-or-self tree rows (``mask``, a
+    ``tree.PackedMask``).  ``backend="sparse"`` attends the prefix through the
+    two-stage operator (``tree.tree_attention``).  Like
+    ``forward``, q and the node K/V enter attention in bf16 (the cache dtype)."""
+    from .tree import tree_attention
+
+    cfg = bundle.config
+    toks = np.asarray(tokens, dtype=np.int64).reshape(-1)
+    dep = np.asarray(depths, dtype=np.int64).reshape(-1)
+    n = toks.size
+    if n == 0:
+        raise ValidationError("empty tree batch")
+    if dep.shape != (n,) or mask.n_nodes != n:
+        raise ValidationError("tokens, depths, and mask disagree on node count")
+    if toks.min() < 0 or toks.max() >= cfg.vocab_size:
+        raise ValidationError("token id out of range")
+    if backend not in ("dense", "sparse"):
+        raise ValidationError(f"unknown attention backend {backend!r}")
+    base = cache.length
+    if base == 0:
+        raise ValidationError("tree scoring needs a non-empty prefix cache")
+    if backend == "sparse" and sparse_config is None:
+        sparse_config = SparseAttentionConfig()
+    dev = cache.layers[0].device
+    p = _device_params(bundle, dev)
+    cos, sin = rope_angles(cfg, base + dep - 1, dev)
+    vis = torch.as_tensor(mask.to_dense(), device=dev)
+    allowed = torch.cat([torch.ones((n, base), dtype=torch.bool, device=dev), vis], dim=1)
+    x = p["embedding"][torch.as_tensor(toks, device=dev)]
+    for i in range(cfg.n_layers):
+        lp = f"layers.{i}."
+        h = rms_norm(x, p[lp + "attn_norm.weight"])
+        q = (h @ p[lp + "attn.wq"]).reshape(n, cfg.n_q_heads, cfg.head_dim)
+        k = (h @ p[lp + "attn.wk"]).reshape(n, cfg.n_kv_heads, cfg.head_dim)
+        v = (h @ p[lp + "attn.wv"]).reshape(n, cfg.n_kv_heads, cfg.head_dim)
+        q = apply_rope(q, cos, sin).to(torch.bfloat16).float()
+        k = apply_rope(k, cos, sin).to(torch.bfloat16).float()
+        v = v.to(torch.bfloat16).float()
+        layer = cache.layers[i]
+        if backend == "sparse":
+            attn = tree_attention(q, layer, sparse_config, k, v, mask).reshape(n, -1)
+        else:
+            keys = torch.cat([layer.keys.float(), k]).reshape(base + n, -1)
+            values = torch.cat([layer.values.float(), v]).reshape(base + n, -1)
+            attn = masked_attention(q.reshape(n, -1), keys, values, allowed, n_q_heads=cfg.n_q_heads,
+                                    n_kv_heads=cfg.n_kv_heads)
+        x = x + attn @ p[lp + "attn.wo"]
+        h = rms_norm(x, p[lp + "mlp_norm.weight"])
+        x = x + (_silu(h @ p[lp + "mlp.w_gate"]) * (h @ p[lp + "mlp.w_up"])) @ p[lp + "mlp.w_down"]
+    logits = rms_norm(x, p["final_norm.weight"]) @ p["_lm_head"].T
+    return ForwardResult(logits=logits, hiddens=x)
+
+
 def _silu(x: torch.Tensor) -> torch.Tensor:
     return x / (1.0 + torch.exp(-x))
 
