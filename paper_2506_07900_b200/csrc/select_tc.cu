@@ -423,9 +423,13 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       // previous tile through a small smem carry.
       mbar_wait(rb_empty + (ucount & 1), ((ucount >> 1) & 1) ^ 1);
       const int kpb = p.kpb;
+      const int kpb_log2 = __ffs(kpb) - 1;                     // kpb is a power of two
       const int jl = quad * 32 + lane;
-      const bool first = (jl % kpb) == 0;
+      const bool first = (jl & (kpb - 1)) == 0;
       const int q0 = half * kQH + cpart * kQS;                 // this sub's first query
+      // a thread's queries lie in one 16-position group of the (16- or
+      // 32-aligned) unit, so with s = 16 they share one kernel count
+      const int64_t nk_thr = pos_nk(p, t0 + q0);
       for (int c = 0; c < tiles; ++c) {
         SEL_T0(tw);
         mbar_wait(acc_full + buf, acc_phase[buf]);
@@ -439,8 +443,9 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           continue;
         }
         const int64_t jg = (int64_t)c * kNT + jl;               // this thread's kernel
-        const int64_t b = jg / kpb;
+        const int64_t b = jg >> kpb_log2;
         const bool writer = first && b < n_cand;
+        const bool live = jg < nk_thr;
         // [slot][sub][carry | part0][quad][kQS]: lane-31 scores (the kernel
         // before the next quadrant's lane 0) and lane-0 partial block maxima;
         // three slots so tile c + 3's writes never race tile c + 1's reads
@@ -470,7 +475,6 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
               a0 += ex2(fmaf(v[u4 * kG + h + 2], p.zscale, -l4.z));
               a1 += ex2(fmaf(v[u4 * kG + h + 3], p.zscale, -l4.w));
             }
-            const bool live = jg < pos_nk(p, t0 + qi);
             sc[u4] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
           }
           float r[kQC];
@@ -513,7 +517,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           const float* prev = (quad > 0) ? carry + (quad - 1) * kQS
                                          : carries + (((slot + 2) % 3) * 2 * kSplit + sub) * 8 * kQS + 3 * kQS;
           const int x = lane & (kQS - 1);
-          const int64_t b0 = ((int64_t)c * kNT + quad * 32) / kpb;
+          const int64_t b0 = ((int64_t)c * kNT + quad * 32) >> kpb_log2;
           const float pr = (quad == 0 && c == 0) ? -INFINITY : prev[x];
           const float r = fmaxf(part0[quad * kQS + x], pr);
           st_global_if(rbuf + (int64_t)(q0 + x) * p.nb_cap + b0, (r == -INFINITY) ? 0.f : r,
