@@ -778,15 +778,24 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         mbar_arrive(z_free);
       }
       named_bar_sync(1, 128);
+      // R_b = max S_j over block b's kernels [lo, hi) (kernel_range_for_block,
+      // sparse.py:191-215: lo = 4b - 1 for b >= 1, hi clipped to the row and nk):
+      // <= 5 kernels, loaded together, in 32-bit offsets from r0
       for (int64_t b = I.b0 + tid; b < I.b1; b += 128) {
         int64_t end = (b + 1) * kM;
         if (end > L) end = L;
-        int64_t lo, hi;
-        kernel_range_for_block(b * kM, end, kP, kS, I.nk, &lo, &hi);
+        int64_t hi64 = (end + kS - 1) / kS;
+        if (hi64 > I.nk) hi64 = I.nk;
+        const int lo = (int)((b == 0 ? 0 : 4 * b - 1) - I.r0);
+        const int hi = (int)(hi64 - I.r0);
         float r = 0.f;
         if (hi > lo) {
-          r = sarr[lo - I.r0];
-          for (int64_t j = lo + 1; j < hi; ++j) r = fmaxf(r, sarr[j - I.r0]);
+          float x[kP / kS + 3];
+#pragma unroll
+          for (int k = 0; k < kP / kS + 3; ++k) x[k] = sarr[lo + k < kMaxRows ? lo + k : lo];
+          r = x[0];
+#pragma unroll
+          for (int k = 1; k < kP / kS + 3; ++k) r = (lo + k < hi) ? fmaxf(r, x[k]) : r;
         }
         rarr[b - I.b0] = r;
       }
