@@ -86,7 +86,8 @@ struct AttCfg {
     static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
     static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
     static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
-    static constexpr uint32_t bars = red + 8 * 16 * 4;
+    static constexpr uint32_t flags = red + 8 * 16 * 4;           // [2 parities][8 warps] rescale votes
+    static constexpr uint32_t bars = flags + 2 * 8 * 4;
     static constexpr uint32_t total = bars + 88 * 8;
   };
 };
@@ -237,6 +238,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
   float* stats = reinterpret_cast<float*>(smem + Smem::stats);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
+  float* vote = reinterpret_cast<float*>(smem + Smem::flags);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -483,20 +485,21 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
 #pragma unroll
         for (int h = 0; h < kSH; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
-        // running max: exact on the first tile, rescale later only if z > M + 8
+        // running max: exact on the first tile, rescale later only if z > M + 8.
+        // The max is per head, so only the four warps of a head half vote (one
+        // 128-thread barrier per tile; votes double-buffered by tile parity: a
+        // warp cannot overwrite a slot before the others passed the next barrier)
         bool need = (c == c0);
         if (c > c0) {
           bool over = false;
 #pragma unroll
           for (int h = 0; h < kSH; ++h) over |= z[h] > mrun[h] + 8.f;
           const unsigned any = __ballot_sync(0xffffffffu, over);
-          if (lane == 0) red[ws * 16] = any ? 1.f : 0.f;
-          named_bar_sync(2, 256);
-          float f = 0.f;
-#pragma unroll
-          for (int x2 = 0; x2 < 8; ++x2) f += red[x2 * 16];
-          need = f > 0.f;
-          named_bar_sync(2, 256);
+          float* vt = vote + (tcount & 1) * 8;
+          if (lane == 0) vt[ws] = any ? 1.f : 0.f;
+          if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+          const int hb = 4 * half;
+          need = (vt[hb] + vt[hb + 1] + vt[hb + 2] + vt[hb + 3]) > 0.f;
         }
         if (need) {
           {
@@ -506,7 +509,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const float v = warp_reduce_n<kSH>(zz, lane, [](float a, float b) { return fmaxf(a, b); });
             if (reduce_writer_n<kSH>(lane)) red[ws * 16 + reduce_head_n<kSH>(lane)] = v;
           }
-          named_bar_sync(2, 256);
+          if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
           float corr[kSH];
           bool any_corr = false;
 #pragma unroll
@@ -521,7 +524,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             lsx[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
             mrun[h] = mnew;
           }
-          named_bar_sync(2, 256);
+          if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
           if (c > c0 && any_corr) {
             // rescale this thread's 8 O^T columns (d lane == row): wait for
             // PV(c-1), whose completion is the next phase of p_empty[its buffer]
