@@ -1,0 +1,29 @@
+"""Per-CTA cycle split of attend_tc (needs a -DATT_PROFILE variant build):
+  tools/build_variant.sh variants/aprof.so paper_2506_07900_b200/csrc/attend_tc.cu -DATT_PROFILE
+  INFLLM2_LIB_PATH=variants/aprof.so python tools/attend_profile.py
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ".")
+from sweep import time_layer  # noqa: E402
+from paper_2506_07900_b200 import _lib  # noqa: E402
+
+time_layer(32, 2, 128, int(os.environ.get("AB_LEN", "131072")), 16, reps=1)
+torch.cuda.synchronize()
+buf = (ctypes.c_longlong * (160 * 16))()
+_lib.load().infllm2_debug_attend_cycles(buf, 160 * 16)
+a = np.frombuffer(buf, dtype=np.int64).reshape(160, 16)[:148].astype(np.float64).mean(axis=0)
+names = {0: "QK total", 1: "(softmax inside tile loops)", 2: "QK s_empty wait", 3: "PV total", 4: "PV v_full wait",
+         5: "PV p_full wait", 6: "PV o_empty wait", 7: "softmax total", 8: "softmax s_full wait",
+         9: "softmax vote barrier", 10: "softmax need path", 11: "softmax p_empty wait",
+         12: "K TMA k_empty wait", 13: "V TMA v_empty wait", 14: "K TMA total", 15: "softmax S tmem ld+wait",
+         6: "(softmax P fence+arrive)"}
+for i, n in names.items():
+    tot = a[7] if i in (1, 6) else a[0] if i < 3 else a[3] if i < 7 else a[7] if i < 12 or i == 15 else a[14]
+    print(f"{n:24s} {a[i] / tot * 100:6.1f} %")

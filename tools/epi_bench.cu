@@ -10,7 +10,7 @@
 using namespace infllm2::sm100;
 
 template <int MODE>
-__global__ void bench(int iters, long long* out, float* sink, int mma, const float* gsrc, int tma) {
+__global__ void bench(int iters, long long* out, float* sink, int mma, const float* gsrc, int tma, int idle) {
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -21,7 +21,7 @@ __global__ void bench(int iters, long long* out, float* sink, int mma, const flo
   const uint32_t tmem = slot;
   const int quad = warp & 3;
   const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-  const int nw = (blockDim.x >> 5) - (mma ? 1 : 0) - (tma ? 1 : 0);
+  const int nw = (blockDim.x >> 5) - (mma ? 1 : 0) - (tma ? 1 : 0) - idle;
   volatile __shared__ int stop;
   if (threadIdx.x == 0) stop = 0;
   // fill: each warp writes its quadrant's columns it owns
@@ -84,6 +84,17 @@ __global__ void bench(int iters, long long* out, float* sink, int mma, const flo
       mbar_wait(&tbar, ph);
       ph ^= 1;
       ++k;
+    }
+    return;
+  }
+  if (warp >= nw + (mma ? 1 : 0) + (tma ? 1 : 0)) {   // idle warps parked on an mbarrier (like the top-k warps)
+    __shared__ uint64_t ibar;
+    if (threadIdx.x == (nw + (mma ? 1 : 0) + (tma ? 1 : 0)) * 32) { mbar_init(&ibar, 1); fence_barrier_init(); }
+    __syncwarp();
+    while (!stop) {
+      uint32_t done;
+      asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, 10000000;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+                   : "=r"(done) : "r"(smem_u32(&ibar)), "r"(0u) : "memory");
     }
     return;
   }
@@ -199,18 +210,19 @@ int main(int argc, char** argv) {
   auto fn = mode == 0 ? bench<0> : mode == 1 ? bench<1> : mode == 2 ? bench<2> : mode == 3 ? bench<3> : bench<4>;
   const int mma = argc > 3 ? atoi(argv[3]) : 0;
   const int tma = argc > 4 ? atoi(argv[4]) : 0;
+  const int idle = argc > 5 ? atoi(argv[5]) : 0;
   float* gsrc;
   cudaMalloc(&gsrc, 4096ull * 4096 * 4);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  fn<<<148, (warps + mma + tma) * 32, 66 * 1024>>>(10, d, sink, mma, gsrc, tma);
-  fn<<<148, (warps + mma + tma) * 32, 66 * 1024>>>(iters, d, sink, mma, gsrc, tma);
+  fn<<<148, (warps + mma + tma + idle) * 32, 66 * 1024>>>(10, d, sink, mma, gsrc, tma, idle);
+  fn<<<148, (warps + mma + tma + idle) * 32, 66 * 1024>>>(iters, d, sink, mma, gsrc, tma, idle);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += h[i];
   avg /= 148;
-  printf("tma=%d mma=%d warps=%2d mode=%d: %.0f cycles per 256x128 tile (MUFU bound 2048) %s\n", tma, mma, warps, mode, avg / iters,
+  printf("idle=%d tma=%d mma=%d warps=%2d mode=%d: %.0f cycles per 256x128 tile (MUFU bound 2048) %s\n", idle, tma, mma, warps, mode, avg / iters,
          cudaGetErrorString(e));
   return 0;
 }
