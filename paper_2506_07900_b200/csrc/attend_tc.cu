@@ -38,6 +38,20 @@ using namespace sm100;
 
 constexpr int kG = 16;
 constexpr int kD = 128;
+#ifdef ATT_PROFILE
+// per-CTA cycle counters (variant builds only, tools/build_variant.sh -DATT_PROFILE;
+// read by tools/attend_profile.py): [0] QK warp total [1] softmax in tile loops
+// [2] QK s_empty wait [3] PV warp total [4] PV v_full wait [5] PV p_full wait
+// [6] softmax P fence+arrive [7] softmax warp 2 total [8] its s_full wait
+// [9] vote barrier [10] need path [11] p_empty wait [12] K TMA k_empty wait
+// [13] V TMA v_empty wait [14] K TMA total [15] softmax S TMEM load + wait
+__device__ long long g_att_cyc[160][16];
+#define ATT_T0(v) long long v = clock64()
+#define ATT_ADD(slot, v) (g_att_cyc[blockIdx.x][slot] += clock64() - (v))
+#else
+#define ATT_T0(v)
+#define ATT_ADD(slot, v)
+#endif
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
 constexpr int kStages = 3;
@@ -241,6 +255,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   float* vote = reinterpret_cast<float*>(smem + Smem::flags);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ATT_T0(t_kernel);
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::kKStages; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
     for (int i = 0; i < C::kVStages; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
@@ -310,7 +325,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int b0 = sr.get(2 * c);
         const int b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         if (lane == 0) {
+          ATT_T0(t0w);
           mbar_wait(ring_empty + stage, phase ^ 1);
+          ATT_ADD(is_k ? 12 : 13, t0w);
           mbar_arrive_expect_tx(ring_full + stage, nt * C::kDH * (kM * 128));
           uint8_t* dst = ring + stage * kTileBytes;
           for (int x = 0; x < nt; ++x) {
@@ -354,7 +371,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       for (int c = c0; c < c1; ++c, ++tcount) {
         const int slot = tcount % kSlots;
         mbar_wait(k_full + stage, phase);
+        ATT_T0(q1);
         mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1);
+        if (lane == 0) ATT_ADD(2, q1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = sdesc_k_sw128(smem_u32(smem + Smem::kv + stage * kTileBytes));
@@ -396,8 +415,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int ob = it & 1;
       for (int c = c0; c < c1; ++c, ++pcount) {
         const int pbuf = pcount & 1;
+        ATT_T0(v0);
         mbar_wait(v_full + stage, vphase);
+        if (lane == 0) ATT_ADD(4, v0);
+        ATT_T0(v1);
         mbar_wait(p_full + pbuf, (pcount >> 1) & 1);
+        if (lane == 0) ATT_ADD(5, v1);
         if (c == c0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
@@ -465,15 +488,20 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       float mrun[kSH], lsum[kSH], lsx[kSH];     // lsum: weights as used by PV; lsx: unrounded (LSE)
 #pragma unroll
       for (int h = 0; h < kSH; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
+      ATT_T0(sloop);
       for (int c = c0; c < c1; ++c) {
         const int sslot = tcount % kSlots;
+        ATT_T0(s0);
         mbar_wait(s_full + sslot, (tcount / kSlots) & 1);
+        if (warp == 2 && lane == 0) ATT_ADD(8, s0);
         ++tcount;
         tc_fence_after();
         float z[kSH], z2[kSH];
+        ATT_T0(s4);
         tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + h0, z);
         tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + kG + h0, z2);
         tmem_wait_ld();
+        if (warp == 2 && lane == 0) ATT_ADD(15, s4);
 #pragma unroll
         for (int h = 0; h < kSH; ++h) z[h] += z2[h];
         tc_fence_before();
@@ -497,10 +525,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           const unsigned any = __ballot_sync(0xffffffffu, over);
           float* vt = vote + (tcount & 1) * 8;
           if (lane == 0) vt[ws] = any ? 1.f : 0.f;
+          ATT_T0(s1);
           if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+          if (warp == 2 && lane == 0) ATT_ADD(9, s1);
           const int hb = 4 * half;
           need = (vt[hb] + vt[hb + 1] + vt[hb + 2] + vt[hb + 3]) > 0.f;
         }
+        ATT_T0(s2);
         if (need) {
           {
             float zz[kSH];
@@ -542,8 +573,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             tc_fence_before();
           }
         }
+        if (warp == 2 && lane == 0) ATT_ADD(10, s2);
         // P = 2^(z - M) as bf16 into the MN-major interleaved buffer
+        ATT_T0(s3);
         mbar_wait(p_empty + pbuf, p_ph[pbuf] ^ 1);
+        if (warp == 2 && lane == 0) ATT_ADD(11, s3);
         p_ph[pbuf] ^= 1;
         // P in bf16 for one PV MMA per k-step; the row sums use the ROUNDED
         // weights, so O = sum P~ V / sum P~ stays a convex combination (error
@@ -573,11 +607,14 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           *reinterpret_cast<uint2*>(pb + base) = make_uint2(phi[0], phi[1]);
           if (p.p_split) *reinterpret_cast<uint2*>(pb + kPHalf + base) = make_uint2(plo[0], plo[1]);
         }
+        ATT_T0(s5);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + pbuf);
+        if (warp == 2 && lane == 0) ATT_ADD(6, s5);
         pbuf ^= 1;
       }
+      if (warp == 2 && lane == 0) ATT_ADD(1, sloop);
       // per-head row sums -> stats for the epilogue
       mbar_wait(st_empty + ob, ((it >> 1) & 1) ^ 1);
       float* st = stats + ob * 9 * 16;
@@ -677,6 +714,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   tc_fence_before();
   __syncthreads();
+#ifdef ATT_PROFILE
+  if (lane == 0 && warp == 1) ATT_ADD(0, t_kernel);
+  if (lane == 0 && warp == 10) ATT_ADD(3, t_kernel);
+  if (lane == 0 && warp == 2) ATT_ADD(7, t_kernel);
+  if (lane == 0 && warp == 0) ATT_ADD(14, t_kernel);
+#endif
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
@@ -881,3 +924,12 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
 
 }  // namespace infllm2
 
+extern "C" int infllm2_debug_attend_cycles(long long* host, int max_entries) {
+#ifdef ATT_PROFILE
+  const int n = max_entries < 160 * 16 ? max_entries : 160 * 16;
+  return cudaMemcpyFromSymbol(host, infllm2::g_att_cyc, sizeof(long long) * n) == cudaSuccess ? 0 : -1;
+#else
+  for (int i = 0; i < max_entries; ++i) host[i] = 0;
+  return 1;   // not a profiling build
+#endif
+}

@@ -19,11 +19,10 @@ torch.cuda.synchronize()
 buf = (ctypes.c_longlong * (160 * 16))()
 _lib.load().infllm2_debug_attend_cycles(buf, 160 * 16)
 a = np.frombuffer(buf, dtype=np.int64).reshape(160, 16)[:148].astype(np.float64).mean(axis=0)
-names = {0: "QK total", 1: "(softmax inside tile loops)", 2: "QK s_empty wait", 3: "PV total", 4: "PV v_full wait",
-         5: "PV p_full wait", 6: "PV o_empty wait", 7: "softmax total", 8: "softmax s_full wait",
+names = {0: "QK total", 2: "QK s_empty wait", 3: "PV total", 4: "PV v_full wait", 5: "PV p_full wait",
+         7: "softmax total", 1: "softmax in tile loops", 8: "softmax s_full wait", 15: "softmax S TMEM ld+wait",
          9: "softmax vote barrier", 10: "softmax need path", 11: "softmax p_empty wait",
-         12: "K TMA k_empty wait", 13: "V TMA v_empty wait", 14: "K TMA total", 15: "softmax S tmem ld+wait",
-         6: "(softmax P fence+arrive)"}
+         6: "softmax P fence+arrive", 14: "K TMA total", 12: "K TMA k_empty wait", 13: "V TMA v_empty wait"}
 for i, n in names.items():
     tot = a[7] if i in (1, 6) else a[0] if i < 3 else a[3] if i < 7 else a[7] if i < 12 or i == 15 else a[14]
     print(f"{n:24s} {a[i] / tot * 100:6.1f} %")
