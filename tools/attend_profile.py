@@ -24,5 +24,5 @@ names = {0: "QK total", 2: "QK s_empty wait", 3: "PV total", 4: "PV v_full wait"
          9: "softmax vote barrier", 10: "softmax need path", 11: "softmax p_empty wait",
          6: "softmax P fence+arrive", 14: "K TMA total", 12: "K TMA k_empty wait", 13: "V TMA v_empty wait"}
 for i, n in names.items():
-    tot = a[7] if i in (1, 6) else a[0] if i < 3 else a[3] if i < 7 else a[7] if i < 12 or i == 15 else a[14]
+    tot = a[0] if i in (0, 2) else a[3] if i in (3, 4, 5) else a[14] if i in (12, 13, 14) else a[7]
     print(f"{n:24s} {a[i] / tot * 100:6.1f} %")
