@@ -153,7 +153,9 @@ __device__ __forceinline__ void s1_item(const S1Params& p, const TableView& tv, 
 __global__ void __launch_bounds__(kS1Threads, 1)
 decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the __shared__ array (a uintptr_t round trip
+  // loses the address space: every access would compile to generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S1Smem::bars);
   uint64_t* mu_full = bars;          // [3]
   uint64_t* mu_empty = bars + 3;     // [3]

@@ -391,7 +391,9 @@ __device__ bool cta_topk(const float* r, int64_t base, int lo, int hi, int budge
 __global__ void __launch_bounds__(kThreads, 1)
 decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the __shared__ array (a uintptr_t round trip
+  // loses the address space: every access would compile to generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
   uint64_t* full = bars;                 // [3]
   uint64_t* empty = bars + 3;            // [3]

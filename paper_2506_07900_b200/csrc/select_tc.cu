@@ -164,7 +164,9 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   constexpr uint32_t kQBytes = C::kQBytes;
   constexpr uint32_t kMuStageBytes = C::kMuStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the __shared__ array (a uintptr_t round trip
+  // loses the address space: every access would compile to generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sq = smem + SmemLayout::q;
   uint8_t* smu = smem + SmemLayout::mu;
   float* stile = reinterpret_cast<float*>(smem + SmemLayout::stile);
