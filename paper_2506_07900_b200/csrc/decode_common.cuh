@@ -68,7 +68,7 @@ __device__ __forceinline__ float window_mean(const __nv_bfloat16* kg, int d, int
   float x[kP];
 #pragma unroll
   for (int r = 0; r < kP; ++r)   // all loads in flight together
-    x[r] = r < w ? (r0 + r == new_row ? knew : __bfloat162float(kg[(r0 + r) * d + e])) : 0.f;
+    x[r] = r < w ? (r0 + r == new_row ? knew : __bfloat162float(__ldg(&kg[(r0 + r) * d + e]))) : 0.f;
   double acc = (double)x[0];
 #pragma unroll
   for (int r = 1; r < kP; ++r)

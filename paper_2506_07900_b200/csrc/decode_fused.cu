@@ -637,7 +637,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
 #pragma unroll
           for (int i = 0; i < kP + kS; ++i) {
             const int64_t r = row0 + i;
-            x[i] = r < L && r != I.pos ? __bfloat162float(kg[r * kD + d]) : 0.f;
+            x[i] = r < L && r != I.pos ? __bfloat162float(__ldg(&kg[r * kD + d])) : 0.f;   // LDG, not generic
           }
 #pragma unroll
           for (int i = 0; i < kP + kS; ++i)
