@@ -60,6 +60,10 @@ constexpr int kStages = 3;
 #endif
 constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
 constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to kSlots tiles ahead of softmax)
+#ifndef ATT_QK_SPLIT
+#define ATT_QK_SPLIT 0   // 1 measured ~1.5 % slower now that the softmax bounds the kernel
+#endif
+constexpr bool kQkSplit = ATT_QK_SPLIT;  // S^T as two interleaved accumulators (summed by the softmax)
 constexpr int kMaxSel = 80;
 
 constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
@@ -383,8 +387,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
             const uint32_t qoff = (k >> 2) * (kG * 128) + (k & 3) * 32;
-            umma_f16_ss(tmem + slot * 2 * kG + (k & 1) * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk,
-                        k > 1 ? 1u : 0u);
+            if constexpr (kQkSplit)
+              umma_f16_ss(tmem + slot * 2 * kG + (k & 1) * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk,
+                          k > 1 ? 1u : 0u);
+            else
+              umma_f16_ss(tmem + slot * 2 * kG, dk + (off >> 4), dq + (qoff >> 4), idesc_qk, k > 0 ? 1u : 0u);
           }
           umma_commit(k_empty + stage);                // K tile consumed: its stage may refill
           umma_commit(s_full + slot);
@@ -501,11 +508,13 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         float z[kSH], z2[kSH];
         ATT_T0(s4);
         tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + h0, z);
-        tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + kG + h0, z2);
+        if constexpr (kQkSplit) tmem_ld_n<kSH>(tmem + lane_base + sslot * 2 * kG + kG + h0, z2);
         tmem_wait_ld();
         if (warp == 2 && lane == 0) ATT_ADD(15, s4);
+        if constexpr (kQkSplit) {
 #pragma unroll
-        for (int h = 0; h < kSH; ++h) z[h] += z2[h];
+          for (int h = 0; h < kSH; ++h) z[h] += z2[h];
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + sslot);
