@@ -78,7 +78,7 @@ __device__ __forceinline__ void warp_best_after(float& bv, int& bb) {
 // candidates of rq[n_init, local_lo) by (score desc, id asc), forced local
 // blocks; written ascending with -1 padding (select_topk, sparse.py:247-277).
 // Fast path (budget <= 64): threshold T0 = budget-th largest of the lanes' top
-// one (budget <= 32) or top two (budget <= 64) values -- at least `budget`
+// K values (K = 1 / 2 / 4 for budget <= 16 / 32 / 64) -- at least `budget`
 // candidates reach it, so the answer lies in {r >= T0} -- compact that set in
 // id order, rank it exactly, and the ballot-compacted survivors come out
 // ascending.  Iterative order statistics only when the set overflows the list
@@ -92,28 +92,51 @@ __device__ __forceinline__ void warp_select(const float* rq, const UnitSel& u, i
   if (budget >= u.n_free) {
     // dense regime: every candidate is selected (assembled below)
   } else if (budget > 0 && budget <= 64) {
-    float m1 = -1.f, m2 = -1.f;                 // lane's two largest values
+    // each lane keeps its K largest values, K = 1 / 2 / 4 for budget <= 16 /
+    // 32 / 64, so T0 (the budget-th largest of those 32K values) sits about
+    // halfway down their sorted order: a tight threshold, ~budget survivors
+    float m[4] = {-1.f, -1.f, -1.f, -1.f};
+    const int K = budget <= 16 ? 1 : budget <= 32 ? 2 : 4;
     for (int b = lo + lane; b < hi; b += 32) {
       const float a = rq[b];
-      if (a > m1) { m2 = m1; m1 = a; }
-      else if (a > m2) m2 = a;
+      if (a > m[3]) {
+        if (a > m[0]) { m[3] = m[2]; m[2] = m[1]; m[1] = m[0]; m[0] = a; }
+        else if (a > m[1]) { m[3] = m[2]; m[2] = m[1]; m[1] = a; }
+        else if (a > m[2]) { m[3] = m[2]; m[2] = a; }
+        else m[3] = a;
+      }
     }
     float t0;
-    if (budget <= 32) {
-      t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m1, lane), budget - 1);
+    if (K == 1) {
+      t0 = __shfl_sync(0xffffffffu, warp_sort_desc(m[0], lane), budget - 1);
     } else {
-      // budget-th largest of the 64 values {m1, m2}: count values above / at least
-      int gt1 = 0, ge1 = 0, gt2 = 0, ge2 = 0;
+      // budget-th largest of the 32K values: count values above / at least each of mine
+      int gt[4] = {0, 0, 0, 0}, ge[4] = {0, 0, 0, 0};
       for (int x = 0; x < 32; ++x) {
-        const float a = __shfl_sync(0xffffffffu, m1, x), c = __shfl_sync(0xffffffffu, m2, x);
-        gt1 += (a > m1) + (c > m1);
-        ge1 += (a >= m1) + (c >= m1);
-        gt2 += (a > m2) + (c > m2);
-        ge2 += (a >= m2) + (c >= m2);
+        float a[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = __shfl_sync(0xffffffffu, m[j], x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (j < K) {
+              gt[i] += a[j] > m[i];
+              ge[i] += a[j] >= m[i];
+            }
+          }
       }
-      const bool k1 = gt1 < budget && ge1 >= budget, k2 = gt2 < budget && ge2 >= budget;
-      const unsigned b1 = __ballot_sync(0xffffffffu, k1), b2 = __ballot_sync(0xffffffffu, k2);
-      t0 = b1 ? __shfl_sync(0xffffffffu, m1, __ffs(b1) - 1) : __shfl_sync(0xffffffffu, m2, __ffs(b2) - 1);
+      t0 = -1.f;
+      bool done = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool hit = i < K && gt[i] < budget && ge[i] >= budget;
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (!done && bal) {
+          t0 = __shfl_sync(0xffffffffu, m[i], __ffs(bal) - 1);
+          done = true;
+        }
+      }
     }
     int cnt = 0;
     for (int base = lo; base < hi; base += 128) {
