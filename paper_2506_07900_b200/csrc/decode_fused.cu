@@ -1136,6 +1136,10 @@ static int max_active_clusters(int np) {
 // B200 (1 CTA/SM) 8-CTA clusters reach 15 co-resident clusters, 6-CTA ones 22.
 static int choose_cluster(int nseg, int64_t max_len_after) {
   const int64_t nb_max = max_len_after / kM + 1;
+  static const int forced = getenv("INFLLM2_DECODE_P") ? atoi(getenv("INFLLM2_DECODE_P")) : 0;   // diagnostic
+  if (forced >= 3 && forced <= kMaxCl && (nb_max + forced - 1) / forced + 1 <= kMaxPieceBlocks &&
+      max_active_clusters(forced) > 0)
+    return forced;
   int best = 0;
   double best_score = -1.0;
   for (int np = kMaxCl; np >= 3; --np) {
