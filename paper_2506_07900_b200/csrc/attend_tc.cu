@@ -65,6 +65,10 @@ constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to kSlo
 #endif
 constexpr bool kQkSplit = ATT_QK_SPLIT;  // S^T as two interleaved accumulators (summed by the softmax)
 constexpr int kMaxSel = 80;
+// Rows at positions below this attend few keys, where bf16 softmax weights
+// would cost up to 2^-9 |v0 - v1| (two keys): they always carry the weights as
+// bf16 hi + lo (a second PV MMA per k-step on <= 2 tiles per item)
+constexpr int64_t kSplitPBelow = 256;
 
 constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
 constexpr uint32_t kTileBytes = 2 * kHalfBytes;         // 32 KB per K or V tile
@@ -440,7 +444,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 16 * kG, 128);
           const uint32_t ocol = tmem + kColO + ob * 2 * kG;
           const uint32_t acc0 = c > c0 ? 1u : 0u;
-          if (p.p_split) {      // hi -> O_a, lo -> O_b
+          if (p.p_split || pos < kSplitPBelow) {      // hi -> O_a, lo -> O_b
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               if (k < ksteps) {
@@ -494,6 +498,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
+      const bool splitp = p.p_split || pos < kSplitPBelow;
       float mrun[kSH], lsum[kSH], lsx[kSH];     // lsum: weights as used by PV; lsx: unrounded (LSE)
 #pragma unroll
       for (int h = 0; h < kSH; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }
@@ -601,8 +606,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           const float b = ex2(z[h + 1] - mrun[h + 1]);
           const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
           const __nv_bfloat162 lo2 = __floats2bfloat162_rn(a - __low2float(hi2), b - __high2float(hi2));
-          lsum[h] += p.p_split ? a : __low2float(hi2);
-          lsum[h + 1] += p.p_split ? b : __high2float(hi2);
+          lsum[h] += splitp ? a : __low2float(hi2);
+          lsum[h + 1] += splitp ? b : __high2float(hi2);
           lsx[h] += a;
           lsx[h + 1] += b;
           phi[h / 2] = *reinterpret_cast<const uint32_t*>(&hi2);
@@ -613,10 +618,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const uint32_t base = (row >> 3) * (16 * kG) + (row & 7) * 16 + 128 * (h0 >> 3) + 2 * (h0 & 7);
         if constexpr (kSH == 8) {
           *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
-          if (p.p_split) *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
+          if (splitp) *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
         } else {
           *reinterpret_cast<uint2*>(pb + base) = make_uint2(phi[0], phi[1]);
-          if (p.p_split) *reinterpret_cast<uint2*>(pb + kPHalf + base) = make_uint2(plo[0], plo[1]);
+          if (splitp) *reinterpret_cast<uint2*>(pb + kPHalf + base) = make_uint2(plo[0], plo[1]);
         }
         ATT_T0(s5);
         fence_proxy_async_smem();

@@ -103,7 +103,6 @@ def test_approx_tensor_core_vs_verifier_and_oracle(length, topk, shape):
     _check_near_ties(s, s2, q, k, v, geom, 0)
     same = (s == s2).all(-1).repeat_interleave(hq // hkv, dim=1)
     ok = (o - o2).abs() <= 2e-3 + 2e-2 * o2.abs()
-    ok[:64] |= (o - o2).abs()[:64] <= 8e-3 + 2e-2 * o2.abs()[:64]     # few-key rows: bf16 weights, 2^-9|v0 - v1|
     assert bool(ok[same].all())
     # sampled rows vs the oracle (float64 dots)
     rows = np.unique(np.concatenate([[0, 127, 128, length - 1], np.random.default_rng(length).integers(0, length, 24)]))
@@ -136,7 +135,7 @@ def test_approx_full_size_128k():
         _check_near_ties(s, s2, q.float().cpu().numpy(), kn, vn, O.Geometry(top_k=16), start, max_frac=0.02)
         same = (s == s2).all(-1).repeat_interleave(16, dim=1)
         err = (o - o2).abs()
-        assert bool((err <= 8e-3 + 2e-2 * o2.abs())[same].all())
+        assert bool((err <= 2e-3 + 2e-2 * o2.abs())[same].all())
 
 
 def test_approx_is_exact_without_coarse_kernels_and_validates():

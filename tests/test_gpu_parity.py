@@ -306,12 +306,10 @@ def test_full_size_128k_tensor_core_vs_float64_verifier(topk):
         o2, s2, l2 = P.two_stage_attention(q, layer, cfg, start, return_selection=True, return_lse=True,
                                            out_dtype=torch.float32, exact=True)
         assert torch.equal(s, s2), (start, int((s != s2).any(-1).sum()))
-        # bf16 softmax weights: each weight is off by <= 2^-9 relative, so a
-        # row over few keys (row 1 attends 2) can be off by 2^-9*|v0 - v1|,
-        # ~4e-3 for N(0,1) values; long rows average it away (measured <=6e-4)
+        # bf16 softmax weights (hi + lo below position 256, where few keys would
+        # expose the 2^-9 per-weight rounding)
         err = (o - o2).abs()
-        assert bool((err[:64] <= 8e-3 + 2e-2 * o2[:64].abs()).all())
-        assert bool((err[64:] <= 2e-3 + 2e-2 * o2[64:].abs()).all())
+        assert bool((err <= 2e-3 + 2e-2 * o2.abs()).all())
         assert (l - l2).abs().max().item() <= 1e-4
         o3 = P.two_stage_attention(q, layer, cfg, start, out_dtype=torch.float32, split_p=True)
         assert (o3 - o2).abs().max().item() <= 5e-5
