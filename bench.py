@@ -160,10 +160,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # INFLLM2_BENCH_SAME_GPU=1 (+ gloo): every rank on cuda:0, to exercise the
+    # multi-rank logic where only one GPU is reachable; never a measurement
+    if os.environ.get("INFLLM2_BENCH_SAME_GPU") == "1":
+        local = 0
+    backend = os.environ.get("INFLLM2_BENCH_BACKEND", "nccl")
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -573,6 +581,17 @@ def _cpu_worker(payload):
 _CPU_STATE = {}
 
 
+def _cpu_worker_init():
+    # one BLAS thread per worker process: the pool already uses every core, and
+    # numpy's BLAS was initialised before any environment variable could apply
+    # (an oversubscribed pool ran the oracle ~20x slower)
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:
+        pass
+
+
 def cpu_baseline(args, seconds=None, cores=None):
     """Time the oracle port (the reference's algorithm in numpy) on sampled
     query rows of a 128K cache, one process per host core.  Returns tok/s for
@@ -602,7 +621,7 @@ def cpu_baseline(args, seconds=None, cores=None):
     done_rows = 0
     busy = 0.0
     t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
+    with ctx.Pool(cores, initializer=_cpu_worker_init) as pool:
         batches = [(rows[i::rows.size // 2][:2].tolist(), i) for i in range(rows.size // 2)]
         it = pool.imap_unordered(_cpu_worker, batches)
         for dt, n in it:
