@@ -612,8 +612,8 @@ def cpu_baseline(args, seconds=None, cores=None):
     _CPU_STATE.update(k=k, v=v, fine=O.window_means(k, 32, 16), geom=geom)
     cores = cores or os.cpu_count() or 1
     # rows sampled uniformly over positions (cost grows with position)
-    n_rows = max(cores * 2, 16)
-    rows = np.sort(rng.choice(seq, size=n_rows * 64, replace=False))
+    # enough rows that the pool stays busy for the whole time budget
+    rows = np.sort(rng.choice(seq, size=min(seq, max(cores * 1024, 8192)), replace=False))
     q = np.zeros((seq, HQ, D), np.float32)
     q[rows] = rng.standard_normal((rows.size, HQ, D), dtype=np.float32)
     _CPU_STATE["q"] = q
