@@ -173,6 +173,20 @@ int infllm2_forward(const infllm2_geometry* g,
                     void* workspace, size_t workspace_bytes, int32_t flags,
                     infllm2_stream_t stream);
 
+/* Tree-draft verification (specdec.py:565-625, the sparse counterpart of
+ * forward_tree): all n query rows sit at the same `position` (the last cached
+ * row; each draft node sees the whole prefix), so they share the candidate
+ * blocks and forced set; selection per (row, KV group) by the float64 scorer,
+ * stage 2 as infllm2_attend.  The tree rows themselves are attended by the
+ * caller (a tiny masked attention) and merged by log-sum-exp. */
+int infllm2_forward_at(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
+                       int64_t position, int32_t hq, int32_t hkv, int32_t d, const void* k_cache,
+                       const void* v_cache, int64_t cap, int64_t cache_len, const float* fine_means,
+                       int64_t means_cap, int32_t* selection, double* sel_scores, void* out, float* lse,
+                       void* workspace, size_t workspace_bytes, int32_t flags, infllm2_stream_t stream);
+size_t infllm2_forward_at_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hkv, int64_t position,
+                                          int64_t cache_len);
+
 /* ---------------------------------------------------------------- batched decode
  * S sequences (each its own blockized cache of one layer) append one token and
  * attend one query row: BASELINE configs[3].  The reference's decode is the same

@@ -208,6 +208,39 @@ int infllm2_forward(const infllm2_geometry* g, const void* q, int64_t q_row_stri
                         selection, out, lse, flags, stream);
 }
 
+int infllm2_forward_at(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n,
+                       int64_t position, int32_t hq, int32_t hkv, int32_t d, const void* k_cache,
+                       const void* v_cache, int64_t cap, int64_t cache_len, const float* fine_means,
+                       int64_t means_cap, int32_t* selection, double* sel_scores, void* out, float* lse,
+                       void* workspace, size_t workspace_bytes, int32_t flags, infllm2_stream_t stream) {
+  CallShape cs;
+  int rc = make_shape(g, n > 0 ? 1 : 0, position, hq, hkv, d, cache_len, &cs);   // validates position < L
+  if (rc) return rc;
+  if (n == 0) return INFLLM2_OK;
+  cs.n = n;
+  cs.bcast = 1;
+  if (cs.nk_total > means_cap) return INFLLM2_ERR_CAPACITY;
+  if (cache_len > cap) return INFLLM2_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t need = select_simt_workspace(n * hkv, cs.nk_total, cs.nb_max);
+  if (workspace == nullptr || workspace_bytes < need) return INFLLM2_ERR_WORKSPACE;
+  rc = cuda_status(launch_select_simt(*g, cs, q, q_row_stride, fine_means, means_cap, selection, sel_scores,
+                                      workspace, workspace_bytes, st));
+  if (rc) return rc;
+  const int out_f32 = (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0;
+  if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_attend_supported(*g, cs))
+    return cuda_status(launch_attend_tc(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32,
+                                        lse, (flags & INFLLM2_FLAG_P_SPLIT) ? 1 : 0, st));
+  return cuda_status(launch_attend_simt(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32,
+                                        lse, st));
+}
+
+size_t infllm2_forward_at_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hkv, int64_t position,
+                                          int64_t cache_len) {
+  if (infllm2_validate_geometry(g) || n <= 0 || hkv <= 0) return 0;
+  return select_simt_workspace(n * hkv, cache_len / g->kernel_stride, position / g->block_size + 1);
+}
+
 size_t infllm2_decode_table_bytes(int32_t n_seq) { return n_seq > 0 ? decode_table_bytes(n_seq) : 0; }
 
 int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq, int32_t hkv,

@@ -30,6 +30,7 @@ struct AttendArgs {
   void* out;
   int out_f32;
   float* lse;
+  int bcast;             // every row at position start
 };
 
 __global__ void __launch_bounds__(kThreads) attend_simt_kernel(AttendArgs a) {
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(kThreads) attend_simt_kernel(AttendArgs a) {
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const int64_t i = item / a.hkv;
     const int grp = (int)(item - i * a.hkv);
-    const int64_t pos = a.start + i;
+    const int64_t pos = a.bcast ? a.start : a.start + i;
     const int32_t* sel = a.selection + item * a.max_sel;
     for (int idx = tid; idx < G * D; idx += kThreads) {
       const int h = idx / D, e = idx - h * D;
@@ -171,6 +172,7 @@ cudaError_t launch_attend_simt(const infllm2_geometry& g, const CallShape& cs, c
   a.out = out;
   a.out_f32 = out_f32;
   a.lse = lse;
+  a.bcast = cs.bcast;
   const int64_t items = cs.n * cs.hkv;
   const int grid = (int)(items < kNumSMs * 4 ? items : kNumSMs * 4);
   if (grid < 1) return cudaSuccess;

@@ -126,6 +126,7 @@ struct Params {
   const CUtensorMap* kv_maps;
   int map_stride;
   const int64_t* seq_len;
+  int bcast;          // prefill rows all at position start (tree-draft nodes)
   // split-K (decode): each work unit is (item, part) covering tiles
   // [part*split, (part+1)*split); partial O^T (unnormalised), max and row sum go
   // to part_o / part_ml and attend_combine_kernel merges them.  split == 0: off.
@@ -162,7 +163,7 @@ __device__ __forceinline__ void unit_of(const Params& p, int64_t w, int64_t* ite
 __device__ __forceinline__ int64_t item_pos(const Params& p, int64_t i) {
   // decode: seq_len holds the length before this step's append = the new
   // token's position
-  return p.seq_len ? p.seq_len[i] : p.start + i;
+  return p.seq_len ? p.seq_len[i] : p.bcast ? p.start : p.start + i;
 }
 
 // The item's selection row, read once per warp with lane-parallel loads
@@ -812,6 +813,7 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   p.kv_maps = kv_maps;
   p.map_stride = map_stride;
   p.seq_len = seq_len;
+  p.bcast = 0;
   // split-K: one 2-block tile per CTA so n_seq*hkv*10 CTAs share the gather
   p.split = split_ws ? 1 : 0;
   p.p_split = 1;
@@ -928,6 +930,7 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.kv_maps = nullptr;
   p.map_stride = 0;
   p.seq_len = nullptr;
+  p.bcast = cs.bcast;
   p.split = 0;
   p.p_split = p_split;
   p.group_major = group_major_enabled();

@@ -25,6 +25,7 @@ struct CallShape {
   int32_t max_sel;
   int64_t nk_total;     // cache_len // s
   int64_t nb_max;       // candidate blocks of the last row
+  int bcast = 0;        // 1: every row sits at position `start` (tree-draft nodes over a prefix)
 };
 
 // First kernel window whose rows change when the cache boundary moves

@@ -39,6 +39,7 @@ struct SelectArgs {
   int64_t ws_per_cta;  // doubles
   const float* coarse;   // approx-LSE mode (nullptr: exact softmax)
   int64_t coarse_cap, nc_total;
+  int bcast;             // every row at position start
 };
 
 __device__ __forceinline__ bool better(double ra, int64_t ba, double rb, int64_t bb) {
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) select_simt_kernel(SelectArgs a) {
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const int64_t i = item / a.hkv;
     const int grp = (int)(item - i * a.hkv);
-    const int64_t pos = a.start + i;
+    const int64_t pos = a.bcast ? a.start : a.start + i;
     const int64_t n_cand = pos / m + 1;
     int64_t nk_t = pos / s + 1;
     if (nk_t > a.nk_total) nk_t = a.nk_total;
@@ -252,6 +253,7 @@ cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, c
                                int32_t* selection, double* sel_scores, void* ws, size_t ws_bytes,
                                cudaStream_t stream, const CoarseArgs* coarse) {
   SelectArgs a;
+  a.bcast = cs.bcast;
   a.coarse = coarse ? coarse->means : nullptr;
   a.coarse_cap = coarse ? coarse->cap : 0;
   a.nc_total = coarse ? coarse->nc_total : 0;

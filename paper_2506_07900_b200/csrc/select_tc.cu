@@ -626,7 +626,7 @@ static bool tc_select_shape(const CallShape& cs, int* kq) {
 }
 
 bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool have_split_means) {
-  if (!have_split_means || !tc_kernels_enabled()) return false;
+  if (!have_split_means || !tc_kernels_enabled() || cs.bcast) return false;   // units need consecutive rows
   int kq;
   if (!tc_select_shape(cs, &kq)) return false;
   if (g.kernel_stride != 16 || g.kernel_size != 32) return false;

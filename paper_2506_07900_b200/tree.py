@@ -16,19 +16,22 @@ Definition (sparse backend): node i's attention is the log-sum-exp merge of
       position ``base - 1`` (it sees every cached row), and
   (b) dense attention over its ancestor-or-self tree rows;
 which is exactly dense attention over prefix ∪ ancestors when (a) selects every
-block.  (a) runs ``two_stage_attention`` once per node (a tree is ≤ a few dozen
-nodes); (b) is a tiny masked float64 attention.
+block.  (a) is one ``infllm2_forward_at`` call for all nodes (every row at the
+same position: shared candidates and forced set; float64 scorer, tensor-core
+stage 2); (b) is a tiny masked float64 attention.
 """
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
 
 import numpy as np
 import torch
 
+from . import _lib
 from .errors import ValidationError
-from .sparse import BlockizedLayerCache, SparseAttentionConfig, two_stage_attention
+from .sparse import BlockizedLayerCache, SparseAttentionConfig, _ptr, _stream, _workspace
 
 
 @dataclasses.dataclass
@@ -101,20 +104,29 @@ def tree_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: SparseAt
     mask.validate()
     dev = layer.device
     base = layer.length
-    outs, lses, sels = [], [], []
-    for i in range(n):
-        o, s, l = two_stage_attention(q[i:i + 1], layer, config, base - 1, return_selection=True, return_lse=True,
-                                      out_dtype=torch.float32, exact=exact, split_p=split_p)
-        outs.append(o)
-        lses.append(l)
-        sels.append(s)
-    o_p = torch.cat(outs).double()
-    l_p = torch.cat(lses).double()
+    hq, d = q.shape[1], q.shape[2]
+    hkv = layer.n_kv_heads
+    if hq % hkv or d != layer.head_dim or k_tree.shape[1:] != (hkv, d):
+        raise ValidationError("tree node heads / head_dim disagree with the cache")
+    qb = q.to(device=dev, dtype=torch.bfloat16).contiguous()
+    geom = config.geometry()
+    sel = torch.empty((n, hkv, config.max_selected), dtype=torch.int32, device=dev)
+    o_p = torch.empty((n, hq, d), dtype=torch.float32, device=dev)
+    l_p = torch.empty((n, hq), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    kc, vc, cap, fine, _, _, mcap = layer._device_args()
+    ws = _workspace(dev, lib.infllm2_forward_at_workspace_bytes(ctypes.byref(geom), n, hkv, base - 1, base))
+    flags = (_lib.FLAG_OUT_F32 | (_lib.FLAG_EXACT_SIMT if exact else 0) | (_lib.FLAG_P_SPLIT if split_p else 0))
+    _lib.check(lib.infllm2_forward_at(ctypes.byref(geom), _ptr(qb), qb.stride(0), n, base - 1, hq, hkv, d, _ptr(kc),
+                                      _ptr(vc), cap, base, _ptr(fine), mcap, _ptr(sel), None, _ptr(o_p), _ptr(l_p),
+                                      _ptr(ws), ws.numel(), flags, _stream(dev)), "tree_attention")
+    o_p = o_p.double()
+    l_p = l_p.double()
     vis = torch.as_tensor(mask.to_dense(), device=dev)
     o_t, l_t = _tree_part(q.to(dev), k_tree.to(dev), v_tree.to(dev), vis)
     m = torch.maximum(l_p, l_t)
     wp, wt = torch.exp(l_p - m), torch.exp(l_t - m)
     out = ((o_p * wp[..., None] + o_t * wt[..., None]) / (wp + wt)[..., None]).float()
     if return_selection:
-        return out, torch.cat(sels)
+        return out, sel
     return out
