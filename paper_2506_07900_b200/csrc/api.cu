@@ -138,6 +138,10 @@ int infllm2_select(const infllm2_geometry* g, const void* q, int64_t q_row_strid
   if (n == 0) return INFLLM2_OK;
   if (cs.nk_total > means_cap) return INFLLM2_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
+  // below the sparsity threshold every row selects every block (the dense
+  // path of configs[4]): no scoring, unless the caller wants the scores
+  if (sel_scores == nullptr && select_dense_regime(*g, cs))
+    return cuda_status(launch_select_dense(*g, cs, selection, st));
   if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_select_supported(*g, cs, means_hi != nullptr)) {
     return cuda_status(launch_select_tc(*g, cs, q, q_row_stride, fine_means, means_hi, means_lo, means_cap,
                                         selection, sel_scores, workspace, workspace_bytes, st));
@@ -164,6 +168,8 @@ int infllm2_select_approx(const infllm2_geometry* g, const void* q, int64_t q_ro
   CoarseArgs ca{coarse_means, coarse_hi, coarse_lo, coarse_cap, nc_total};
   const CoarseArgs* cp = nc_total > 0 ? &ca : nullptr;      // no coarse kernel yet: the exact softmax
   cudaStream_t st = (cudaStream_t)stream;
+  if (sel_scores == nullptr && select_dense_regime(*g, cs))   // every block selected: the LSE cannot matter
+    return cuda_status(launch_select_dense(*g, cs, selection, st));
   if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_select_supported(*g, cs, means_hi != nullptr) &&
       (cp == nullptr || coarse_hi != nullptr)) {
     return cuda_status(launch_select_tc(*g, cs, q, q_row_stride, fine_means, means_hi, means_lo, means_cap,

@@ -69,6 +69,9 @@ struct CoarseArgs {
   int64_t nc_total;        // cache_len // s_c (>= 1)
 };
 size_t select_simt_workspace(int64_t items, int64_t nk_total, int64_t nb_max);
+bool select_dense_regime(const infllm2_geometry& g, const CallShape& cs);
+cudaError_t launch_select_dense(const infllm2_geometry& g, const CallShape& cs, int32_t* selection,
+                                cudaStream_t stream);
 cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
                                int64_t q_row_stride, const float* means, int64_t means_cap,
                                int32_t* selection, double* sel_scores, void* ws, size_t ws_bytes,

@@ -248,6 +248,51 @@ size_t select_simt_workspace(int64_t items, int64_t nk_total, int64_t nb_max) {
   return (size_t)grid * (size_t)(nk_total + nb_max) * sizeof(double);
 }
 
+// Dense regime (every row's budget covers all its non-forced candidates,
+// select_topk sparse.py:268-276): the selection is every candidate block
+// 0..t//m, ascending -- no scoring needed.  One thread per (row, group, slot).
+__global__ void select_dense_kernel(int64_t n, int64_t start, int hkv, int m, int max_sel, int bcast,
+                                    int32_t* selection) {
+  const int64_t total = n * hkv * max_sel;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / ((int64_t)hkv * max_sel);
+    const int slot = (int)(x % max_sel);
+    const int64_t pos = bcast ? start : start + i;
+    const int64_t n_cand = pos / m + 1;
+    selection[x] = slot < n_cand ? slot : -1;
+  }
+}
+
+bool select_dense_regime(const infllm2_geometry& g, const CallShape& cs) {
+  // the last row has the most candidates; budget never grows with position
+  const int64_t t = cs.bcast ? cs.start : cs.start + cs.n - 1;
+  const int64_t qb = t / g.block_size, n_cand = qb + 1;
+  const int64_t n_init = g.n_init_blocks < n_cand ? g.n_init_blocks : n_cand;
+  int64_t local_lo = qb + 1;
+  if (g.n_local_blocks > 0) {
+    local_lo = qb - g.n_local_blocks + 1;
+    if (local_lo < 0) local_lo = 0;
+    if (local_lo < n_init) local_lo = n_init;
+  }
+  const int64_t n_forced = n_init + (qb + 1 - local_lo);
+  int64_t budget = g.top_k;
+  if (g.forced_consume_budget) budget = g.top_k - n_forced > 0 ? g.top_k - n_forced : 0;
+  if (cs.max_sel < n_cand) return false;      // the output row could not hold every block
+  return budget >= n_cand - n_forced;
+}
+
+cudaError_t launch_select_dense(const infllm2_geometry& g, const CallShape& cs, int32_t* selection,
+                                cudaStream_t stream) {
+  const int64_t total = cs.n * cs.hkv * cs.max_sel;
+  const int threads = 256;
+  const int64_t blocks64 = (total + threads - 1) / threads;
+  const int blocks = (int)(blocks64 < 4 * kNumSMs ? blocks64 : 4 * kNumSMs);
+  count_launch();
+  select_dense_kernel<<<blocks, threads, 0, stream>>>(cs.n, cs.start, cs.hkv, g.block_size, cs.max_sel, cs.bcast,
+                                                       selection);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select_simt(const infllm2_geometry& g, const CallShape& cs, const void* q,
                                int64_t q_row_stride, const float* means, int64_t means_cap,
                                int32_t* selection, double* sel_scores, void* ws, size_t ws_bytes,

@@ -313,3 +313,22 @@ def test_full_size_128k_tensor_core_vs_float64_verifier(topk):
         assert (l - l2).abs().max().item() <= 1e-4
         o3 = P.two_stage_attention(q, layer, cfg, start, out_dtype=torch.float32, split_p=True)
         assert (o3 - o2).abs().max().item() <= 5e-5
+
+
+def test_dense_regime_shortcut_equals_scored_selection():
+    """Below the sparsity threshold the selection is written without scoring
+    (every candidate block); it must equal the scored selection (requesting
+    the traces forces the scorer)."""
+    cfg = P.SparseAttentionConfig(top_k=64)
+    q, k, v = make_qkv(4040, 4096, 4096, 32, 2, 128)          # 64 blocks - 3 forced <= 64: dense
+    layer = P.BlockizedLayerCache(2, 128, cfg)
+    layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd = torch.from_numpy(q).cuda()
+    o1, s1 = P.two_stage_attention(qd, layer, cfg, 0, return_selection=True, out_dtype=torch.float32)
+    traces = []
+    o2, s2 = P.two_stage_attention(qd[-96:], layer, cfg, 4096 - 96, return_selection=True, out_dtype=torch.float32,
+                                   traces=traces)
+    assert torch.equal(s1[-96:], s2)
+    assert torch.equal(o1[-96:], o2)
+    nb = torch.arange(64, device="cuda")
+    assert torch.equal(s1[-1, 0, :64], nb.int())
