@@ -173,6 +173,18 @@ int infllm2_forward(const infllm2_geometry* g,
                     void* workspace, size_t workspace_bytes, int32_t flags,
                     infllm2_stream_t stream);
 
+/* Dense causal GQA attention over the cache (row i at position start + i sees
+ * rows [0, start + i]): the path below the sparsity threshold (every block
+ * selected) and the dense backend (model.py:194-253), on the tensor cores with
+ * 8 query rows x 16 heads per MMA tile.  G = 16, D = 128 only
+ * (INFLLM2_ERR_UNSUPPORTED otherwise).  out (n, HQ, D), lse (n, HQ) or NULL. */
+int infllm2_dense_attend(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n, int64_t start,
+                         int32_t hq, int32_t hkv, int32_t d, const void* k_cache, const void* v_cache, int64_t cap,
+                         int64_t cache_len, void* out, float* lse, int32_t flags, infllm2_stream_t stream);
+/* 1 when every row of the call selects every candidate block (select_topk's
+ * budget covers all non-forced candidates of the last row, sparse.py:268). */
+int infllm2_dense_regime(const infllm2_geometry* g, int64_t n, int64_t start, int64_t cache_len);
+
 /* Tree-draft verification (specdec.py:565-625, the sparse counterpart of
  * forward_tree): all n query rows sit at the same `position` (the last cached
  * row; each draft node sees the whole prefix), so they share the candidate

@@ -72,6 +72,9 @@ SIGNATURES.update({
                                           c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
                                           c_i32, c_vp]),
     "infllm2_forward_at_workspace_bytes": (c_sz, [ctypes.POINTER(Geometry), c_i64, c_i32, c_i64, c_i64]),
+    "infllm2_dense_attend": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,
+                                            c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i32, c_vp]),
+    "infllm2_dense_regime": (ctypes.c_int, [ctypes.POINTER(Geometry), c_i64, c_i64, c_i64]),
     "infllm2_decode_table_bytes": (c_sz, [c_i32]),
     "infllm2_decode_table_build": (ctypes.c_int, [ctypes.POINTER(SeqDesc), ctypes.POINTER(c_i64), c_i32, c_i32,
                                                   c_i32, c_vp, c_vp]),

@@ -247,6 +247,25 @@ size_t infllm2_forward_at_workspace_bytes(const infllm2_geometry* g, int64_t n, 
   return select_simt_workspace(n * hkv, cache_len / g->kernel_stride, position / g->block_size + 1);
 }
 
+int infllm2_dense_attend(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n, int64_t start,
+                         int32_t hq, int32_t hkv, int32_t d, const void* k_cache, const void* v_cache, int64_t cap,
+                         int64_t cache_len, void* out, float* lse, int32_t flags, infllm2_stream_t stream) {
+  CallShape cs;
+  int rc = make_shape(g, n, start, hq, hkv, d, cache_len, &cs);
+  if (rc) return rc;
+  if (cache_len > cap) return INFLLM2_ERR_CAPACITY;
+  if (n == 0) return INFLLM2_OK;
+  if (!dense_tc_supported(cs)) return INFLLM2_ERR_UNSUPPORTED;
+  return cuda_status(launch_dense_tc(cs, q, q_row_stride, k_cache, v_cache, cap, out,
+                                     (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0, lse, (cudaStream_t)stream));
+}
+
+int infllm2_dense_regime(const infllm2_geometry* g, int64_t n, int64_t start, int64_t cache_len) {
+  CallShape cs;
+  if (make_shape(g, n, start, 32, 2, 128, cache_len, &cs) || n == 0) return 0;
+  return select_dense_regime(*g, cs) ? 1 : 0;
+}
+
 size_t infllm2_decode_table_bytes(int32_t n_seq) { return n_seq > 0 ? decode_table_bytes(n_seq) : 0; }
 
 int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq, int32_t hkv,

@@ -13,6 +13,10 @@ cudaError_t launch_select_tc(const infllm2_geometry& g, const CallShape& cs, con
                              double* sel_scores, void* ws, size_t ws_bytes, cudaStream_t stream,
                              const CoarseArgs* coarse = nullptr);
 bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs);
+bool dense_tc_supported(const CallShape& cs);
+cudaError_t launch_dense_tc(const CallShape& cs, const void* q, int64_t q_row_stride, const void* k_cache,
+                            const void* v_cache, int64_t cap, void* out, int out_f32, float* lse,
+                            cudaStream_t stream);
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
                              int64_t q_row_stride, const void* k_cache, const void* v_cache,
                              int64_t cap, const int32_t* selection, void* out, int out_f32,

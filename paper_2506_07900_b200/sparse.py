@@ -435,7 +435,21 @@ def two_stage_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: Spa
     kc, vc, cap, fine, hi, lo, mcap = layer._device_args()
     ws_bytes = lib.infllm2_select_workspace_bytes(ctypes.byref(geom), n, hq, hkv, d, layer.length, flags)
     ws = _workspace(dev, ws_bytes)
-    if n and lse == "approx":
+    # below the sparsity threshold every row selects every block: dense causal
+    # attention on the tensor cores (8 query rows x 16 heads per MMA tile)
+    dense = (n > 0 and not exact and not split_p and hq // hkv == 16 and d == 128
+             and lib.infllm2_dense_regime(ctypes.byref(geom), n, start, layer.length) == 1)
+    if dense:
+        st = _stream(dev)
+        if return_selection or stats is not None or traces is not None:
+            _lib.check(lib.infllm2_select(
+                ctypes.byref(geom), _ptr(qb), qb.stride(0), n, start, hq, hkv, d, _ptr(fine), _ptr(hi), _ptr(lo),
+                mcap, layer.length, _ptr(sel), _ptr(sel_scores), _ptr(ws), ws.numel(), flags, st),
+                "two_stage_attention")
+        _lib.check(lib.infllm2_dense_attend(
+            ctypes.byref(geom), _ptr(qb), qb.stride(0), n, start, hq, hkv, d, _ptr(kc), _ptr(vc), cap, layer.length,
+            _ptr(out), _ptr(lse_out), flags, st), "two_stage_attention")
+    elif n and lse == "approx":
         layer._coarse_split()
         st = _stream(dev)
         _lib.check(lib.infllm2_select_approx(

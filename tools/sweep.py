@@ -43,7 +43,13 @@ def time_layer(hq, hkv, d, L, k, reps=3, attend_too=True):
         _lib.check(lib.infllm2_select(ctypes.byref(geom), _ptr(q), hq * d, L, 0, hq, hkv, d, _ptr(fine), _ptr(hi),
                                       _ptr(lo), mcap, L, _ptr(sel), None, _ptr(ws), ws.numel(), 0, st), "select")
 
+    dense_path = hq // hkv == 16 and d == 128 and lib.infllm2_dense_regime(ctypes.byref(geom), L, 0, L) == 1
+
     def attend():
+        if dense_path:      # what two_stage_attention runs below the sparsity threshold
+            _lib.check(lib.infllm2_dense_attend(ctypes.byref(geom), _ptr(q), hq * d, L, 0, hq, hkv, d, _ptr(kc),
+                                                _ptr(vc), cap, L, _ptr(out), None, 0, st), "dense attend")
+            return
         _lib.check(lib.infllm2_attend(ctypes.byref(geom), _ptr(q), hq * d, L, 0, hq, hkv, d, _ptr(kc), _ptr(vc), cap, L,
                                       _ptr(sel), _ptr(out), None, 0, st), "attend")
 
