@@ -45,9 +45,9 @@ constexpr int kD = 128;
 // [6] softmax P fence+arrive [7] softmax warp 2 total [8] its s_full wait
 // [9] vote barrier [10] need path [11] p_empty wait [12] K TMA k_empty wait
 // [13] V TMA v_empty wait [14] K TMA total [15] softmax S TMEM load + wait
-__device__ long long g_att_cyc[160][16];
+__device__ long long g_att_cyc[160][24];
 #define ATT_T0(v) long long v = clock64()
-#define ATT_ADD(slot, v) (g_att_cyc[blockIdx.x][slot] += clock64() - (v))
+#define ATT_ADD(slot, v) (att_acc[slot] += clock64() - (v))   // registers; flushed once at kernel end
 #else
 #define ATT_T0(v)
 #define ATT_ADD(slot, v)
@@ -267,6 +267,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ATT_T0(t_kernel);
+#ifdef ATT_PROFILE
+  long long att_acc[24];
+#pragma unroll
+  for (int i = 0; i < 24; ++i) att_acc[i] = 0;
+#endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::kKStages; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
     for (int i = 0; i < C::kVStages; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
@@ -338,7 +343,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (lane == 0) {
           ATT_T0(t0w);
           mbar_wait(ring_empty + stage, phase ^ 1);
-          ATT_ADD(is_k ? 12 : 13, t0w);
+          if (is_k) ATT_ADD(12, t0w); else ATT_ADD(13, t0w);
           mbar_arrive_expect_tx(ring_full + stage, nt * C::kDH * (kM * 128));
           uint8_t* dst = ring + stage * kTileBytes;
           for (int x = 0; x < nt; ++x) {
@@ -493,7 +498,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       int grp;
       unit_of(p, w, &item, &part, &i, &grp);
       const int64_t pos = item_pos(p, i);
+      ATT_T0(s16);
       const SelRow sr = pf.take(p, w, items, pos, lane);
+      if (warp == 2 && lane == 0) ATT_ADD(16, s16);
       const int nb = sr.nb;
       int c0, c1;
       tile_range(p, part, (nb + 1) / 2, &c0, &c1);
@@ -524,6 +531,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + sslot);
+        ATT_T0(s19);
         const int x = row >> 6;
         const int b0 = sr.get(2 * c), b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         bool valid = (2 * c + x) < nb;
@@ -534,6 +542,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         // The max is per head, so only the four warps of a head half vote (one
         // 128-thread barrier per tile; votes double-buffered by tile parity: a
         // warp cannot overwrite a slot before the others passed the next barrier)
+        if (warp == 2 && lane == 0) ATT_ADD(19, s19);
         bool need = (c == c0);
         if (c > c0) {
           bool over = false;
@@ -600,6 +609,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         // weights, so O = sum P~ V / sum P~ stays a convex combination (error
         // ~2^-9 |V| / sqrt(rows)).  p_split: P also as a bf16 lo part (second
         // PV MMA), ~16-bit weights, for callers that want 1e-5 outputs.
+        ATT_T0(s20);
         uint32_t phi[kSH / 2], plo[kSH / 2];
 #pragma unroll
         for (int h = 0; h < kSH; h += 2) {
@@ -624,6 +634,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           *reinterpret_cast<uint2*>(pb + base) = make_uint2(phi[0], phi[1]);
           if (splitp) *reinterpret_cast<uint2*>(pb + kPHalf + base) = make_uint2(plo[0], plo[1]);
         }
+        if (warp == 2 && lane == 0) ATT_ADD(20, s20);
         ATT_T0(s5);
         fence_proxy_async_smem();
         __syncwarp();
@@ -633,7 +644,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       if (warp == 2 && lane == 0) ATT_ADD(1, sloop);
       // per-head row sums -> stats for the epilogue
+      ATT_T0(s17);
       mbar_wait(st_empty + ob, ((it >> 1) & 1) ^ 1);
+      if (warp == 2 && lane == 0) ATT_ADD(17, s17);
+      ATT_T0(s18);
       float* st = stats + ob * 9 * 16;
       {
         const float v = warp_reduce_n<kSH>(lsum, lane, [](float a, float b) { return a + b; });
@@ -651,6 +665,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(st_full + ob);
+      if (warp == 2 && lane == 0) ATT_ADD(18, s18);
       ++it;
     }
   } else {
@@ -736,6 +751,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   if (lane == 0 && warp == 10) ATT_ADD(3, t_kernel);
   if (lane == 0 && warp == 2) ATT_ADD(7, t_kernel);
   if (lane == 0 && warp == 0) ATT_ADD(14, t_kernel);
+#ifdef ATT_PROFILE
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 24; ++i)
+      if (att_acc[i]) atomicAdd(reinterpret_cast<unsigned long long*>(&g_att_cyc[blockIdx.x][i]), (unsigned long long)att_acc[i]);
+#endif
 #endif
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
