@@ -14,11 +14,17 @@
 //     lo part (second PV MMA) so few-key rows stay exact to ~1e-5
 //   O^T [128 d x 128 (q,h)]  += V_tile^T (MN-major) . P^T            (TMEM)
 //
-// Warp roles (8 warps): 0 = TMA producer (Q per item, K + V per tile, two
-// stages), 1 = TMEM alloc + MMA issuer, 4..7 = softmax, then epilogue (thread
-// = d lane of O^T: divide by the row sums, store; thread = row: LSE).
+// Warp roles (12 warps): 0 = TMA producer (Q per item, K + V per tile, two
+// stages), 1 = TMEM alloc + MMA issuer, 4..11 = softmax, then epilogue.  Warps
+// w and w + 4 share TMEM lane quadrant w % 4: thread = (q,h) row r, the first
+// four take keys 0..63 of every tile, the others keys 64..127 (both take the
+// max over the whole row; one OR-reducing barrier per tile is the rescale
+// vote); in the epilogue thread = d lane of O^T over its half of the
+// (q,h) columns (divide by the row sums, store) and thread = row (LSE).
 #include <float.h>
 #include <stdlib.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -36,7 +42,7 @@ constexpr int kG = 16;
 constexpr int kD = 128;
 constexpr int kQR = 8;                        // query rows per item (8 x 16 heads = 128 MMA rows)
 constexpr int kKT = 128;                      // keys per tile
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int64_t kSplitBelow = 256;          // items starting below this position carry P lo too
 constexpr uint32_t kHalf = 128 * 128;         // 16 KB: 128 rows x 64 bf16 (one 128-B swizzle half)
 constexpr uint32_t kTile = 2 * kHalf;         // 32 KB: 128 rows x 128 bf16
@@ -46,9 +52,9 @@ struct Smem {
   static constexpr uint32_t kv = q + kTile;                 // [2 stages][K, V] 128 KB
   static constexpr uint32_t p = kv + 4 * kTile;             // [2] P tiles (hi; the lo part uses the other) 64 KB
   static constexpr uint32_t corr = p + 2 * kTile;           // [128] per-row rescale factors
-  static constexpr uint32_t stats = corr + 128 * 4;         // [128] row sums (the epilogue lanes need all)
-  static constexpr uint32_t red = stats + 128 * 4;          // [2][4 warps] votes
-  static constexpr uint32_t bars = red + 8 * 4;
+  static constexpr uint32_t bars = corr + 128 * 4;
+  // the epilogue's row sums [2 halves][128] l, [2][128] l exact live in the
+  // P region (idle once O is complete)
   static constexpr uint32_t total = bars + 18 * 8;
 };
 static_assert(Smem::total + 1024 <= 232448, "dense attention shared memory");
@@ -87,8 +93,7 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   uint64_t* o_empty = bars + 15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   float* corr = reinterpret_cast<float*>(smem + Smem::corr);
-  float* st_l = reinterpret_cast<float*>(smem + Smem::stats);
-  float* vote = reinterpret_cast<float*>(smem + Smem::red);
+  float* st_l = reinterpret_cast<float*>(smem + Smem::p);          // [2][128], then l exact [2][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -98,12 +103,12 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
       mbar_init(s_full + i, 1);
-      mbar_init(s_empty + i, 4);
-      mbar_init(p_full + i, 4);
+      mbar_init(s_empty + i, 8);
+      mbar_init(p_full + i, 8);
       mbar_init(p_empty + i, 1);
     }
     mbar_init(o_full, 1);
-    mbar_init(o_empty, 4);
+    mbar_init(o_empty, 8);
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
@@ -217,11 +222,12 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
     const int quad = warp & 3;
+    const int hf = (warp - 4) >> 2;                   // key half of every tile
     const int r = quad * 32 + lane;                   // S row (q, h) == O^T lane d
     const int qr = r >> 4, h = r & 15;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const float c2 = 1.4426950408889634f / sqrtf((float)kD);
-    uint32_t tcount = 0, pcount = 0, vcnt = 0;
+    uint32_t tcount = 0, pcount = 0;
     uint32_t p_ph[2] = {0, 0};
     int it = 0;
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x, ++it) {
@@ -240,30 +246,31 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         mbar_wait(s_full + slot, (tcount >> 1) & 1);
         tc_fence_after();
         const int64_t key0 = (int64_t)t * kKT;
-        // two sweeps over the 128 scores in TMEM (max, then weights): 32
-        // registers of scores instead of 128
-        const int nvalid = (int)(pos - key0 + 1 < kKT ? pos - key0 + 1 : kKT);   // keys <= pos in this tile
+        // keys <= pos in this tile, counted from this half's first key
+        const int nvalid = (int)(pos - key0 + 1 < kKT ? pos - key0 + 1 : kKT) - hf * 64;
+        const uint32_t scol = tmem + lane_base + slot * 128 + hf * 64;
+        // both halves take the max over the whole row (identical values, no
+        // exchange); the barrier ORs the rescale vote: exact max on the first
+        // tile, later a rescale only when some row's score exceeds its max by 8
+        // (tiles wholly below the item's first row need no causal mask: the
+        // max is taken on the raw scores, then scaled, c2 > 0)
+        const bool full = key0 + kKT - 1 <= p.start + i0;
         float tmax = -INFINITY;
 #pragma unroll 1
         for (int c = 0; c < kKT; c += 32) {
           float z[32];
           tmem_ld32(tmem + lane_base + slot * 128 + c, z);
           tmem_wait_ld();
+          if (full) {
 #pragma unroll
-          for (int x = 0; x < 32; ++x) tmax = fmaxf(tmax, c + x < nvalid ? z[x] * c2 : -INFINITY);
+            for (int x = 0; x < 32; x += 2) tmax = fmax3(tmax, z[x], z[x + 1]);
+          } else {
+#pragma unroll
+            for (int x = 0; x < 32; ++x) tmax = fmaxf(tmax, c + x < nvalid + hf * 64 ? z[x] : -INFINITY);
+          }
         }
-        // running max: exact on the first tile; later a rescale only when some
-        // row's score exceeds its max by 8 (all 128 rows vote: O^T columns
-        // are rescaled lane-wise by every thread)
-        bool need = t == 0;
-        if (t > 0) {
-          const unsigned any = __ballot_sync(0xffffffffu, tmax > mrun + 8.f);
-          float* vt = vote + (vcnt & 1) * 4;
-          ++vcnt;
-          if (lane == 0) vt[quad] = any ? 1.f : 0.f;
-          named_bar_sync(1, 128);
-          need = (vt[0] + vt[1] + vt[2] + vt[3]) > 0.f;
-        }
+        tmax *= c2;
+        const bool need = named_bar_or(1, 256, t == 0 || tmax > mrun + 8.f);
         if (need) {
           const float mnew = fmaxf(mrun, tmax);
           const float cf = mrun == -INFINITY ? 1.f : ex2(mrun - mnew);
@@ -271,14 +278,15 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           lsx *= mrun == -INFINITY ? 0.f : cf;
           mrun = mnew;
           if (t > 0) {
-            corr[r] = cf;
+            if (hf == 0) corr[r] = cf;
             // O^T holds PV(t-1) once p_empty of its buffer completes again
             const int pb = (int)((pcount - 1) & 1);
             mbar_wait(p_empty + pb, p_ph[pb] ^ 1);
-            named_bar_sync(1, 128);
+            named_bar_sync(1, 256);
             tc_fence_after();
+            // this thread's O^T lane over its half of the (q,h) columns
 #pragma unroll 1
-            for (int c = 0; c < 128; c += 32) {
+            for (int c = hf * 64; c < hf * 64 + 64; c += 32) {
               float o[32];
               tmem_ld32(tmem + lane_base + kColO + c, o);
               tmem_wait_ld();
@@ -289,11 +297,11 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             }
             tmem_wait_st();
             tc_fence_before();
-            named_bar_sync(1, 128);
           }
         }
         // P = 2^(z - M) as bf16 (hi; lo into the second buffer for split items),
-        // K-major with the 128-B swizzle: 16-byte chunk c of row r at c ^ (r & 7)
+        // K-major with the 128-B swizzle: 16-byte chunk c of row r at c ^ (r & 7);
+        // key half hf is swizzle half hf of the tile
         const int pb = split ? 0 : (int)(pcount & 1);
         mbar_wait(p_empty + (pcount & 1), p_ph[pcount & 1] ^ 1);   // PV(tile - 2) done
         p_ph[pcount & 1] ^= 1;
@@ -303,34 +311,68 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           const int ob = (int)((pcount - 1) & 1);
           mbar_wait(p_empty + ob, p_ph[ob] ^ 1);
         }
-        uint8_t* ph = smem + Smem::p + pb * kTile;
-        uint8_t* pl = smem + Smem::p + kTile;
+        uint8_t* ph = smem + Smem::p + pb * kTile + hf * kHalf;
+        uint8_t* pl = smem + Smem::p + kTile + hf * kHalf;
+        // one body per (split, masked) combination: packed fp32 pairs for the
+        // scale (FFMA2) and the row sums (FADD2)
+        uint64_t lsum2 = 0, lsx2 = 0;
+        const uint64_t c2x2 = pk2(c2, c2), nm2 = pk2(-mrun, -mrun), neg1 = pk2(-1.f, -1.f);
+        auto emit = [&](auto split_c, auto masked_c) {
+          constexpr bool kSplit = decltype(split_c)::value, kMasked = decltype(masked_c)::value;
 #pragma unroll 1
-        for (int c = 0; c < kKT; c += 32) {
-          float z[32];
-          tmem_ld32(tmem + lane_base + slot * 128 + c, z);
-          tmem_wait_ld();
+          for (int c = 0; c < 64; c += 32) {
+            float z[32];
+            tmem_ld32(scol + c, z);
+            tmem_wait_ld();
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8) {
-            uint32_t hw[4], lw[4];
+            for (int c8 = 0; c8 < 4; ++c8) {
+              uint32_t hw[4], lw[4];
 #pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              const int k0 = c + c8 * 8 + e;
-              const float a = k0 < nvalid ? ex2(z[c8 * 8 + e] * c2 - mrun) : 0.f;
-              const float b = k0 + 1 < nvalid ? ex2(z[c8 * 8 + e + 1] * c2 - mrun) : 0.f;
-              const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
-              const __nv_bfloat162 lo2 = __floats2bfloat162_rn(a - __low2float(hi2), b - __high2float(hi2));
-              lsum += split ? a + b : __low2float(hi2) + __high2float(hi2);
-              lsx += a + b;
-              hw[e / 2] = *reinterpret_cast<const uint32_t*>(&hi2);
-              lw[e / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
+              for (int e = 0; e < 8; e += 2) {
+                float xa, xb;
+                upk2(ffma2(pk2(z[c8 * 8 + e], z[c8 * 8 + e + 1]), c2x2, nm2), xa, xb);
+                float a = ex2(xa), b = ex2(xb);
+                if constexpr (kMasked) {
+                  const int k0 = c + c8 * 8 + e;
+                  a = k0 < nvalid ? a : 0.f;
+                  b = k0 + 1 < nvalid ? b : 0.f;
+                }
+                const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
+                const uint32_t hb = *reinterpret_cast<const uint32_t*>(&hi2);
+                const uint64_t ab = pk2(a, b);
+                const uint64_t hf2 = pk2(__uint_as_float(hb << 16), __uint_as_float(hb & 0xffff0000u));
+                lsx2 = fadd2(lsx2, ab);
+                hw[e / 2] = hb;
+                if constexpr (kSplit) {
+                  float la, lb;
+                  upk2(ffma2(hf2, neg1, ab), la, lb);       // a - hi(a), exact
+                  const __nv_bfloat162 lo2 = __floats2bfloat162_rn(la, lb);
+                  lw[e / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
+                  lsum2 = fadd2(lsum2, ab);
+                } else {
+                  lsum2 = fadd2(lsum2, hf2);
+                }
+              }
+              const int chunk = (c >> 3) + c8;               // 16-byte chunk within the half (0..7)
+              const uint32_t off = r * 128 + ((chunk ^ (r & 7)) * 16);
+              *reinterpret_cast<uint4*>(ph + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              if constexpr (kSplit) *reinterpret_cast<uint4*>(pl + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }
-            const int cg = (c >> 3) + c8;                  // 16-byte chunk index across the row (0..15)
-            const int half = cg >> 3, chunk = cg & 7;
-            const uint32_t off = half * kHalf + r * 128 + ((chunk ^ (r & 7)) * 16);
-            *reinterpret_cast<uint4*>(ph + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            if (split) *reinterpret_cast<uint4*>(pl + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        if (split) {
+          if (full) emit(T_{}, F_{}); else emit(T_{}, T_{});
+        } else {
+          if (full) emit(F_{}, F_{}); else emit(F_{}, T_{});
+        }
+        {
+          float s0, s1, x0, x1;
+          upk2(lsum2, s0, s1);
+          upk2(lsx2, x0, x1);
+          lsum += s0 + s1;
+          lsx += x0 + x1;
         }
         tc_fence_before();
         __syncwarp();
@@ -339,13 +381,16 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + (pcount & 1));
       }
-      // ---- epilogue: thread r = O^T lane d; row stats via smem
-      st_l[r] = lsum;
+      // ---- epilogue: thread = O^T lane d over its half of the (q,h) columns;
+      // row sums of both key halves via smem (the P region: every PV is done)
       mbar_wait(o_full, it & 1);
-      named_bar_sync(1, 128);
+      st_l[hf * 128 + r] = lsum;
+      st_l[256 + hf * 128 + r] = lsx;
+      named_bar_sync(1, 256);
       tc_fence_after();
       const int d = r;
-      for (int c = 0; c < 128; c += 32) {
+#pragma unroll 1
+      for (int c = hf * 64; c < hf * 64 + 64; c += 32) {
         float o[32];
         tmem_ld32(tmem + lane_base + kColO + c, o);
         tmem_wait_ld();
@@ -354,19 +399,18 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           const int col = c + x;                         // (q, h) column
           const int64_t ri = i0 + (col >> 4);
           if (ri < p.n) {
-            const float v = o[x] / st_l[col];
+            const float v = o[x] / (st_l[col] + st_l[128 + col]);
             const int64_t idx = (ri * p.hq + (int64_t)grp * kG + (col & 15)) * kD + d;
             if (p.out_f32) static_cast<float*>(p.out)[idx] = v;
             else static_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(v);
           }
         }
       }
+      if (p.lse && row_ok && hf == 0)
+        p.lse[row_i * p.hq + grp * kG + h] = (mrun + log2f(st_l[256 + r] + st_l[384 + r])) * 0.6931471805599453f;
       tc_fence_before();
-      named_bar_sync(1, 128);
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty);
-      if (p.lse && row_ok)
-        p.lse[row_i * p.hq + grp * kG + h] = (mrun + log2f(lsx)) * 0.6931471805599453f;
     }
   }
   tc_fence_before();
