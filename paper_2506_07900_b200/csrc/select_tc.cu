@@ -372,16 +372,29 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 #pragma unroll
               for (int x = 0; x < 32; ++x) v[x] = (j0 + x < nk_row) ? v[x] : -INFINITY;
             }
-            float m4[4] = {v[0], v[1], v[2], v[3]};
+            // packed fp32 pairs (FFMA2 / FADD2) and 3-input max: the same
+            // per-element arithmetic and summation order as four scalar
+            // partial sums a[x & 3]
+            float mA = v[0], mB = v[1];
 #pragma unroll
-            for (int x = 4; x < 32; ++x) m4[x & 3] = fmaxf(m4[x & 3], v[x]);
-            const float cmax = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * p.zscale;
+            for (int x = 2; x < 30; x += 4) { mA = fmax3(mA, v[x], v[x + 1]); mB = fmax3(mB, v[x + 2], v[x + 3]); }
+            const float cmax = fmaxf(fmax3(mA, v[30], v[31]), mB) * p.zscale;
             const float mnew = fmaxf(mrun, cmax);
             if (mnew != -INFINITY) {
-              float a4[4] = {0.f, 0.f, 0.f, 0.f};
+              const uint64_t zs2 = pk2(p.zscale, p.zscale), nm2 = pk2(-mnew, -mnew);
+              uint64_t s01 = 0, s23 = 0;
 #pragma unroll
-              for (int x = 0; x < 32; ++x) a4[x & 3] += ex2(fmaf(v[x], p.zscale, -mnew));
-              srun = srun * ex2(mrun - mnew) + ((a4[0] + a4[1]) + (a4[2] + a4[3]));
+              for (int x = 0; x < 32; x += 4) {
+                float e0, e1, e2, e3;
+                upk2(ffma2(pk2(v[x], v[x + 1]), zs2, nm2), e0, e1);
+                upk2(ffma2(pk2(v[x + 2], v[x + 3]), zs2, nm2), e2, e3);
+                s01 = fadd2(s01, pk2(ex2(e0), ex2(e1)));
+                s23 = fadd2(s23, pk2(ex2(e2), ex2(e3)));
+              }
+              float a0, a1, a2, a3;
+              upk2(s01, a0, a1);
+              upk2(s23, a2, a3);
+              srun = srun * ex2(mrun - mnew) + ((a0 + a1) + (a2 + a3));
               mrun = mnew;
             }
             if (ch + 1 < kCols1 / 32) tmem_wait_ld();
@@ -392,7 +405,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           buf ^= 1;
         }
         if constexpr (kSplit == 1) {
-          lse2[row] = mrun + log2f(srun) + p.lse_bias2;
+          lse2[row] = -(mrun + log2f(srun) + p.lse_bias2);     // negated: the FFMA2 addend
         } else {
           pm[cpart * kRows + row] = mrun;
           ps[cpart * kRows + row] = srun;
@@ -411,7 +424,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const float mx = pm[x * kRows + etid];
             sum += (mx == -INFINITY) ? 0.f : ps[x * kRows + etid] * ex2(mx - m);
           }
-          lse2[etid] = m + log2f(sum) + p.lse_bias2;
+          lse2[etid] = -(m + log2f(sum) + p.lse_bias2);
         }
         named_bar_sync(1, kEpiThreads);
       }
@@ -468,15 +481,21 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           for (int u4 = 0; u4 < kQC; ++u4) {
             const int qi = q0 + qq + u4;
             const uint32_t l2 = smem_u32(lse2 + qi * kG);
-            float a0 = 0.f, a1 = 0.f;
+            // packed pairs: acc = (a0, a1), a0 over even heads, a1 over odd
+            // heads, in head order (the scalar two-accumulator order)
+            const uint64_t zs2 = pk2(p.zscale, p.zscale);
+            uint64_t acc = 0;
 #pragma unroll
             for (int h = 0; h < kG; h += 4) {
-              const float4 l4 = lds4(l2 + h * 4);
-              a0 += ex2(fmaf(v[u4 * kG + h], p.zscale, -l4.x));
-              a1 += ex2(fmaf(v[u4 * kG + h + 1], p.zscale, -l4.y));
-              a0 += ex2(fmaf(v[u4 * kG + h + 2], p.zscale, -l4.z));
-              a1 += ex2(fmaf(v[u4 * kG + h + 3], p.zscale, -l4.w));
+              const float4 l4 = lds4(l2 + h * 4);                // -lse2
+              float e0, e1, e2, e3;
+              upk2(ffma2(pk2(v[u4 * kG + h], v[u4 * kG + h + 1]), zs2, pk2(l4.x, l4.y)), e0, e1);
+              upk2(ffma2(pk2(v[u4 * kG + h + 2], v[u4 * kG + h + 3]), zs2, pk2(l4.z, l4.w)), e2, e3);
+              acc = fadd2(acc, pk2(ex2(e0), ex2(e1)));
+              acc = fadd2(acc, pk2(ex2(e2), ex2(e3)));
             }
+            float a0, a1;
+            upk2(acc, a0, a1);
             sc[u4] = live ? (a0 + a1) * (1.0f / kG) : -INFINITY;
           }
           float r[kQC];
