@@ -536,8 +536,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         const int b0 = sr.get(2 * c), b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
         bool valid = (2 * c + x) < nb;
         if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
+        {
+          // z * c2 as packed pairs (FFMA2, zero addend); masked rows -inf by
+          // select (a row past the tile's blocks may hold stale smem: NaN)
+          const uint64_t c2x2 = pk2(c2, c2);
 #pragma unroll
-        for (int h = 0; h < kSH; ++h) z[h] = valid ? z[h] * c2 : -INFINITY;
+          for (int h = 0; h < kSH; h += 2) upk2(ffma2(pk2(z[h], z[h + 1]), c2x2, 0ull), z[h], z[h + 1]);
+#pragma unroll
+          for (int h = 0; h < kSH; ++h) z[h] = valid ? z[h] : -INFINITY;
+        }
         // running max: exact on the first tile, rescale later only if z > M + 8.
         // The max is per head, so only the four warps of a head half vote (one
         // 128-thread barrier per tile; votes double-buffered by tile parity: a
@@ -547,7 +554,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (c > c0) {
           bool over = false;
 #pragma unroll
-          for (int h = 0; h < kSH; ++h) over |= z[h] > mrun[h] + 8.f;
+          for (int h = 0; h < kSH; h += 2) {
+            float t0, t1;
+            upk2(fadd2(pk2(mrun[h], mrun[h + 1]), pk2(8.f, 8.f)), t0, t1);
+            over |= (z[h] > t0) | (z[h + 1] > t1);
+          }
           const unsigned any = __ballot_sync(0xffffffffu, over);
           float* vt = vote + (tcount & 1) * 8;
           if (lane == 0) vt[ws] = any ? 1.f : 0.f;
@@ -613,15 +624,21 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         uint32_t phi[kSH / 2], plo[kSH / 2];
 #pragma unroll
         for (int h = 0; h < kSH; h += 2) {
-          const float a = ex2(z[h] - mrun[h]);
-          const float b = ex2(z[h + 1] - mrun[h + 1]);
+          // packed pairs: z - M (FADD2), the row sums (FADD2), a - hi (FFMA2)
+          float xa, xb;
+          upk2(fadd2(pk2(z[h], z[h + 1]), pk2(-mrun[h], -mrun[h + 1])), xa, xb);
+          const float a = ex2(xa);
+          const float b = ex2(xb);
           const __nv_bfloat162 hi2 = __floats2bfloat162_rn(a, b);
-          const __nv_bfloat162 lo2 = __floats2bfloat162_rn(a - __low2float(hi2), b - __high2float(hi2));
-          lsum[h] += splitp ? a : __low2float(hi2);
-          lsum[h + 1] += splitp ? b : __high2float(hi2);
-          lsx[h] += a;
-          lsx[h + 1] += b;
-          phi[h / 2] = *reinterpret_cast<const uint32_t*>(&hi2);
+          const uint32_t hb = *reinterpret_cast<const uint32_t*>(&hi2);
+          const uint64_t ab = pk2(a, b);
+          const uint64_t hf2 = pk2(__uint_as_float(hb << 16), __uint_as_float(hb & 0xffff0000u));
+          upk2(fadd2(pk2(lsx[h], lsx[h + 1]), ab), lsx[h], lsx[h + 1]);
+          upk2(fadd2(pk2(lsum[h], lsum[h + 1]), splitp ? ab : hf2), lsum[h], lsum[h + 1]);
+          float la, lb;
+          upk2(ffma2(hf2, pk2(-1.f, -1.f), ab), la, lb);    // a - hi(a), exact
+          const __nv_bfloat162 lo2 = __floats2bfloat162_rn(la, lb);
+          phi[h / 2] = hb;
           plo[h / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
         }
         uint8_t* pb = smem + Smem::p + pbuf * kPBytes;
