@@ -58,6 +58,9 @@ constexpr int kRows = kQ * kG;    // 256 (query, head) rows
 constexpr int kD = 128;
 constexpr int kNT = 128;          // kernels per tile
 constexpr int kStages = 2;
+#ifndef SEL_POLY
+#define SEL_POLY 0   // of every 4 odd element pairs, how many take 2^x on the FMA pipe
+#endif
 #ifndef SEL_SPLIT
 #define SEL_SPLIT 1   // 2 (16 epilogue warps at 80 registers) measured ~2% slower
 #endif
@@ -387,9 +390,11 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
               for (int x = 0; x < 32; x += 4) {
                 float e0, e1, e2, e3;
                 upk2(ffma2(pk2(v[x], v[x + 1]), zs2, nm2), e0, e1);
-                upk2(ffma2(pk2(v[x + 2], v[x + 3]), zs2, nm2), e2, e3);
+                const uint64_t x23 = ffma2(pk2(v[x + 2], v[x + 3]), zs2, nm2);
+                upk2(x23, e2, e3);
                 s01 = fadd2(s01, pk2(ex2(e0), ex2(e1)));
-                s23 = fadd2(s23, pk2(ex2(e2), ex2(e3)));
+                // SEL_POLY of every 4 odd pairs on the FMA pipe (MUFU relief)
+                s23 = fadd2(s23, ((x >> 2) & 3) < SEL_POLY ? ex2_poly2(x23) : pk2(ex2(e2), ex2(e3)));
               }
               float a0, a1, a2, a3;
               upk2(s01, a0, a1);
@@ -490,9 +495,10 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
               const float4 l4 = lds4(l2 + h * 4);                // -lse2
               float e0, e1, e2, e3;
               upk2(ffma2(pk2(v[u4 * kG + h], v[u4 * kG + h + 1]), zs2, pk2(l4.x, l4.y)), e0, e1);
-              upk2(ffma2(pk2(v[u4 * kG + h + 2], v[u4 * kG + h + 3]), zs2, pk2(l4.z, l4.w)), e2, e3);
+              const uint64_t x23 = ffma2(pk2(v[u4 * kG + h + 2], v[u4 * kG + h + 3]), zs2, pk2(l4.z, l4.w));
+              upk2(x23, e2, e3);
               acc = fadd2(acc, pk2(ex2(e0), ex2(e1)));
-              acc = fadd2(acc, pk2(ex2(e2), ex2(e3)));
+              acc = fadd2(acc, ((u4 * kG + h) / 4 & 3) < SEL_POLY ? ex2_poly2(x23) : pk2(ex2(e2), ex2(e3)));
             }
             float a0, a1;
             upk2(acc, a0, a1);
