@@ -52,7 +52,8 @@ struct Smem {
   static constexpr uint32_t kv = q + kTile;                 // [2 stages][K, V] 128 KB
   static constexpr uint32_t p = kv + 4 * kTile;             // [2] P tiles (hi; the lo part uses the other) 64 KB
   static constexpr uint32_t corr = p + 2 * kTile;           // [128] per-row rescale factors
-  static constexpr uint32_t bars = corr + 128 * 4;
+  static constexpr uint32_t xch = corr + 128 * 4;           // [2 parities][2 key halves][128] bf16 row maxima
+  static constexpr uint32_t bars = xch + 2 * 2 * 128 * 2;
   // the epilogue's row sums [2 halves][128] l, [2][128] l exact live in the
   // P region (idle once O is complete)
   static constexpr uint32_t total = bars + 18 * 8;
@@ -93,6 +94,7 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   uint64_t* o_empty = bars + 15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   float* corr = reinterpret_cast<float*>(smem + Smem::corr);
+  __nv_bfloat16* xch = reinterpret_cast<__nv_bfloat16*>(smem + Smem::xch);
   float* st_l = reinterpret_cast<float*>(smem + Smem::p);          // [2][128], then l exact [2][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,20 +259,30 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const bool full = key0 + kKT - 1 <= p.start + i0;
         float tmax = -INFINITY;
 #pragma unroll 1
-        for (int c = 0; c < kKT; c += 32) {
+        for (int c = 0; c < 64; c += 32) {
           float z[32];
-          tmem_ld32(tmem + lane_base + slot * 128 + c, z);
+          tmem_ld32(scol + c, z);
           tmem_wait_ld();
           if (full) {
 #pragma unroll
             for (int x = 0; x < 32; x += 2) tmax = fmax3(tmax, z[x], z[x + 1]);
           } else {
 #pragma unroll
-            for (int x = 0; x < 32; ++x) tmax = fmaxf(tmax, c + x < nvalid + hf * 64 ? z[x] : -INFINITY);
+            for (int x = 0; x < 32; ++x) tmax = fmaxf(tmax, c + x < nvalid ? z[x] : -INFINITY);
           }
         }
-        tmax *= c2;
-        const bool need = named_bar_or(1, 256, t == 0 || tmax > mrun + 8.f);
+        // row max of both halves through smem, rounded UP to bf16 on both
+        // sides (the two threads of a row then hold the same M >= the true
+        // max; M only needs to bound the scores, the LSE and O are exact for
+        // any M); slots double-buffered by tile parity: a slot is rewritten
+        // only after every reader passed the next tile's barrier
+        __nv_bfloat16* xb = xch + (tcount & 1) * 256;
+        const __nv_bfloat16 mine = __float2bfloat16_ru(tmax * c2);
+        xb[hf * 128 + r] = mine;
+        tmax = __bfloat162float(mine);
+        const bool over_own = tmax > mrun + 8.f;
+        const bool need = named_bar_or(1, 256, t == 0 || over_own);
+        tmax = fmaxf(tmax, __bfloat162float(xb[(hf ^ 1) * 128 + r]));
         if (need) {
           const float mnew = fmaxf(mrun, tmax);
           const float cf = mrun == -INFINITY ? 1.f : ex2(mrun - mnew);
