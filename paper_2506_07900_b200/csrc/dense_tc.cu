@@ -17,9 +17,9 @@
 // Warp roles (12 warps): 0 = TMA producer (Q per item, K + V per tile, two
 // stages), 1 = TMEM alloc + MMA issuer, 4..11 = softmax, then epilogue.  Warps
 // w and w + 4 share TMEM lane quadrant w % 4: thread = (q,h) row r, the first
-// four take keys 0..63 of every tile, the others keys 64..127 (both take the
-// max over the whole row; one OR-reducing barrier per tile is the rescale
-// vote); in the epilogue thread = d lane of O^T over its half of the
+// four take keys 0..63 of every tile, the others keys 64..127 (half maxima
+// exchanged through smem as bf16 rounded up; one OR-reducing barrier per tile
+// is also the rescale vote); in the epilogue thread = d lane of O^T over its half of the
 // (q,h) columns (divide by the row sums, store) and thread = row (LSE).
 #include <float.h>
 #include <stdlib.h>
