@@ -108,7 +108,7 @@ struct AttCfg {
     static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
     static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
     static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
-    static constexpr uint32_t flags = red + 8 * 16 * 4;           // [2 parities][8 warps] rescale votes
+    static constexpr uint32_t flags = red + 8 * 16 * 4;           // (unused)
     static constexpr uint32_t bars = flags + 2 * 8 * 4;
     static constexpr uint32_t total = bars + 88 * 8;
   };
@@ -263,7 +263,6 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
   float* stats = reinterpret_cast<float*>(smem + Smem::stats);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
-  float* vote = reinterpret_cast<float*>(smem + Smem::flags);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ATT_T0(t_kernel);
@@ -547,8 +546,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         }
         // running max: exact on the first tile, rescale later only if z > M + 8.
         // The max is per head, so only the four warps of a head half vote (one
-        // 128-thread barrier per tile; votes double-buffered by tile parity: a
-        // warp cannot overwrite a slot before the others passed the next barrier)
+        // OR-reducing 128-thread barrier per tile)
         if (warp == 2 && lane == 0) ATT_ADD(19, s19);
         bool need = (c == c0);
         if (c > c0) {
@@ -559,14 +557,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             upk2(fadd2(pk2(mrun[h], mrun[h + 1]), pk2(8.f, 8.f)), t0, t1);
             over |= (z[h] > t0) | (z[h + 1] > t1);
           }
-          const unsigned any = __ballot_sync(0xffffffffu, over);
-          float* vt = vote + (tcount & 1) * 8;
-          if (lane == 0) vt[ws] = any ? 1.f : 0.f;
+          // the half's 128-thread barrier ORs the votes (bar.red)
           ATT_T0(s1);
-          if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+          need = named_bar_or(half ? 3 : 2, 128, over);
           if (warp == 2 && lane == 0) ATT_ADD(9, s1);
-          const int hb = 4 * half;
-          need = (vt[hb] + vt[hb + 1] + vt[hb + 2] + vt[hb + 3]) > 0.f;
         }
         ATT_T0(s2);
         if (need) {
