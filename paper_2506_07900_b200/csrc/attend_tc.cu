@@ -148,14 +148,32 @@ __device__ __forceinline__ void tile_range(const Params& p, int64_t part, int ti
 // Work unit w -> (selection/output item = i*hkv + grp, split part, row i, group).
 __device__ __forceinline__ void unit_of(const Params& p, int64_t w, int64_t* item, int64_t* part, int64_t* i,
                                         int* grp) {
-  const int64_t u = w / p.parts;
-  *part = w - u * p.parts;
-  if (p.group_major) {
-    *grp = (int)(u / p.n);
-    *i = u - (int64_t)(*grp) * p.n;
+  // 32-bit divisions whenever the unit space fits (a 64-bit division is a
+  // ~100-instruction subroutine, paid by every warp role once per item)
+  if (w < 0x7fffffff && p.n < 0x7fffffff) {
+    const uint32_t w32 = (uint32_t)w, parts = (uint32_t)p.parts;
+    const uint32_t u = parts == 1 ? w32 : w32 / parts;
+    *part = (int64_t)(w32 - u * parts);
+    uint32_t i32, g32;
+    if (p.group_major) {
+      g32 = u / (uint32_t)p.n;
+      i32 = u - g32 * (uint32_t)p.n;
+    } else {
+      i32 = u / (uint32_t)p.hkv;
+      g32 = u - i32 * (uint32_t)p.hkv;
+    }
+    *i = (int64_t)i32;
+    *grp = (int)g32;
   } else {
-    *i = u / p.hkv;
-    *grp = (int)(u - *i * p.hkv);
+    const int64_t u = w / p.parts;
+    *part = w - u * p.parts;
+    if (p.group_major) {
+      *grp = (int)(u / p.n);
+      *i = u - (int64_t)(*grp) * p.n;
+    } else {
+      *i = u / p.hkv;
+      *grp = (int)(u - *i * p.hkv);
+    }
   }
   *item = *i * p.hkv + *grp;
 }
