@@ -59,7 +59,11 @@ constexpr int kStages = 3;
 #define ATT_KSTAGES 3
 #endif
 constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
-constexpr int kSlots = 4;               // S^T slots in TMEM (QK runs up to kSlots tiles ahead of softmax)
+#ifndef ATT_SLOTS
+#define ATT_SLOTS 6   // 4 / 5 / 6 measured 12.75 / 12.61 / 12.59 ms per 128K layer
+#endif
+constexpr int kSlots = ATT_SLOTS;       // S^T slots in TMEM (QK runs up to kSlots tiles ahead of softmax)
+static_assert(kSlots <= 6, "(kSlots + 2) * 2 * G TMEM columns must fit the 256-column allocation at G = 16");
 #ifndef ATT_QK_SPLIT
 #define ATT_QK_SPLIT 0   // 1 measured ~1.5 % slower now that the softmax bounds the kernel
 #endif
