@@ -43,6 +43,11 @@ constexpr int kD = 128;
 constexpr int kQR = 8;                        // query rows per item (8 x 16 heads = 128 MMA rows)
 constexpr int kKT = 128;                      // keys per tile
 constexpr int kThreads = 384;
+#ifndef DENSE_SLOTS
+#define DENSE_SLOTS 2   // 3 measured equal (softmax-bound)
+#endif
+constexpr int kSSlots = DENSE_SLOTS;          // S tiles in TMEM (QK runs up to kSSlots tiles ahead)
+static_assert(kSSlots >= 2 && kSSlots <= 3, "S slots + O^T must fit 512 TMEM columns");
 constexpr int64_t kSplitBelow = 256;          // items starting below this position carry P lo too
 constexpr uint32_t kHalf = 128 * 128;         // 16 KB: 128 rows x 64 bf16 (one 128-B swizzle half)
 constexpr uint32_t kTile = 2 * kHalf;         // 32 KB: 128 rows x 128 bf16
@@ -56,7 +61,7 @@ struct Smem {
   static constexpr uint32_t bars = xch + 2 * 2 * 128 * 2;
   // the epilogue's row sums [2 halves][128] l, [2][128] l exact live in the
   // P region (idle once O is complete)
-  static constexpr uint32_t total = bars + 18 * 8;
+  static constexpr uint32_t total = bars + 20 * 8;
 };
 static_assert(Smem::total + 1024 <= 232448, "dense attention shared memory");
 
@@ -86,13 +91,13 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   uint64_t* q_empty = bars + 1;
   uint64_t* kv_full = bars + 2;      // [2]
   uint64_t* kv_empty = bars + 4;     // [2]
-  uint64_t* s_full = bars + 6;       // [2]
-  uint64_t* s_empty = bars + 8;      // [2]
-  uint64_t* p_full = bars + 10;      // [2]
-  uint64_t* p_empty = bars + 12;     // [2]
-  uint64_t* o_full = bars + 14;
-  uint64_t* o_empty = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* s_full = bars + 6;       // [kSSlots <= 3]
+  uint64_t* s_empty = bars + 9;      // [kSSlots <= 3]
+  uint64_t* p_full = bars + 12;      // [2]
+  uint64_t* p_empty = bars + 14;     // [2]
+  uint64_t* o_full = bars + 16;
+  uint64_t* o_empty = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
   float* corr = reinterpret_cast<float*>(smem + Smem::corr);
   __nv_bfloat16* xch = reinterpret_cast<__nv_bfloat16*>(smem + Smem::xch);
   float* st_l = reinterpret_cast<float*>(smem + Smem::p);          // [2][128], then l exact [2][128]
@@ -104,10 +109,12 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     for (int i = 0; i < 2; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
-      mbar_init(s_full + i, 1);
-      mbar_init(s_empty + i, 8);
       mbar_init(p_full + i, 8);
       mbar_init(p_empty + i, 1);
+    }
+    for (int i = 0; i < kSSlots; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 8);
     }
     mbar_init(o_full, 1);
     mbar_init(o_empty, 8);
@@ -121,7 +128,7 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t kColO = 256;     // S slots at [0, 256), O^T at [256, 384)
+  constexpr uint32_t kColO = kSSlots * 128;     // S slots at [0, kColO), O^T at [kColO, kColO + 128)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -163,7 +170,7 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     const uint64_t dq = sdesc_k_sw128(smem_u32(smem + Smem::q));
     int stage = 0;
     uint32_t phase = 0;
-    uint32_t tcount = 0;       // tiles issued (S slot = tcount & 1)
+    uint32_t tcount = 0;       // tiles issued (S slot = tcount % kSSlots)
     uint32_t pcount = 0;       // PV tiles issued (P buffer = pcount & 1)
     int it = 0;
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x, ++it) {
@@ -201,9 +208,9 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         if (++pv_stage == 2) { pv_stage = 0; pv_phase ^= 1; }
       };
       for (int t = 0; t < tiles; ++t, ++tcount) {
-        const int slot = tcount & 1;
+        const int slot = tcount % kSSlots;
         mbar_wait(kv_full + stage, phase);
-        mbar_wait(s_empty + slot, ((tcount >> 1) & 1) ^ 1);
+        mbar_wait(s_empty + slot, ((tcount / kSSlots) & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = sdesc_k_sw128(smem_u32(smem + Smem::kv + stage * 2 * kTile));
@@ -244,8 +251,8 @@ dense_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       const int64_t pos = p.start + (row_ok ? row_i : last);
       float mrun = -INFINITY, lsum = 0.f, lsx = 0.f;
       for (int t = 0; t < tiles; ++t, ++tcount, ++pcount) {
-        const int slot = tcount & 1;
-        mbar_wait(s_full + slot, (tcount >> 1) & 1);
+        const int slot = tcount % kSSlots;
+        mbar_wait(s_full + slot, (tcount / kSSlots) & 1);
         tc_fence_after();
         const int64_t key0 = (int64_t)t * kKT;
         // keys <= pos in this tile, counted from this half's first key
