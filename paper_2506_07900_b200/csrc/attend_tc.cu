@@ -54,7 +54,6 @@ __device__ long long g_att_cyc[160][24];
 #endif
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
-constexpr int kStages = 3;
 #ifndef ATT_KSTAGES
 #define ATT_KSTAGES 3
 #endif
@@ -75,11 +74,6 @@ constexpr int kMaxSel = 80;
 constexpr int64_t kSplitPBelow = 256;
 
 constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
-constexpr uint32_t kTileBytes = 2 * kHalfBytes;         // 32 KB per K or V tile
-constexpr uint32_t kStageBytes = 2 * kTileBytes;        // K + V = 64 KB
-constexpr uint32_t kQBytes = 2 * kG * 128;              // 4 KB (two 64-d halves of 16 rows)
-constexpr uint32_t kPBytes = 2 * kRowsT * kG * 2;       // 8 KB: P_hi and P_lo (bf16 each)
-constexpr uint32_t kPHalf = kRowsT * kG * 2;            // 4 KB
 
 // Per-geometry constants: G heads per KV group (16 or 8), head dim D (128 or
 // 64).  MiniCPM4-8B is (16, 128), MiniCPM4-0.5B (8, 64).  Tiles stay 128 rows;
@@ -88,7 +82,6 @@ template <int G, int D>
 struct AttCfg {
   static constexpr int kDH = D / 64;                              // 64-d halves per row
   static constexpr uint32_t kTileBytes = kDH * kHalfBytes;        // K or V tile
-  static constexpr uint32_t kStageBytes = 2 * kTileBytes;
   static constexpr int kStages = 3 * (128 / D);                   // K + V stage pairs of smem
   static constexpr int kKStages = ATT_KSTAGES * (128 / D);        // K ring depth
   static constexpr int kVStages = 2 * kStages - kKStages;         // V ring depth
@@ -252,9 +245,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   using Smem = typename C::Smem;
   constexpr int kG = G;
   constexpr int kD = D;
-  constexpr int kStages = C::kStages;
   constexpr uint32_t kTileBytes = C::kTileBytes;
-  constexpr uint32_t kStageBytes = C::kStageBytes;
   constexpr uint32_t kQBytes = C::kQBytes;
   constexpr uint32_t kPBytes = C::kPBytes;
   constexpr uint32_t kPHalf = C::kPHalf;

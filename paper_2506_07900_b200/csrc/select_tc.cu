@@ -55,7 +55,6 @@ __device__ long long g_sel_cyc[160][8];
 constexpr int kQ = 16;            // query positions per work unit
 constexpr int kG = 16;            // heads per KV group
 constexpr int kRows = kQ * kG;    // 256 (query, head) rows
-constexpr int kD = 128;
 constexpr int kNT = 128;          // kernels per tile
 constexpr int kStages = 2;
 #ifndef SEL_POLY
@@ -75,9 +74,7 @@ using topk::UnitSel;
 using topk::unit_sel;
 using topk::warp_select;
 
-constexpr uint32_t kQBytes = kRows * kD * 2;               // 64 KB
 constexpr uint32_t kMuHalfBytes = kNT * 64 * 2;            // 16 KB (128 rows x 128 B)
-constexpr uint32_t kMuStageBytes = 4 * kMuHalfBytes;       // hi h0,h1, lo h0,h1 = 64 KB
 constexpr int kSTileLd = kNT + 4;                          // epilogue scratch (see the epilogue)
 
 // Per-geometry constants: G heads per KV group, head dim D; a unit is always
@@ -316,7 +313,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     const int half = sub & 1;                // pass 1: row half; pass 2: query half
     const int cpart = sub >> 1;              // pass 1: column part; pass 2: query part
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    const int etid = ew * 32 + lane;
+    [[maybe_unused]] const int etid = ew * 32 + lane;   // kSplit > 1 only
     int buf = 0;
     uint32_t acc_phase[2] = {0, 0};
     int ucount = 0;
@@ -326,8 +323,8 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     constexpr int kCols1 = 128 / kSplit;             // pass-1 columns per thread
     // scratch in the stile region: pass-1 partial (max, sum) per (part, row),
     // then pass-2 carries [3 slots][subs][2][4 quads][kQS]
-    float* pm = stile;
-    float* ps = stile + kSplit * kRows;
+    [[maybe_unused]] float* pm = stile;
+    [[maybe_unused]] float* ps = stile + kSplit * kRows;
     float* carries = stile + 2 * kSplit * kRows;
     for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++ucount) {
       float* rbuf = p.rbuf + ((int64_t)blockIdx.x * 2 + (ucount & 1)) * kQ * p.nb_cap;
