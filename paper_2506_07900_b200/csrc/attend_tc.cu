@@ -55,7 +55,7 @@ __device__ long long g_att_cyc[160][24];
 constexpr int kM = 64;                 // block size
 constexpr int kRowsT = 128;            // rows per tile (two blocks)
 #ifndef ATT_KSTAGES
-#define ATT_KSTAGES 3
+#define ATT_KSTAGES 2   // K ring 2 + V ring 4: 12.24 vs 12.34 ms (3 + 3) per 128K layer
 #endif
 constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
 #ifndef ATT_SLOTS
