@@ -215,6 +215,10 @@ typedef struct infllm2_seq_desc {
   int64_t coarse_cap;
 } infllm2_seq_desc;
 
+/* 1 when infllm2_decode_step covers this geometry (G = 16, D = 128, s = 16,
+ * p = 32, m = 64, max_selected <= 80), else 0: callers step other shapes
+ * through infllm2_forward one sequence at a time. */
+int infllm2_decode_supported(const infllm2_geometry* g, int32_t hq, int32_t hkv, int32_t d);
 /* Device table (descriptors, TMA tensor maps, device-resident lengths). */
 size_t infllm2_decode_table_bytes(int32_t n_seq);
 /* Build it from HOST descriptors and lengths into `table` (device memory of
@@ -222,6 +226,10 @@ size_t infllm2_decode_table_bytes(int32_t n_seq);
  * cache is reallocated or its length changes outside infllm2_decode_step. */
 int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq,
                                int32_t hkv, int32_t d, void* table, infllm2_stream_t stream);
+/* Copy the table's device-resident lengths (advanced by every decode step,
+ * including graph replays) into host `lens` (n_seq entries); synchronises
+ * `stream`.  Lets a caller check its host bookkeeping after replays. */
+int infllm2_decode_table_lengths(const void* table, int32_t n_seq, int64_t* lens, infllm2_stream_t stream);
 size_t infllm2_decode_workspace_bytes(const infllm2_geometry* g, int32_t n_seq, int32_t hkv,
                                       int64_t max_cache_len);
 /* One decode step for all sequences: append k_new/v_new ((S, HKV, D) bf16) at

@@ -11,12 +11,33 @@
 #include "tc_dispatch.cuh"
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 using namespace infllm2;
 
 namespace infllm2 {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return dev;
+}
+
+cudaError_t smem_attr_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;   // (kernel, device) -> bytes set
+  const auto key = std::make_pair(kernel, current_device());
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
 }  // namespace infllm2
 
 namespace {
@@ -266,6 +287,11 @@ int infllm2_dense_regime(const infllm2_geometry* g, int64_t n, int64_t start, in
   return select_dense_regime(*g, cs) ? 1 : 0;
 }
 
+int infllm2_decode_supported(const infllm2_geometry* g, int32_t hq, int32_t hkv, int32_t d) {
+  if (infllm2_validate_geometry(g) || hq <= 0 || hkv <= 0 || hq % hkv) return 0;
+  return decode_supported(*g, hq, hkv, d) ? 1 : 0;
+}
+
 size_t infllm2_decode_table_bytes(int32_t n_seq) { return n_seq > 0 ? decode_table_bytes(n_seq) : 0; }
 
 int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq, int32_t hkv,
@@ -274,6 +300,11 @@ int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens
   for (int s = 0; s < n_seq; ++s)
     if (lens[s] < 0 || lens[s] > seqs[s].cap) return INFLLM2_ERR_CAPACITY;
   return decode_table_build(seqs, lens, n_seq, hkv, d, table, (cudaStream_t)stream);
+}
+
+int infllm2_decode_table_lengths(const void* table, int32_t n_seq, int64_t* lens, infllm2_stream_t stream) {
+  if (n_seq <= 0 || !table || !lens) return INFLLM2_ERR_SHAPE;
+  return cuda_status(decode_table_lengths(table, n_seq, lens, (cudaStream_t)stream));
 }
 
 size_t infllm2_decode_workspace_bytes(const infllm2_geometry* g, int32_t n_seq, int32_t hkv, int64_t max_cache_len) {

@@ -872,8 +872,7 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   const uint32_t box[3] = {64, (uint32_t)kG, 1};
   if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
   const size_t smem = AttCfg<16, 128>::Smem::total + 1024;
-  cudaError_t e =
-      cudaFuncSetAttribute(attend_tc_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr_once((const void*)attend_tc_kernel<16, 128>, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t items = n_seq * hkv * p.parts;
   int dev = 0, sms = kNumSMs;
@@ -931,11 +930,9 @@ static cudaError_t launch_attend_prefill(const CallShape& cs, const void* q, int
     if (!encode_tmap_3d_bf16(&tv, v_cache, dims, strides, box)) return cudaErrorInvalidValue;
   }
   const size_t smem = AttCfg<G, D>::Smem::total + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<G, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr_once((const void*)attend_tc_kernel<G, D>, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -51,6 +51,11 @@ __host__ __device__ inline void kernel_range_for_block(int64_t start, int64_t en
 // Kernel-launch entry points implemented in the .cu files (host side).
 namespace infllm2 {
 void count_launch();  // host-side counter behind infllm2_launch_count()
+// Raise `kernel`'s dynamic shared-memory limit to `bytes` once per (kernel,
+// device): the attribute is per device, so a process driving several GPUs
+// sets it on each (thread-safe; later calls are a map lookup).
+cudaError_t smem_attr_once(const void* kernel, int bytes);
+int current_device();
 cudaError_t launch_append_kv(void* k_cache, void* v_cache, int64_t cap, int hkv, int d,
                              const void* k_new, const void* v_new, int64_t n_new,
                              int64_t src_row_stride, int src_is_f32, int64_t l_old,

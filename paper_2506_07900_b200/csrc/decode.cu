@@ -98,16 +98,19 @@ __global__ void __launch_bounds__(256) decode_append_compress_kernel(void* table
       ds.k[((int64_t)g * ds.cap + l_old) * d + e] = k_new[(int64_t)s * hkv * d + idx];
       ds.v[((int64_t)g * ds.cap + l_old) * d + e] = v_new[(int64_t)s * hkv * d + idx];
     }
-    if (j >= count) continue;
-    const float mu = window_mean(ds.k + (int64_t)g * ds.cap * d, d, j, stride, l_new, e, l_old, knew);
     if (role < 2) {
+      if (j >= count) continue;
+      const float mu = window_mean(ds.k + (int64_t)g * ds.cap * d, d, j, stride, l_new, e, l_old, knew);
       const int64_t dst = ((int64_t)g * ds.means_cap + j) * d + e;
       ds.fine[dst] = mu;
       const __nv_bfloat16 h = __float2bfloat16_rn(mu);
       ds.hi[dst] = h;
       ds.lo[dst] = __float2bfloat16_rn(mu - __bfloat162float(h));
     } else {
-      ds.coarse[((int64_t)g * ds.coarse_cap + j) * d + e] = mu;
+      // every dirty coarse window (two when coarse_stride < kernel_size)
+      for (int64_t jc = first; jc < count; ++jc)
+        ds.coarse[((int64_t)g * ds.coarse_cap + jc) * d + e] =
+            window_mean(ds.k + (int64_t)g * ds.cap * d, d, jc, stride, l_new, e, l_old, knew);
     }
   }
 }
@@ -457,6 +460,12 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
 
 size_t decode_table_bytes(int n_seq) { return table_bytes(n_seq); }
 
+cudaError_t decode_table_lengths(const void* table, int n_seq, int64_t* lens, cudaStream_t stream) {
+  const TableView tv = table_view(const_cast<void*>(table), n_seq);
+  const cudaError_t e = cudaMemcpyAsync(lens, tv.len, sizeof(int64_t) * n_seq, cudaMemcpyDeviceToHost, stream);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(stream);
+}
+
 int decode_table_build(const infllm2_seq_desc* host, const int64_t* lens, int n_seq, int hkv, int d,
                        void* table_dev, cudaStream_t stream) {
   const size_t bytes = table_bytes(n_seq);
@@ -581,8 +590,7 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
     if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
   }
   const size_t smem1 = S1Smem::total + 1024;
-  if (cudaFuncSetAttribute(decode_stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) !=
-      cudaSuccess)
+  if (smem_attr_once((const void*)decode_stage1_kernel, (int)smem1) != cudaSuccess)
     return INFLLM2_ERR_CUDA;
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -612,8 +620,7 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   scp.selection = selection;
   const size_t sc_smem = sizeof(float) * (size_t)w.nb_cap;
   if (sc_smem > 40 * 1024 &&
-      cudaFuncSetAttribute(decode_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem) !=
-          cudaSuccess)
+      smem_attr_once((const void*)decode_scores_kernel, (int)sc_smem) != cudaSuccess)
     return INFLLM2_ERR_UNSUPPORTED;
   if (launch_pdl(decode_scores_kernel, dim3((unsigned)(n_seq * hkv * w.nbchunk)), dim3(256), sc_smem, stream, scp) !=
       cudaSuccess)

@@ -670,9 +670,10 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           int64_t first = I.pos < kP ? 0 : (I.pos - kP) / cs + 1;
           const int64_t count_old = I.pos / cs, count = L / cs;
           if (first > count_old) first = count_old;
-          if (first < count) {
-            const float mu = window_mean(kg, kD, first, cs, L, d, I.pos, knew);
-            ds.coarse[((int64_t)I.g * ds.coarse_cap + first) * kD + d] = mu;
+          // every dirty coarse window (two when coarse_stride < kernel_size)
+          for (int64_t j = first; j < count; ++j) {
+            const float mu = window_mean(kg, kD, j, cs, L, d, I.pos, knew);
+            ds.coarse[((int64_t)I.g * ds.coarse_cap + j) * kD + d] = mu;
           }
         }
       }
@@ -981,7 +982,9 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         }
         for (int x = tid; x < p.max_sel; x += 128) {
           int id = -2;
-          if (dense) id = x < I.n_cand ? x : -1;
+          // every candidate only when the budget covers them all; budget 0 with
+          // free blocks left (forced_consume_budget) selects the forced blocks
+          if (I.budget >= I.n_free) id = x < I.n_cand ? x : -1;
           else if (x < I.n_init) id = x;
           else if (x >= I.n_init + I.n_ch && x < I.n_sel) id = I.local_lo + (x - I.n_init - I.n_ch);
           else if (x >= I.n_sel) id = -1;
@@ -1109,12 +1112,18 @@ size_t decode_fused_workspace_bytes(int n_seq, int hkv) {
 }
 
 static int max_active_clusters(int np) {
-  static int cached[kMaxCl + 1] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
-  if (cached[np] >= 0) return cached[np];
+  constexpr int kMaxDev = 64;
+  static int cached[kMaxDev][kMaxCl + 1];
+  static bool init = false;
+  if (!init) {
+    for (auto& row : cached)
+      for (int& c : row) c = -1;
+    init = true;
+  }
+  const int dev = current_device() % kMaxDev;   // occupancy is per device
+  if (cached[dev][np] >= 0) return cached[dev][np];
   const size_t smem = Smem::total + 1024;
-  if (cudaFuncSetAttribute(decode_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return cached[np] = 0;
+  if (smem_attr_once((const void*)decode_cluster_kernel, (int)smem) != cudaSuccess) return cached[dev][np] = 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1128,7 +1137,7 @@ static int max_active_clusters(int np) {
   cfg.numAttrs = 1;
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel, &cfg) != cudaSuccess) n = 0;
-  return cached[np] = n;
+  return cached[dev][np] = n;
 }
 
 // Cluster size (= pieces per segment): the largest per-round parallelism

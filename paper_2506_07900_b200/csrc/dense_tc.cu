@@ -470,11 +470,9 @@ cudaError_t launch_dense_tc(const CallShape& cs, const void* q, int64_t q_row_st
     if (!encode_tmap_3d_bf16(&tv, v_cache, dims, strides, box)) return cudaErrorInvalidValue;
   }
   const size_t smem = Smem::total + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dense_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr_once((const void*)dense_tc_kernel, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

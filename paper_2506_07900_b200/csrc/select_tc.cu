@@ -713,11 +713,9 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
     tclo = tlo;
   }
   const size_t smem = C::Smem::total + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<G, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr_once((const void*)select_tc_kernel<G, D>, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   count_launch();
   select_tc_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, thi, tlo, tchi, tclo, p);

@@ -37,6 +37,7 @@ class DecodeBatch:
         self.device = l0.device
         self._table: Optional[torch.Tensor] = None
         self._sig = None
+        self._ws: Optional[torch.Tensor] = None   # owned scratch: a captured graph keeps its pointer
         self._lib = _lib.load()
 
     def _signature(self):
@@ -65,9 +66,10 @@ class DecodeBatch:
         self._sig = sig
 
     def _fused_ok(self, hq: int, hkv: int, d: int) -> bool:
-        """The batched decode kernels cover G = 16, D = 128 (MiniCPM4-8B); other
-        head geometries step each sequence through the prefill kernels."""
-        return hkv > 0 and hq // hkv == 16 and hq % hkv == 0 and d == 128
+        """The library's own predicate (infllm2_decode_supported: G = 16, D = 128,
+        s = 16, p = 32, m = 64, max_selected <= 80); other geometries step each
+        sequence through the prefill kernels."""
+        return bool(self._lib.infllm2_decode_supported(ctypes.byref(self.config.geometry()), hq, hkv, d))
 
     def _step_per_sequence(self, q, k_new, v_new, return_selection, return_lse, out_dtype, bookkeep):
         """One decode step per sequence with the (n = 1) prefill kernels — same
@@ -98,6 +100,20 @@ class DecodeBatch:
         for l in self.layers:
             l._reserve(l.length + extra_tokens)
         self._ensure()
+        l0 = self.layers[0]
+        bound = max(l.length for l in self.layers) + max(int(extra_tokens), 1)
+        self._workspace(self._lib.infllm2_decode_workspace_bytes(ctypes.byref(self.config.geometry()),
+                                                                 len(self.layers), l0.n_kv_heads, bound))
+
+    def _workspace(self, nbytes: int) -> torch.Tensor:
+        """This batch's own scratch, grown only outside graph capture: a graph
+        captured over step() keeps the pointer, so the buffer lives (and is never
+        shared with another stream's calls) as long as the batch does."""
+        if self._ws is None or self._ws.numel() < nbytes:
+            if torch.cuda.is_current_stream_capturing():
+                raise ValidationError("decode workspace too small inside graph capture: call reserve() first")
+            self._ws = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=self.device)
+        return self._ws
 
     def advance(self, n: int = 1) -> None:
         """Host bookkeeping for `n` steps replayed from a captured graph."""
@@ -143,8 +159,7 @@ class DecodeBatch:
         if max_len < cur:
             raise ValidationError("max_len below the longest sequence")
         ws_bytes = self._lib.infllm2_decode_workspace_bytes(ctypes.byref(geom), n, l0.n_kv_heads, max_len)
-        from .sparse import _workspace
-        ws = _workspace(dev, ws_bytes)
+        ws = self._workspace(ws_bytes)
         flags = _lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0
         _lib.check(self._lib.infllm2_decode_step(
             ctypes.byref(geom), self._table.data_ptr(), n, max_len, hq, l0.n_kv_heads, d, _ptr(qb), _ptr(kb),

@@ -141,15 +141,24 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 
 
 _WS: dict = {}
+_WS_CAPTURED: list = []     # buffers a captured CUDA graph may reference: never released
 
 
 def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
-    """Per-device scratch reused across calls (grown on demand)."""
-    key = (device.type, device.index)
+    """Scratch reused across calls, one buffer per (device, stream): calls on
+    different streams never share scratch.  A buffer used while a CUDA graph is
+    being captured is kept alive for the life of the process (the graph holds
+    its address), so growing the cache later cannot hand that memory to
+    anything else."""
+    stream = torch.cuda.current_stream(device)
+    key = (device.type, device.index, stream.cuda_stream)
     ws = _WS.get(key)
+    capturing = torch.cuda.is_current_stream_capturing()
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         _WS[key] = ws
+    if capturing and not any(w is ws for w in _WS_CAPTURED):
+        _WS_CAPTURED.append(ws)
     return ws
 
 

@@ -41,8 +41,6 @@ with torch.cuda.stream(s_):
     step(); torch.cuda.synchronize()
     with torch.cuda.graph(graph, stream=s_):
         step(bookkeep=False)
-for b in batches:
-    b.advance(1)
 torch.cuda.synchronize()
 e0.record()
 for _ in range(REPS):

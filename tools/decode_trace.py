@@ -46,8 +46,6 @@ with torch.cuda.stream(side):
     torch.cuda.synchronize()
     with torch.cuda.graph(graph, stream=side):
         step(bookkeep=False)
-for b in batches:
-    b.advance(1)
 for _ in range(3):
     graph.replay()
     for b in batches:
