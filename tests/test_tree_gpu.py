@@ -21,6 +21,8 @@ import numpy as np
 import pytest
 import torch
 
+from bars import LSE_TC, OUT_ABS, OUT_REL  # noqa: F401
+
 from golden_util import GOLDEN
 from inputs import make_qkv
 from oracle import infllm2_oracle as O
@@ -111,7 +113,7 @@ def test_tree_attention_sparse_regime_vs_oracle(exact):
     if exact:
         assert np.max(np.abs(got - ref_out)) <= 1e-5
     else:
-        assert np.all(np.abs(got - ref_out) <= 2e-3 + 2e-2 * np.abs(ref_out))
+        assert np.all(np.abs(got - ref_out) <= OUT_ABS + OUT_REL * np.abs(ref_out))
 
 
 def test_tree_validation():
