@@ -497,6 +497,10 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
         b.reserve(extra)
         batches.append(b)
     bound = L + extra
+    # layer i's step L2-prefetches layer i+1's kernel means during its tail
+    # (DecodeBatch.link_next; a hint, results unchanged)
+    for i in range(layers - 1):
+        batches[i].link_next(batches[i + 1])
     q = torch.randn((layers, S, HQ, D), generator=gen, device=dev).to(torch.bfloat16)
     kn = torch.randn((layers, S, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
     vn = torch.randn((layers, S, HKV, D), generator=gen, device=dev).to(torch.bfloat16)

@@ -226,6 +226,12 @@ size_t infllm2_decode_table_bytes(int32_t n_seq);
  * cache is reallocated or its length changes outside infllm2_decode_step. */
 int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens, int32_t n_seq,
                                int32_t hkv, int32_t d, void* table, infllm2_stream_t stream);
+/* Link `table` to the NEXT layer's table of the same sequences (or NULL to
+ * unlink): while a decode step of this layer runs its dependent tail, each
+ * CTA L2-prefetches the piece of the next layer's kernel means it will stream
+ * next (a hint: no effect on results).  Stream-ordered; capture-safe.  The
+ * link is cleared by infllm2_decode_table_build. */
+int infllm2_decode_table_link(void* table, int32_t n_seq, const void* next_table, infllm2_stream_t stream);
 /* Copy the table's device-resident lengths (advanced by every decode step,
  * including graph replays) into host `lens` (n_seq entries); synchronises
  * `stream`.  Lets a caller check its host bookkeeping after replays. */

@@ -79,6 +79,7 @@ SIGNATURES.update({
     "infllm2_decode_table_bytes": (c_sz, [c_i32]),
     "infllm2_decode_table_build": (ctypes.c_int, [ctypes.POINTER(SeqDesc), ctypes.POINTER(c_i64), c_i32, c_i32,
                                                   c_i32, c_vp, c_vp]),
+    "infllm2_decode_table_link": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
     "infllm2_decode_table_lengths": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_i64), c_vp]),
     "infllm2_decode_workspace_bytes": (c_sz, [ctypes.POINTER(Geometry), c_i32, c_i32, c_i64]),
     "infllm2_decode_step": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp,

@@ -302,6 +302,11 @@ int infllm2_decode_table_build(const infllm2_seq_desc* seqs, const int64_t* lens
   return decode_table_build(seqs, lens, n_seq, hkv, d, table, (cudaStream_t)stream);
 }
 
+int infllm2_decode_table_link(void* table, int32_t n_seq, const void* next_table, infllm2_stream_t stream) {
+  if (n_seq <= 0 || !table) return INFLLM2_ERR_SHAPE;
+  return cuda_status(decode_table_link(table, n_seq, const_cast<void*>(next_table), (cudaStream_t)stream));
+}
+
 int infllm2_decode_table_lengths(const void* table, int32_t n_seq, int64_t* lens, infllm2_stream_t stream) {
   if (n_seq <= 0 || !table || !lens) return INFLLM2_ERR_SHAPE;
   return cuda_status(decode_table_lengths(table, n_seq, lens, (cudaStream_t)stream));

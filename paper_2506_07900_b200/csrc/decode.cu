@@ -460,6 +460,14 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
 
 size_t decode_table_bytes(int n_seq) { return table_bytes(n_seq); }
 
+__global__ void decode_table_link_kernel(void** slot, void* next) { *slot = next; }
+
+cudaError_t decode_table_link(void* table, int n_seq, void* next_table, cudaStream_t stream) {
+  const TableView tv = table_view(table, n_seq);
+  decode_table_link_kernel<<<1, 1, 0, stream>>>(tv.next, next_table);
+  return cudaGetLastError();
+}
+
 cudaError_t decode_table_lengths(const void* table, int n_seq, int64_t* lens, cudaStream_t stream) {
   const TableView tv = table_view(const_cast<void*>(table), n_seq);
   const cudaError_t e = cudaMemcpyAsync(lens, tv.len, sizeof(int64_t) * n_seq, cudaMemcpyDeviceToHost, stream);

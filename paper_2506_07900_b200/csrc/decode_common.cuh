@@ -35,6 +35,7 @@ struct TableView {
   int64_t* len;        // OLD length during a step; bumped by the last kernel
   int* counters;       // [n_seq][8] last-CTA-done counters of the scores kernel
   int* fused;          // [n_seq*kMaxHkv][4] per-segment counters, then the CTA-done counter
+  void** next;         // the next layer's table (same sequences), or null: L2 prefetch target
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -49,12 +50,15 @@ __host__ __device__ inline TableView table_view(void* base, int n_seq) {
   t.len = reinterpret_cast<int64_t*>(b + len_off);
   t.counters = reinterpret_cast<int*>(b + len_off + sizeof(int64_t) * n_seq);
   t.fused = t.counters + kMaxHkv * n_seq;
+  const size_t next_off = align_up(len_off + sizeof(int64_t) * n_seq + sizeof(int) * kMaxHkv * n_seq +
+                                       sizeof(int) * (4 * kMaxHkv * n_seq + 4), 16);
+  t.next = reinterpret_cast<void**>(b + next_off);
   return t;
 }
 
 inline size_t table_bytes(int n_seq) {
   return align_up(sizeof(SeqDesc) * n_seq, 128) + sizeof(CUtensorMap) * kMaps * n_seq + sizeof(int64_t) * n_seq +
-         sizeof(int) * kMaxHkv * n_seq + sizeof(int) * (4 * kMaxHkv * n_seq + 4);
+         sizeof(int) * kMaxHkv * n_seq + sizeof(int) * (4 * kMaxHkv * n_seq + 4) + 32;
 }
 
 // Window mean over the cache rows, with row `new_row` taken from `knew` (the

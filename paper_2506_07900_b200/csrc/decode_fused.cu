@@ -104,6 +104,7 @@ struct Params {
   float* lse;
   float zscale;            // log2(e) / sqrt(D)
   int trace;
+  int prefetch;            // 1: L2-prefetch the linked next layer's means (infllm2_decode_table_link)
 };
 
 // One piece's view of one segment.
@@ -469,6 +470,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      void* next_table = p.prefetch ? *tv.next : nullptr;
       for (int sg = cid; sg < nseg; sg += ncl, ++it) {
         Info I;
         seg_info(p, len_s, sg, rank, P, I);
@@ -499,6 +501,22 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (it == 0) trace(p.trace, 1);
+        if (next_table != nullptr) {
+          // this CTA's stream is issued: pull the SAME piece of the next
+          // layer's means (hi + lo rows [r0, r1) of this segment) into L2 while
+          // this layer's dependent tail keeps HBM otherwise idle
+          const TableView tn = table_view(next_table, p.n_seq);
+          Info In;
+          seg_info(p, tn.len, sg, rank, P, In);
+          const SeqDesc dn = tn.desc[In.s];
+          const int64_t off = ((int64_t)In.g * dn.means_cap + In.r0) * kD;
+          const int64_t bytes = (In.r1 - In.r0) * kD * 2;
+          for (int64_t b = 0; b < bytes; b += 32768) {
+            const uint32_t nb = (uint32_t)(bytes - b < 32768 ? bytes - b : 32768);
+            l2_prefetch_bulk(reinterpret_cast<const uint8_t*>(dn.hi + off) + b, nb);
+            l2_prefetch_bulk(reinterpret_cast<const uint8_t*>(dn.lo + off) + b, nb);
+          }
+        }
         for (int t = 0; t < I.t2; ++t) {
           if (tile_owner(I, t) != (int)rank) continue;
           // the K/V row of this step (piece 7) is published with the stage-1 exchange
@@ -1199,6 +1217,10 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t
   p.out_f32 = out_f32;
   p.lse = lse;
   p.zscale = 1.4426950408889634f / sqrtf((float)kD);
+  // L2 prefetch of the linked next layer's means: measured neutral to slightly
+  // slower (the means stream already runs at ~6.2 TB/s; DESIGN §4 K4), so opt-in
+  static const bool pf = getenv("INFLLM2_DECODE_PREFETCH") != nullptr;
+  p.prefetch = pf ? 1 : 0;
   static const bool tr = getenv("INFLLM2_DECODE_TRACE") != nullptr;
   static int launches = 0;
   p.trace = tr ? 1 + (launches++ % kTraceRing) : 0;

@@ -118,6 +118,7 @@ struct Params {
   // LSE + log2(s_c / s); pass 2 unchanged
   int approx;
   int64_t nc_total;
+  int p1hi;                       // experiment (INFLLM2_SELECT_P1HI=1): pass 1 over mu_hi only
   int sc;
   float lse_bias2;
 };
@@ -230,11 +231,12 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           for (int c = 0; c < (pass ? tiles : tiles1); ++c) {
             mbar_wait(mu_empty + stage, phase ^ 1);
             uint8_t* dst = smu + stage * kMuStageBytes;
-            mbar_arrive_expect_tx(mu_full + stage, kMuStageBytes);
+            const bool hi_only = pass == 0 && p.p1hi;
+            mbar_arrive_expect_tx(mu_full + stage, hi_only ? kMuStageBytes / 2 : kMuStageBytes);
 #pragma unroll
             for (int hh = 0; hh < C::kDH; ++hh) {
               tma_load_3d(dst + hh * kMuHalfBytes, mh, mu_full + stage, 64 * hh, c * kNT, grp);
-              tma_load_3d(dst + (C::kDH + hh) * kMuHalfBytes, ml, mu_full + stage, 64 * hh, c * kNT, grp);
+              if (!hi_only) tma_load_3d(dst + (C::kDH + hh) * kMuHalfBytes, ml, mu_full + stage, 64 * hh, c * kNT, grp);
             }
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
@@ -271,7 +273,8 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           if (elect_one()) {
             const uint32_t mu_s = mu_addr + stage * kMuStageBytes;
             const uint32_t d0 = tmem + buf * 256;
-            for (int part = 0; part < 2; ++part) {           // hi, then lo
+            const int parts = (pass == 0 && p.p1hi) ? 1 : 2;
+            for (int part = 0; part < parts; ++part) {       // hi, then lo
               const uint32_t mu_p = mu_s + part * C::kDH * kMuHalfBytes;
               for (int k = 0; k < kD / 16; ++k) {
                 const uint32_t koff = (k >> 2) * 0 + (k & 3) * 32;
@@ -680,6 +683,10 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
   p.units_per_group = (last - p.first_t0) / kQ + 1;
   p.n_units = p.units_per_group * cs.hkv;
   p.zscale = 1.4426950408889634f / sqrtf((float)D);
+  {
+    const char* e = getenv("INFLLM2_SELECT_P1HI");
+    p.p1hi = e && e[0] == '1';
+  }
 #ifdef SEL_PROFILE
   p.dbg = getenv("INFLLM2_SELECT_DBG") ? atoi(getenv("INFLLM2_SELECT_DBG")) : 0;   // experiments only
 #else

@@ -24,6 +24,7 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
 size_t decode_table_bytes(int n_seq);
 int decode_table_build(const infllm2_seq_desc* host, const int64_t* lens, int n_seq, int hkv, int d,
                        void* table_dev, cudaStream_t stream);
+cudaError_t decode_table_link(void* table, int n_seq, void* next_table, cudaStream_t stream);
 cudaError_t decode_table_lengths(const void* table, int n_seq, int64_t* lens, cudaStream_t stream);
 bool decode_supported(const infllm2_geometry& g, int hq, int hkv, int d);
 size_t decode_workspace_bytes(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len);

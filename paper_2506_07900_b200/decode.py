@@ -38,6 +38,7 @@ class DecodeBatch:
         self._table: Optional[torch.Tensor] = None
         self._sig = None
         self._ws: Optional[torch.Tensor] = None   # owned scratch: a captured graph keeps its pointer
+        self._next: Optional["DecodeBatch"] = None
         self._lib = _lib.load()
 
     def _signature(self):
@@ -64,6 +65,26 @@ class DecodeBatch:
                                                         self.layers[0].head_dim, self._table.data_ptr(),
                                                         _stream(self.device)), "decode table")
         self._sig = sig
+        self._write_link()
+
+    def _write_link(self) -> None:
+        nxt = self._next._table.data_ptr() if self._next is not None and self._next._table is not None else None
+        _lib.check(self._lib.infllm2_decode_table_link(self._table.data_ptr(), len(self.layers), nxt,
+                                                       _stream(self.device)), "decode table link")
+
+    def link_next(self, nxt: Optional["DecodeBatch"]) -> None:
+        """Declare the batch of the NEXT layer (same sequences, stepped right
+        after this one): this layer's decode step then L2-prefetches the part
+        of the next layer's kernel means each CTA streams next, during its own
+        dependent tail.  A performance hint only (results are unchanged); the
+        next batch's table must exist (call its reserve() first)."""
+        if nxt is not None:
+            if len(nxt.layers) != len(self.layers) or nxt.device != self.device:
+                raise ValidationError("linked decode batches must hold the same number of sequences on one device")
+            nxt._ensure()
+        self._next = nxt
+        self._ensure()
+        self._write_link()
 
     def _fused_ok(self, hq: int, hkv: int, d: int) -> bool:
         """The library's own predicate (infllm2_decode_supported: G = 16, D = 128,

@@ -29,6 +29,8 @@ for layer in range(4):          # 4 layers, one graph: the trace ring holds all 
     b = P.DecodeBatch(caches, cfg)
     b.reserve(32)
     batches.append(b)
+for i in range(3):                # layer i prefetches layer i+1's means (INFLLM2_DECODE_PREFETCH=1: on)
+    batches[i].link_next(batches[i + 1])
 q = torch.randn((S, 32, 128), generator=g, device="cuda").to(torch.bfloat16)
 kn = torch.randn((S, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
 
