@@ -111,6 +111,22 @@ int infllm2_compress(const void* k_cache, int64_t cap, int32_t hkv, int32_t d,
                      float* means, void* means_hi, void* means_lo, int64_t means_cap,
                      infllm2_stream_t stream);
 
+/* Fused append + re-sync of the fine (stride s) and coarse (stride s_c) kernel
+ * means in ONE streaming pass (the prefill path of LayerCache.append +
+ * BlockizedLayerCache.notify_append, model.py:322-336, sparse.py:111-133):
+ * with n_new > 0 the rows [l_old, l_new = l_old + n_new) are read from k_new /
+ * v_new (as infllm2_append_kv) and written to the cache while the dirty
+ * windows are recomputed from the staged rows; with n_new = 0 it re-syncs
+ * after a truncate (l_new < l_old) or rebuilds (l_old = 0).  fine_count_old /
+ * coarse_count_old are the windows valid before the call (F18 clip).  coarse
+ * (and its hi/lo split) may be NULL.  Bitwise equal to build_kernels. */
+int infllm2_append_compress(void* k_cache, void* v_cache, int64_t cap, int32_t hkv, int32_t d, const void* k_new,
+                            const void* v_new, int64_t n_new, int64_t src_row_stride, int32_t src_is_f32,
+                            int64_t l_old, int64_t l_new, int64_t fine_count_old, int64_t coarse_count_old,
+                            int32_t kernel_size, int32_t stride, int32_t coarse_stride, float* fine, void* fine_hi,
+                            void* fine_lo, int64_t fine_cap, float* coarse, void* coarse_hi, void* coarse_lo,
+                            int64_t coarse_cap, infllm2_stream_t stream);
+
 /* Workspace for infllm2_select / infllm2_forward (bytes). */
 size_t infllm2_select_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hq,
                                       int32_t hkv, int32_t d, int64_t cache_len, int32_t flags);

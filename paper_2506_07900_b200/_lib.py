@@ -45,6 +45,9 @@ SIGNATURES = {
                                          c_i32, c_i64, c_vp]),
     "infllm2_compress": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_i64, c_i64, c_i64, c_i32, c_i32,
                                         c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "infllm2_append_compress": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_i64, c_i32,
+                                               c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                               c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "infllm2_select_workspace_bytes": (c_sz, [ctypes.POINTER(Geometry), c_i64, c_i32, c_i32, c_i32,
                                               c_i64, c_i32]),
     "infllm2_select": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,

@@ -133,8 +133,62 @@ int infllm2_compress(const void* k_cache, int64_t cap, int32_t hkv, int32_t d, i
   if (first > count) first = count;
   if (first > means_count_old) first = means_count_old;  // F18: windows that never existed
   if (first < 0) first = 0;
+  if (first >= count) return INFLLM2_OK;
+  // the vectorised streaming kernel when the shape allows (d % 8, p >= stride, alignment)
+  const cudaError_t e = launch_append_compress(const_cast<void*>(k_cache), nullptr, cap, hkv, d, nullptr, nullptr, 0, 0,
+                                               0, l_new, l_new, first, count, 0, 0, kernel_size, stride, stride, means,
+                                               means_hi, means_lo, means_cap, nullptr, nullptr, nullptr, 0,
+                                               (cudaStream_t)stream);
+  if (e != cudaErrorNotSupported) return cuda_status(e);
   return cuda_status(launch_compress(k_cache, cap, hkv, d, first, count, l_new, kernel_size, stride,
                                      means, means_hi, means_lo, means_cap, (cudaStream_t)stream));
+}
+
+int infllm2_append_compress(void* k_cache, void* v_cache, int64_t cap, int32_t hkv, int32_t d, const void* k_new,
+                            const void* v_new, int64_t n_new, int64_t src_row_stride, int32_t src_is_f32,
+                            int64_t l_old, int64_t l_new, int64_t fine_count_old, int64_t coarse_count_old,
+                            int32_t kernel_size, int32_t stride, int32_t coarse_stride, float* fine, void* fine_hi,
+                            void* fine_lo, int64_t fine_cap, float* coarse, void* coarse_hi, void* coarse_lo,
+                            int64_t coarse_cap, infllm2_stream_t stream) {
+  if (kernel_size <= 0 || stride <= 0 || coarse_stride <= 0 || hkv <= 0 || d <= 0) return INFLLM2_ERR_CONFIG;
+  if (n_new < 0 || l_old < 0 || l_new < 0 || l_new > cap) return INFLLM2_ERR_CAPACITY;
+  if (n_new > 0 && (l_new != l_old + n_new || !k_new || !v_new)) return INFLLM2_ERR_SHAPE;
+  if ((fine_hi == nullptr) != (fine_lo == nullptr) || (coarse_hi == nullptr) != (coarse_lo == nullptr))
+    return INFLLM2_ERR_SHAPE;
+  const int64_t count_f = l_new / stride, count_c = l_new / coarse_stride;
+  if (count_f > fine_cap || (coarse && count_c > coarse_cap)) return INFLLM2_ERR_CAPACITY;
+  // boundary = old length on append, new length on truncate (sparse.py:129-133)
+  const int64_t boundary = l_new >= l_old ? l_old : l_new;
+  auto first_of = [&](int32_t st, int64_t count, int64_t count_old) {
+    int64_t f = first_dirty_window(boundary, kernel_size, st);
+    if (f > count) f = count;
+    if (f > count_old) f = count_old;   // F18: windows that never existed
+    return f < 0 ? (int64_t)0 : f;
+  };
+  const int64_t f0 = first_of(stride, count_f, fine_count_old);
+  const int64_t c0 = first_of(coarse_stride, count_c, coarse_count_old);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_append_compress(k_cache, v_cache, cap, hkv, d, k_new, v_new, n_new, src_row_stride,
+                                         src_is_f32, l_old, l_new, f0, count_f, c0, coarse ? count_c : 0, kernel_size,
+                                         stride, coarse_stride, fine, fine_hi, fine_lo, fine_cap, coarse, coarse_hi,
+                                         coarse_lo, coarse_cap, st);
+  if (e != cudaErrorNotSupported) return cuda_status(e);
+  // outside the vectorised envelope: copy, then one re-sync pass per stride
+  if (n_new > 0) {
+    e = launch_append_kv(k_cache, v_cache, cap, hkv, d, k_new, v_new, n_new, src_row_stride, src_is_f32, l_old, st);
+    if (e != cudaSuccess) return INFLLM2_ERR_CUDA;
+  }
+  if (f0 < count_f) {
+    e = launch_compress(k_cache, cap, hkv, d, f0, count_f, l_new, kernel_size, stride, fine, fine_hi, fine_lo,
+                        fine_cap, st);
+    if (e != cudaSuccess) return INFLLM2_ERR_CUDA;
+  }
+  if (coarse && c0 < count_c) {
+    e = launch_compress(k_cache, cap, hkv, d, c0, count_c, l_new, kernel_size, coarse_stride, coarse, coarse_hi,
+                        coarse_lo, coarse_cap, st);
+    if (e != cudaSuccess) return INFLLM2_ERR_CUDA;
+  }
+  return INFLLM2_OK;
 }
 
 size_t infllm2_select_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hq, int32_t hkv,

@@ -73,6 +73,12 @@ struct CoarseArgs {
   int64_t cap;
   int64_t nc_total;        // cache_len // s_c (>= 1)
 };
+cudaError_t launch_append_compress(void* k_cache, void* v_cache, int64_t cap, int hkv, int d, const void* k_new,
+                                   const void* v_new, int64_t n_new, int64_t src_row_stride, int src_f32,
+                                   int64_t l_old, int64_t l_new, int64_t jf0, int64_t count_f, int64_t c0,
+                                   int64_t count_c, int p, int s, int sc, float* fine, void* fine_hi, void* fine_lo,
+                                   int64_t fine_cap, float* coarse, void* coarse_hi, void* coarse_lo,
+                                   int64_t coarse_cap, cudaStream_t stream);
 size_t select_simt_workspace(int64_t items, int64_t nk_total, int64_t nb_max);
 bool select_dense_regime(const infllm2_geometry& g, const CallShape& cs);
 cudaError_t launch_select_dense(const infllm2_geometry& g, const CallShape& cs, int32_t* selection,

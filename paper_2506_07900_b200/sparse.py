@@ -274,15 +274,12 @@ class BlockizedLayerCache:
         if k.dtype != v.dtype:
             v = v.to(k.dtype)
         n = k.shape[0]
+        if n == 0:
+            return
         self._reserve(self.length + n)
-        lib = _lib.load()
-        _lib.check(lib.infllm2_append_kv(
-            _ptr(self._k), _ptr(self._v), self._cap, self.n_kv_heads, self.head_dim,
-            _ptr(k), _ptr(v), n, self.n_kv_heads * self.head_dim,
-            1 if k.dtype == torch.float32 else 0, self.length, _stream(self.device)), "append")
-        old = self.length
-        self.length = old + n
-        self.notify_append(old)
+        # one streaming pass: the new rows enter the cache and the dirty fine and
+        # coarse windows are recomputed from the same staged rows
+        self._sync(self.length, self.length + n, k, v)
 
     def truncate(self, new_length: int) -> None:
         if not 0 <= new_length <= self.length:
@@ -293,26 +290,30 @@ class BlockizedLayerCache:
             self.notify_truncate(old)
 
     def notify_append(self, old_length: int) -> None:
-        self._resync(old_length)
+        """Re-sync after rows [old_length, length) were written externally."""
+        self._sync(old_length, self.length)
 
     def notify_truncate(self, old_length: int) -> None:
-        self._resync(old_length)
+        self._sync(old_length, self.length)
 
-    def _resync(self, l_old: int) -> None:
+    def _sync(self, l_old: int, l_new: int, k_new=None, v_new=None) -> None:
+        """infllm2_append_compress: append k_new/v_new (if given) at l_old and
+        recompute the dirty fine + coarse windows (sparse.py:111-133)."""
         lib = _lib.load()
         cfg = self.config
         st = _stream(self.device)
         split_full = self._nc_split >= self._nc_valid
-        _lib.check(lib.infllm2_compress(
-            _ptr(self._k), self._cap, self.n_kv_heads, self.head_dim, l_old, self.length,
-            self._nk_valid, cfg.kernel_size, cfg.kernel_stride, _ptr(self._fine), _ptr(self._fine_hi),
-            _ptr(self._fine_lo), self._fine.shape[1], st), "compress fine")
-        _lib.check(lib.infllm2_compress(
-            _ptr(self._k), self._cap, self.n_kv_heads, self.head_dim, l_old, self.length,
-            self._nc_valid, cfg.kernel_size, cfg.coarse_stride, _ptr(self._coarse), _ptr(self._coarse_hi),
-            _ptr(self._coarse_lo), self._coarse.shape[1], st), "compress coarse")
-        self._nk_valid = self.length // cfg.kernel_stride
-        self._nc_valid = self.length // cfg.coarse_stride
+        n_new = 0 if k_new is None else k_new.shape[0]
+        f32 = 1 if (k_new is not None and k_new.dtype == torch.float32) else 0
+        _lib.check(lib.infllm2_append_compress(
+            _ptr(self._k), _ptr(self._v), self._cap, self.n_kv_heads, self.head_dim, _ptr(k_new), _ptr(v_new),
+            n_new, self.n_kv_heads * self.head_dim, f32, l_old, l_new, self._nk_valid, self._nc_valid,
+            cfg.kernel_size, cfg.kernel_stride, cfg.coarse_stride, _ptr(self._fine), _ptr(self._fine_hi),
+            _ptr(self._fine_lo), self._fine.shape[1], _ptr(self._coarse), _ptr(self._coarse_hi),
+            _ptr(self._coarse_lo), self._coarse.shape[1], st), "append/compress")
+        self.length = l_new
+        self._nk_valid = l_new // cfg.kernel_stride
+        self._nc_valid = l_new // cfg.coarse_stride
         self._nc_split = self._nc_valid if split_full else min(self._nc_split, self._nc_valid)
 
     def _coarse_split(self) -> None:
