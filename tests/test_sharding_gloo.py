@@ -51,8 +51,9 @@ def _worker(rank, world, port, seq, out_q):
         v_local = [full_v[lo:hi] for lo, hi in chunks]
         cache = _FakeCache()
         S.fill_layer_cache(cache, k_local, v_local, world)
-        (k, v), = cache.rows
-        ok = torch.equal(k, full_k) and torch.equal(v, full_v)
+        k = torch.cat([kk for kk, _ in cache.rows])
+        v = torch.cat([vv for _, vv in cache.rows])
+        ok = torch.equal(k, full_k) and torch.equal(v, full_v) and len(cache.rows) == world + 1
         q_local = [torch.arange(lo, hi) for lo, hi in chunks]
         outs = S.sharded_prefill(q_local, cache, None, chunks, lambda q, c, cfg, lo: q - lo)
         ok = ok and all(torch.equal(o, torch.arange(0, hi - lo)) for o, (lo, hi) in zip(outs, chunks))
