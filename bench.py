@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-approx", action="store_true", help="skip the opt-in approx-LSE prefill line")
     ap.add_argument("--decode-seqs", type=int, default=8, help="sequences per GPU (configs[3]: 64 over 8 GPUs)")
+    ap.add_argument("--decode-microbatches", type=int, default=1,
+                    help="sequence micro-batches per GPU, each on its own stream (1 = one batch per layer)")
     return ap.parse_args()
 
 
@@ -486,11 +488,13 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
     import torch
 
     S, L, layers = args.decode_seqs, args.seq, args.layers
+    mb = max(1, min(args.decode_microbatches, S))       # sequence micro-batches, one stream each
     # rows every cache gains over the leg: 1 eager warm step + `warmup` graph
     # replays + `steps` timed replays + `steps` eager e2e steps (+ margin)
     extra = 1 + args.warmup + 2 * args.steps + 8
     gen = torch.Generator(device=dev)
-    batches = []
+    bounds = [(m * S // mb, (m + 1) * S // mb) for m in range(mb)]
+    batches = [[] for _ in range(mb)]       # [micro-batch][layer]
     for layer in range(layers):
         caches = []
         for s in range(S):
@@ -500,38 +504,49 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
             v = torch.randn((L, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
             c.append(k, v)
             caches.append(c)
-        b = P.DecodeBatch(caches, cfg)
-        b.reserve(extra)
-        batches.append(b)
+        for m, (lo, hi) in enumerate(bounds):
+            b = P.DecodeBatch(caches[lo:hi], cfg, concurrent=mb)
+            b.reserve(extra)
+            batches[m].append(b)
+    all_batches = [b for row in batches for b in row]
     bound = L + extra
-    # layer i's step L2-prefetches layer i+1's kernel means during its tail
-    # (DecodeBatch.link_next; a hint, results unchanged)
-    for i in range(layers - 1):
-        batches[i].link_next(batches[i + 1])
     q = torch.randn((layers, S, HQ, D), generator=gen, device=dev).to(torch.bfloat16)
     kn = torch.randn((layers, S, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
     vn = torch.randn((layers, S, HKV, D), generator=gen, device=dev).to(torch.bfloat16)
-    outs = [None] * layers
+    outs = [[None] * layers for _ in range(mb)]
+    streams = [torch.cuda.Stream(dev) for _ in range(mb)]
 
-    def step(bookkeep=True):
-        for i, b in enumerate(batches):
-            outs[i] = b.step(q[i], kn[i], vn[i], max_len=bound, bookkeep=bookkeep)
+    def step(qq, kk, vv, bookkeep=True):
+        """One decode step of all S sequences through all layers.  Micro-batch m
+        runs its layers in order on its own stream (layer l+1 after layer l, as
+        a model requires); the micro-batches are independent, so one's
+        dependent tail overlaps another's means stream."""
+        cur = torch.cuda.current_stream(dev)
+        for m, st in enumerate(streams):
+            st.wait_stream(cur)
+            lo, hi = bounds[m]
+            with torch.cuda.stream(st):
+                for i in range(layers):
+                    outs[m][i] = batches[m][i].step(qq[i, lo:hi], kk[i, lo:hi], vv[i, lo:hi], max_len=bound,
+                                                    bookkeep=bookkeep)
+        for st in streams:
+            cur.wait_stream(st)
 
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
     graph = torch.cuda.CUDAGraph()
     lib = P._lib.load()
     with torch.cuda.stream(side):
-        step()
+        step(q, kn, vn)
         torch.cuda.synchronize(dev)
         n0 = lib.infllm2_launch_count()
         with torch.cuda.graph(graph, stream=side):
-            step(bookkeep=False)
+            step(q, kn, vn, bookkeep=False)
         launches_per_step = lib.infllm2_launch_count() - n0
     # the capture executed nothing: host and device lengths are still equal
     for _ in range(args.warmup):
         graph.replay()
-        for b in batches:
+        for b in all_batches:
             b.advance(1)
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -541,7 +556,7 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
         graph.replay()
     t1.record()
     barrier()
-    for b in batches:
+    for b in all_batches:
         b.advance(args.steps)
     ms = t0.elapsed_time(t1)
     # e2e: per step H2D of every layer's q/k/v from pinned host memory and D2H
@@ -556,10 +571,9 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
     te0.record()
     for _ in range(args.steps):
         qd, kd, vd = hq_.to(dev, non_blocking=True), hk_.to(dev, non_blocking=True), hv_.to(dev, non_blocking=True)
-        o = None
-        for i, b in enumerate(batches):
-            o = b.step(qd[i], kd[i], vd[i], max_len=bound)
-        out_host.copy_(o, non_blocking=True)
+        step(qd, kd, vd)
+        for m, (lo, hi) in enumerate(bounds):      # the last layer's output of every sequence
+            out_host[lo:hi].copy_(outs[m][layers - 1], non_blocking=True)
     te1.record()
     barrier()
     ms_e2e = te0.elapsed_time(te1)
@@ -591,8 +605,10 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
                     "h2d_bytes_per_step": int((q.numel() + kn.numel() + vn.numel()) * 2),
                     "d2h_bytes_per_step": int(out_host.numel() * 2)},
             "gpu_launches_per_step": int(launches_per_step),
-            "graph": f"{layers}-layer step captured once ({launches_per_step // max(1, layers)} launch(es) per layer: "
-                     "fused cluster kernel), replayed per step"}
+            "microbatches": mb,
+            "graph": f"{layers}-layer step captured once ({launches_per_step // max(1, layers * mb)} launch(es) per "
+                     f"layer and micro-batch: fused cluster kernel; {mb} sequence micro-batch(es) on their own "
+                     "streams, pipelined across layers), replayed per step"}
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle)

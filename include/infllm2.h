@@ -76,8 +76,12 @@ enum {
   INFLLM2_FLAG_EXACT_SIMT = 1 << 0,  /* force the CUDA-core float64 scorer (verifier) */
   INFLLM2_FLAG_CHECK_FINITE = 1 << 1,/* report non-finite q / means (costs a sync)    */
   INFLLM2_FLAG_OUT_F32 = 1 << 2,     /* `out` is float32 instead of bf16              */
-  INFLLM2_FLAG_P_SPLIT = 1 << 3      /* stage 2: softmax weights as bf16 hi + lo (two PV
+  INFLLM2_FLAG_P_SPLIT = 1 << 3,     /* stage 2: softmax weights as bf16 hi + lo (two PV
                                         MMAs, ~1e-5 outputs) instead of bf16 P          */
+  /* infllm2_decode_step: bits 8..11 = how many decode batches run CONCURRENTLY
+   * on the device (micro-batches on separate streams); the fused kernel then
+   * sizes its thread-block clusters so that many launches are co-resident. */
+  INFLLM2_FLAG_DECODE_SHARE_SHIFT = 8
 };
 
 const char* infllm2_strerror(int code);

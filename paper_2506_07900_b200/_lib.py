@@ -32,6 +32,7 @@ OK = 0
 ERR_CONFIG, ERR_SHAPE, ERR_POSITION, ERR_CAPACITY = -1, -2, -3, -4
 ERR_WORKSPACE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NUMERIC, ERR_EMPTY = -5, -6, -7, -8, -9
 FLAG_EXACT_SIMT, FLAG_CHECK_FINITE, FLAG_OUT_F32, FLAG_P_SPLIT = 1, 2, 4, 8
+DECODE_SHARE_SHIFT = 8          # infllm2_decode_step flags bits 8..11: concurrent decode batches
 
 # Exported symbols and their signatures (restype, argtypes); tests check every
 # symbol declared in include/infllm2.h is exported.

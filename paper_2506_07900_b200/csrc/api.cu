@@ -379,8 +379,11 @@ int infllm2_decode_step(const infllm2_geometry* g, void* table, int32_t n_seq, i
   if (rc) return rc;
   if (n_seq <= 0 || hq <= 0 || hkv <= 0 || hq % hkv || max_len_after < 1) return INFLLM2_ERR_SHAPE;
   if (!decode_supported(*g, hq, hkv, d)) return INFLLM2_ERR_UNSUPPORTED;
+  int share = (flags >> INFLLM2_FLAG_DECODE_SHARE_SHIFT) & 15;
+  if (share < 1) share = 1;
   return decode_step(*g, table, n_seq, max_len_after, hq, hkv, d, q, k_new, v_new, selection, out,
-                     (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0, lse, workspace, workspace_bytes, (cudaStream_t)stream);
+                     (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0, lse, workspace, workspace_bytes, (cudaStream_t)stream,
+                     share);
 }
 
 }  // extern "C"

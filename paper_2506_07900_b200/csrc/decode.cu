@@ -36,10 +36,10 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
                                     float* split_ws, cudaStream_t stream);
 size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel);
 size_t decode_fused_workspace_bytes(int n_seq, int hkv);
-bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int sms);
+bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int share);
 int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
                       const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
-                      int out_f32, float* lse, void* ws, cudaStream_t stream, int sms);
+                      int out_f32, float* lse, void* ws, cudaStream_t stream, int share);
 
 namespace {
 
@@ -563,18 +563,14 @@ size_t decode_workspace_bytes(const infllm2_geometry& g, int n_seq, int hkv, int
 
 int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv, int d,
                 const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32,
-                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream) {
+                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream, int share) {
   DecodeWs w = decode_ws_layout(g, n_seq, hkv, max_len_after, ws);
   if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
   const int max_sel = infllm2_max_selected(&g);
   const TableView tvd = table_view(table, n_seq);
-  {
-    int dev = 0, sms = kNumSMs;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (decode_fused_supported(g, n_seq, hkv, max_len_after, sms))
-      return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
-                               lse, w.fused, stream, sms);
-  }
+  if (decode_fused_supported(g, n_seq, hkv, max_len_after, share))
+    return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
+                             lse, w.fused, stream, share);
   // 1. append + compress (3 CTAs per sequence)
   if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,
                  static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),

@@ -1161,17 +1161,19 @@ static int max_active_clusters(int np) {
 // Cluster size (= pieces per segment): the largest per-round parallelism
 // np / rounds over the sizes whose pieces fit the TMEM-resident z tiles.  On a
 // B200 (1 CTA/SM) 8-CTA clusters reach 15 co-resident clusters, 6-CTA ones 22.
-static int choose_cluster(int nseg, int64_t max_len_after) {
+// `share` launches of this kernel run concurrently (decode micro-batches on
+// separate streams): each may use 1/share of the co-resident clusters.
+static int choose_cluster(int nseg, int64_t max_len_after, int share) {
   const int64_t nb_max = max_len_after / kM + 1;
   static const int forced = getenv("INFLLM2_DECODE_P") ? atoi(getenv("INFLLM2_DECODE_P")) : 0;   // diagnostic
   if (forced >= 3 && forced <= kMaxCl && (nb_max + forced - 1) / forced + 1 <= kMaxPieceBlocks &&
-      max_active_clusters(forced) > 0)
+      max_active_clusters(forced) / share > 0)
     return forced;
   int best = 0;
   double best_score = -1.0;
   for (int np = kMaxCl; np >= 3; --np) {
     if ((nb_max + np - 1) / np + 1 > kMaxPieceBlocks) continue;
-    const int n = max_active_clusters(np);
+    const int n = max_active_clusters(np) / share;
     if (n <= 0) continue;
     const int rounds = (nseg + n - 1) / n;
     const double score = (double)np / rounds;
@@ -1185,20 +1187,18 @@ static int choose_cluster(int nseg, int64_t max_len_after) {
 
 // Host-side eligibility: pieces must fit the TMEM-resident z tiles for every
 // length up to max_len_after and budgets must fit the warp top-k.
-bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int sms) {
-  (void)sms;
+bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int share) {
   if (getenv("INFLLM2_DECODE_LEGACY")) return false;
   if (n_seq > kMaxSeq || n_seq < 1) return false;
   if (g.top_k > kMaxBudget || g.top_k < 1) return false;
   if (infllm2_max_selected(&g) > 96) return false;
-  return choose_cluster(n_seq * hkv, max_len_after) > 0;
+  return choose_cluster(n_seq * hkv, max_len_after, share) > 0;
 }
 
 int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
                       const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
-                      int out_f32, float* lse, void* ws, cudaStream_t stream, int sms) {
+                      int out_f32, float* lse, void* ws, cudaStream_t stream, int share) {
   (void)ws;
-  (void)sms;
   Params p;
   p.table = table;
   p.n_seq = n_seq;
@@ -1230,9 +1230,9 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t
   const uint32_t box[3] = {64, (uint32_t)kG, 1};
   if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
   const int nseg = n_seq * hkv;
-  const int np = choose_cluster(nseg, max_len_after);
+  const int np = choose_cluster(nseg, max_len_after, share);
   if (np <= 0) return INFLLM2_ERR_UNSUPPORTED;
-  int ncl = max_active_clusters(np);
+  int ncl = max_active_clusters(np) / share;
   if (ncl > nseg) ncl = nseg;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;

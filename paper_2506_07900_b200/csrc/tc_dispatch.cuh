@@ -30,5 +30,5 @@ bool decode_supported(const infllm2_geometry& g, int hq, int hkv, int d);
 size_t decode_workspace_bytes(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len);
 int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv, int d,
                 const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32,
-                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream);
+                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream, int share = 1);
 }  // namespace infllm2

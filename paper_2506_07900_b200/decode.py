@@ -25,7 +25,11 @@ from .sparse import BlockizedLayerCache, SparseAttentionConfig, _ptr, _stream, t
 class DecodeBatch:
     """One layer's caches of S sequences, stepped together."""
 
-    def __init__(self, layers: Sequence[BlockizedLayerCache], config: SparseAttentionConfig):
+    def __init__(self, layers: Sequence[BlockizedLayerCache], config: SparseAttentionConfig, *, concurrent: int = 1):
+        """`concurrent`: how many decode batches will run AT THE SAME TIME on
+        this device (micro-batches on separate streams, e.g. two halves of the
+        sequences pipelined across layers): the fused kernel then sizes its
+        thread-block clusters so that many launches are co-resident."""
         if not layers:
             raise ValidationError("empty decode batch")
         l0 = layers[0]
@@ -34,6 +38,9 @@ class DecodeBatch:
                 raise ValidationError("decode batch caches must share head geometry and device")
         self.layers = list(layers)
         self.config = config
+        if not 1 <= int(concurrent) <= 15:
+            raise ValidationError("concurrent must be in 1..15")
+        self.concurrent = int(concurrent)
         self.device = l0.device
         self._table: Optional[torch.Tensor] = None
         self._sig = None
@@ -181,7 +188,7 @@ class DecodeBatch:
             raise ValidationError("max_len below the longest sequence")
         ws_bytes = self._lib.infllm2_decode_workspace_bytes(ctypes.byref(geom), n, l0.n_kv_heads, max_len)
         ws = self._workspace(ws_bytes)
-        flags = _lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0
+        flags = (_lib.FLAG_OUT_F32 if out_dtype == torch.float32 else 0) | (self.concurrent << _lib.DECODE_SHARE_SHIFT)
         _lib.check(self._lib.infllm2_decode_step(
             ctypes.byref(geom), self._table.data_ptr(), n, max_len, hq, l0.n_kv_heads, d, _ptr(qb), _ptr(kb),
             _ptr(vb), _ptr(sel), _ptr(out), _ptr(lse), _ptr(ws), ws.numel(), flags, _stream(dev)), "decode step")

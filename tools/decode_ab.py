@@ -17,9 +17,10 @@ ap.add_argument("--layers", type=int, default=bench.LAYERS)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--decode-seqs", type=int, default=8)
+ap.add_argument("--decode-microbatches", type=int, default=1)
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 cfg = P.SparseAttentionConfig(top_k=16)
 res = bench.run_decode(args, P, cfg, 1, 0, dev, lambda: torch.cuda.synchronize(dev), None)
-print(json.dumps({k: res[k] for k in ("ms_per_step", "us_per_token")} | {"roofline_frac": res["roofline"]["frac"],
+print(json.dumps({k: res[k] for k in ("ms_per_step", "us_per_token", "microbatches")} | {"roofline_frac": res["roofline"]["frac"],
                   "e2e_ms": res["e2e"]["ms_per_step"]}))
