@@ -219,6 +219,25 @@ int infllm2_forward_at(const infllm2_geometry* g, const void* q, int64_t q_row_s
 size_t infllm2_forward_at_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hkv, int64_t position,
                                           int64_t cache_len);
 
+/* Tree-draft verification on the tensor cores with the uint64 packed ancestor
+ * mask (PackedMask specdec.py:117-157, the sparse
+ * counterpart of forward_tree specdec.py:565-625).  The n draft nodes' K/V
+ * rows must already sit in the cache at rows [prefix_len, prefix_len + n)
+ * (written with infllm2_append_kv without advancing the cache length; cap >=
+ * prefix_len + n).  Every node is a query at position prefix_len - 1 (it sees
+ * every cached row): stage 1 selects its prefix blocks (tcgen05; the float64
+ * scorer with INFLLM2_FLAG_EXACT_SIMT), stage 2 attends those blocks AND the
+ * tree rows j whose bit j is set in tree_words[i * words_per_row + j / 64], in
+ * one online softmax.  n <= 1024.  out (n, HQ, D), lse (n, HQ) or NULL. */
+int infllm2_forward_tree(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n, int32_t hq,
+                         int32_t hkv, int32_t d, const void* k_cache, const void* v_cache, int64_t cap,
+                         int64_t prefix_len, const float* fine_means, const void* means_hi, const void* means_lo,
+                         int64_t means_cap, const uint64_t* tree_words, int32_t words_per_row, int32_t* selection,
+                         double* sel_scores, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                         int32_t flags, infllm2_stream_t stream);
+size_t infllm2_forward_tree_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hq, int32_t hkv,
+                                            int32_t d, int64_t prefix_len);
+
 /* ---------------------------------------------------------------- batched decode
  * S sequences (each its own blockized cache of one layer) append one token and
  * attend one query row: BASELINE configs[3].  The reference's decode is the same

@@ -75,6 +75,10 @@ SIGNATURES.update({
     "infllm2_forward_at": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,
                                           c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
                                           c_i32, c_vp]),
+    "infllm2_forward_tree": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_vp,
+                                            c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp,
+                                            c_vp, c_vp, c_vp, c_sz, c_i32, c_vp]),
+    "infllm2_forward_tree_workspace_bytes": (c_sz, [ctypes.POINTER(Geometry), c_i64, c_i32, c_i32, c_i32, c_i64]),
     "infllm2_forward_at_workspace_bytes": (c_sz, [ctypes.POINTER(Geometry), c_i64, c_i32, c_i64, c_i64]),
     "infllm2_dense_attend": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,
                                             c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i32, c_vp]),

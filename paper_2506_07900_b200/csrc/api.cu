@@ -44,6 +44,7 @@ namespace {
 
 constexpr int kMaxHeadDim = 256;
 constexpr int kMaxGroup = 256;
+constexpr int64_t kMaxTreeNodes = 1024;
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? INFLLM2_OK : INFLLM2_ERR_CUDA; }
 
@@ -314,6 +315,51 @@ int infllm2_forward_at(const infllm2_geometry* g, const void* q, int64_t q_row_s
                                         lse, (flags & INFLLM2_FLAG_P_SPLIT) ? 1 : 0, st));
   return cuda_status(launch_attend_simt(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32,
                                         lse, st));
+}
+
+int infllm2_forward_tree(const infllm2_geometry* g, const void* q, int64_t q_row_stride, int64_t n, int32_t hq,
+                         int32_t hkv, int32_t d, const void* k_cache, const void* v_cache, int64_t cap,
+                         int64_t prefix_len, const float* fine_means, const void* means_hi, const void* means_lo,
+                         int64_t means_cap, const uint64_t* tree_words, int32_t words_per_row, int32_t* selection,
+                         double* sel_scores, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                         int32_t flags, infllm2_stream_t stream) {
+  if (prefix_len < 1) return INFLLM2_ERR_POSITION;
+  CallShape cs;
+  int rc = make_shape(g, n > 0 ? 1 : 0, prefix_len - 1, hq, hkv, d, prefix_len, &cs);   // nodes see every cached row
+  if (rc) return rc;
+  if (n == 0) return INFLLM2_OK;
+  if (n > kMaxTreeNodes || !tree_words || words_per_row < (n + 63) / 64) return INFLLM2_ERR_SHAPE;
+  if (prefix_len + n > cap) return INFLLM2_ERR_CAPACITY;   // the draft rows live at [prefix_len, prefix_len + n)
+  cs.n = n;
+  cs.bcast = 1;
+  if (cs.nk_total > means_cap) return INFLLM2_ERR_CAPACITY;
+  if (!tc_attend_supported(*g, cs)) return INFLLM2_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(flags & INFLLM2_FLAG_EXACT_SIMT) && tc_select_supported(*g, cs, means_hi != nullptr)) {
+    rc = cuda_status(launch_select_tc(*g, cs, q, q_row_stride, fine_means, means_hi, means_lo, means_cap, selection,
+                                      sel_scores, workspace, workspace_bytes, st));
+  } else {
+    const size_t need = select_simt_workspace(n * hkv, cs.nk_total, cs.nb_max);
+    if (workspace == nullptr || workspace_bytes < need) return INFLLM2_ERR_WORKSPACE;
+    rc = cuda_status(launch_select_simt(*g, cs, q, q_row_stride, fine_means, means_cap, selection, sel_scores,
+                                        workspace, workspace_bytes, st));
+  }
+  if (rc) return rc;
+  const TreeArgs tree{tree_words, (int)n, words_per_row, prefix_len};
+  return cuda_status(launch_attend_tc(*g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out,
+                                      (flags & INFLLM2_FLAG_OUT_F32) ? 1 : 0, lse,
+                                      (flags & INFLLM2_FLAG_P_SPLIT) ? 1 : 0, st, &tree));
+}
+
+size_t infllm2_forward_tree_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hq, int32_t hkv,
+                                            int32_t d, int64_t prefix_len) {
+  CallShape cs;
+  if (prefix_len < 1 || n <= 0 || make_shape(g, 1, prefix_len - 1, hq, hkv, d, prefix_len, &cs)) return 0;
+  cs.n = n;
+  cs.bcast = 1;
+  const size_t a = select_simt_workspace(n * hkv, cs.nk_total, cs.nb_max);
+  const size_t b = tc_select_workspace(*g, cs, 0);
+  return a > b ? a : b;
 }
 
 size_t infllm2_forward_at_workspace_bytes(const infllm2_geometry* g, int64_t n, int32_t hkv, int64_t position,

@@ -133,6 +133,30 @@ struct Params {
   int64_t parts;
   float* part_o;      // [item][part][16][128]
   float* part_ml;     // [item][part][16][2]
+  // tree-draft verification (infllm2_forward_tree): after its selected prefix
+  // blocks every row also attends the tree rows [tree_row0, tree_row0 +
+  // tree_n) of the cache, row j admitted iff bit j of its packed ancestor mask
+  // (PackedMask, specdec.py:117-157) is set: word j / 64 of tree_words[row]
+  const uint64_t* tree_words;
+  int tree_n, tree_nw;
+  int64_t tree_row0;
+};
+
+// Tiles of one item: prefix tiles (pairs of selected blocks) first, then the
+// tree tiles (pairs of 64-row tree blocks).
+struct Tiles {
+  int nb, tp, tb, tt;
+  __device__ __forceinline__ Tiles(const Params& p, int nb_) : nb(nb_), tp((nb_ + 1) / 2) {
+    tb = p.tree_n > 0 ? (p.tree_n + kM - 1) / kM : 0;
+    tt = (tb + 1) / 2;
+  }
+  __device__ __forceinline__ int total() const { return tp + tt; }
+  __device__ __forceinline__ bool tree(int c) const { return c >= tp; }
+  // 64-row blocks in tile c (1 or 2)
+  __device__ __forceinline__ int blocks(int c) const {
+    const int left = c < tp ? nb - 2 * c : tb - 2 * (c - tp);
+    return left >= 2 ? 2 : 1;
+  }
 };
 
 __device__ __forceinline__ void tile_range(const Params& p, int64_t part, int tiles, int* c0, int* c1) {
@@ -334,9 +358,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const CUtensorMap* mv = p.kv_maps ? p.kv_maps + (int64_t)p.map_stride * i + 1 : &tm_v;
       const CUtensorMap* mm = is_k ? mk : mv;
       const SelRow sr = pf.take(p, w, items, pos, lane);
-      const int nb = sr.nb;
+      const Tiles tl(p, sr.nb);
       int c0, c1;
-      tile_range(p, part, (nb + 1) / 2, &c0, &c1);
+      tile_range(p, part, tl.total(), &c0, &c1);
       if (c0 >= c1) continue;
       const int qb = it & 1;
       const uint32_t q_par = ((it >> 1) & 1) ^ 1;
@@ -349,9 +373,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         for (int hh = 0; hh < C::kDH; ++hh) tma_load_3d(qd + hh * kG * 128, &tm_q, q_full + qb, 64 * hh, grp * kG, (int)i);
       }
       for (int c = c0; c < c1; ++c) {
-        const int nt = (nb - 2 * c) >= 2 ? 2 : 1;
-        const int b0 = sr.get(2 * c);
+        const int nt = tl.blocks(c);
+        const int b0 = sr.get(2 * c < 96 ? 2 * c : 95);
         const int b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
+        const bool tree = tl.tree(c);
         if (lane == 0) {
           ATT_T0(t0w);
           mbar_wait(ring_empty + stage, phase ^ 1);
@@ -359,7 +384,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           mbar_arrive_expect_tx(ring_full + stage, nt * C::kDH * (kM * 128));
           uint8_t* dst = ring + stage * kTileBytes;
           for (int x = 0; x < nt; ++x) {
-            const int row0 = (x ? b1 : b0) * kM;
+            const int row0 = tree ? (int)(p.tree_row0 + (int64_t)kM * (2 * (c - tl.tp) + x)) : (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
 #pragma unroll
             for (int hh = 0; hh < C::kDH; ++hh)
@@ -391,7 +416,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int64_t pos = item_pos(p, i);
       const SelRow sr = pf.take(p, w, items, pos, lane);
       int c0, c1;
-      tile_range(p, part, (sr.nb + 1) / 2, &c0, &c1);
+      tile_range(p, part, Tiles(p, sr.nb).total(), &c0, &c1);
       if (c0 >= c1) continue;
       const int qb = it & 1;
       mbar_wait(q_full + qb, (it >> 1) & 1);
@@ -439,9 +464,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       unit_of(p, w, &item, &part, &i, &grp);
       const int64_t pos = item_pos(p, i);
       const SelRow sr = pf.take(p, w, items, pos, lane);
-      const int nb = sr.nb;
+      const Tiles tl(p, sr.nb);
       int c0, c1;
-      tile_range(p, part, (nb + 1) / 2, &c0, &c1);
+      tile_range(p, part, tl.total(), &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
       for (int c = c0; c < c1; ++c, ++pcount) {
@@ -454,7 +479,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (lane == 0) ATT_ADD(5, v1);
         if (c == c0) mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const int ksteps = (nb - 2 * c) >= 2 ? 8 : 4;
+        const int ksteps = tl.blocks(c) == 2 ? 8 : 4;
         if (elect_one()) {
           const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + (C::kKStages + stage) * kTileBytes),
                                              kHalfBytes, 1024);
@@ -513,9 +538,9 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       ATT_T0(s16);
       const SelRow sr = pf.take(p, w, items, pos, lane);
       if (warp == 2 && lane == 0) ATT_ADD(16, s16);
-      const int nb = sr.nb;
+      const Tiles tl(p, sr.nb);
       int c0, c1;
-      tile_range(p, part, (nb + 1) / 2, &c0, &c1);
+      tile_range(p, part, tl.total(), &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
       const bool splitp = p.p_split || pos < kSplitPBelow;
@@ -545,9 +570,15 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         if (lane == 0) mbar_arrive(s_empty + sslot);
         ATT_T0(s19);
         const int x = row >> 6;
-        const int b0 = sr.get(2 * c), b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
-        bool valid = (2 * c + x) < nb;
-        if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
+        const int b0 = sr.get(2 * c < 96 ? 2 * c : 95), b1 = sr.get(2 * c + 1 < 96 ? 2 * c + 1 : 95);
+        bool valid;
+        if (!tl.tree(c)) {
+          valid = (2 * c + x) < tl.nb;
+          if (valid) valid = (int64_t)(x ? b1 : b0) * kM + (row & 63) <= pos;
+        } else {   // tree row j: admitted by the packed ancestor-or-self mask
+          const int j = kM * (2 * (c - tl.tp) + x) + (row & 63);
+          valid = j < p.tree_n && ((p.tree_words[i * p.tree_nw + (j >> 6)] >> (j & 63)) & 1ull);
+        }
         {
           // z * c2 as packed pairs (FFMA2, zero addend); masked rows -inf by
           // select (a row past the tile's blocks may hold stale smem: NaN)
@@ -705,7 +736,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       if (p.split) {
         const SelRow sr = load_sel(p, item, item_pos(p, i), lane);
         int c0, c1;
-        tile_range(p, part, (sr.nb + 1) / 2, &c0, &c1);
+        tile_range(p, part, Tiles(p, sr.nb).total(), &c0, &c1);
         if (c0 >= c1) {   // empty part: neutral partial for the combine
           if (quad == 0 && lane < kG) {
             p.part_ml[(w * kG + lane) * 2] = -INFINITY;
@@ -866,6 +897,9 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   p.parts = split_ws ? (max_sel + 1) / 2 : 1;
   p.part_o = split_ws;
   p.part_ml = split_ws ? split_ws + n_seq * hkv * p.parts * (kG * kD) : nullptr;
+  p.tree_words = nullptr;
+  p.tree_n = p.tree_nw = 0;
+  p.tree_row0 = 0;
   CUtensorMap tq;
   const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
   const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
@@ -923,7 +957,9 @@ static cudaError_t launch_attend_prefill(const CallShape& cs, const void* q, int
     if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
-    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.cache_len, (uint64_t)cs.hkv};
+    // rows past the cache length are visible only to tree tiles (the draft rows)
+    const uint64_t rows = (uint64_t)(p.tree_n > 0 ? p.tree_row0 + p.tree_n : cs.cache_len);
+    const uint64_t dims[3] = {(uint64_t)D, rows, (uint64_t)cs.hkv};
     const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)cap * D * 2};
     const uint32_t box[3] = {64, (uint32_t)kM, 1};
     if (!encode_tmap_3d_bf16(&tk, k_cache, dims, strides, box)) return cudaErrorInvalidValue;
@@ -958,7 +994,8 @@ bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
 
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q, int64_t q_row_stride,
                              const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
-                             void* out, int out_f32, float* lse, int p_split, cudaStream_t stream) {
+                             void* out, int out_f32, float* lse, int p_split, cudaStream_t stream,
+                             const TreeArgs* tree) {
   Params p;
   p.n = cs.n;
   p.start = cs.start;
@@ -979,6 +1016,10 @@ cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, con
   p.parts = 1;
   p.part_o = nullptr;
   p.part_ml = nullptr;
+  p.tree_words = tree ? tree->words : nullptr;
+  p.tree_n = tree ? tree->n : 0;
+  p.tree_nw = tree ? tree->words_per_row : 0;
+  p.tree_row0 = tree ? tree->row0 : 0;
   if (cs.group == 8 && cs.d == 64) return launch_attend_prefill<8, 64>(cs, q, q_row_stride, k_cache, v_cache, cap, p, stream);
   return launch_attend_prefill<16, 128>(cs, q, q_row_stride, k_cache, v_cache, cap, p, stream);
 }

@@ -119,6 +119,10 @@ struct Params {
   int approx;
   int64_t nc_total;
   int p1hi;                       // experiment (INFLLM2_SELECT_P1HI=1): pass 1 over mu_hi only
+  // broadcast position (tree-draft nodes, infllm2_forward_tree): every row
+  // sits at position bpos; units are 16 consecutive ROWS (start = 0)
+  int bcast;
+  int64_t bpos;
   int sc;
   float lse_bias2;
 };
@@ -130,8 +134,12 @@ __device__ __forceinline__ void unit_coords(const Params& p, int64_t u, int64_t*
   *t0 = p.first_t0 + tile * p.kq;
 }
 
+// position of unit coordinate t (the row's own position, or the broadcast one)
+__device__ __forceinline__ int64_t upos(const Params& p, int64_t t) { return p.bcast ? p.bpos : t; }
+
 // kernel count of query position t (sparse.py:426)
 __device__ __forceinline__ int64_t pos_nk(const Params& p, int64_t t) {
+  t = upos(p, t);
   int64_t nk = t / 16 + 1;
   return nk < p.nk_total ? nk : p.nk_total;
 }
@@ -139,6 +147,7 @@ __device__ __forceinline__ int64_t pos_nk(const Params& p, int64_t t) {
 __device__ __forceinline__ int64_t unit_nk(const Params& p, int64_t t0) { return pos_nk(p, t0 + p.kq - 1); }
 // coarse kernel count of query position t (approx-LSE mode)
 __device__ __forceinline__ int64_t pos_nc(const Params& p, int64_t t) {
+  t = upos(p, t);
   const int64_t nc = t / p.sc + 1;
   return nc < p.nc_total ? nc : p.nc_total;
 }
@@ -146,7 +155,7 @@ __device__ __forceinline__ int64_t pos_nc(const Params& p, int64_t t) {
 __device__ __forceinline__ int64_t pos_n1(const Params& p, int64_t t) { return p.approx ? pos_nc(p, t) : pos_nk(p, t); }
 
 __device__ __forceinline__ int unit_tiles(const Params& p, int64_t t0, int64_t nk) {
-  const int64_t qb = t0 / p.m;
+  const int64_t qb = upos(p, t0) / p.m;
   int64_t need = (qb + 1) * p.kpb;
   if (nk > need) need = nk;
   return (int)((need + kNT - 1) / kNT);
@@ -337,7 +346,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       const int64_t nk = unit_nk(p, t0);
       const int tiles = unit_tiles(p, t0, nk);
       const int tiles1 = p.approx ? (int)((pos_nc(p, t0 + p.kq - 1) + kNT - 1) / kNT) : tiles;
-      const int64_t qb = t0 / p.m;
+      const int64_t qb = upos(p, t0) / p.m;
       const int64_t n_cand = qb + 1;
 
       SEL_T0(tp1);
@@ -567,7 +576,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       int64_t t0;
       int grp;
       unit_coords(p, u, &t0, &grp);
-      const UnitSel us = unit_sel(t0, p.m, p.top_k, p.n_init, p.n_local, p.consume);
+      const UnitSel us = unit_sel(upos(p, t0), p.m, p.top_k, p.n_init, p.n_local, p.consume);
       const float* rbuf = p.rbuf + ((int64_t)blockIdx.x * 2 + (ucount & 1)) * kQ * p.nb_cap;
       mbar_wait(rb_full + (ucount & 1), (ucount >> 1) & 1);
       for (int qi = tw; qi < kQ; qi += kTopkWarps) {
@@ -651,7 +660,7 @@ static bool tc_select_shape(const CallShape& cs, int* kq) {
 }
 
 bool tc_select_supported(const infllm2_geometry& g, const CallShape& cs, bool have_split_means) {
-  if (!have_split_means || !tc_kernels_enabled() || cs.bcast) return false;   // units need consecutive rows
+  if (!have_split_means || !tc_kernels_enabled()) return false;
   int kq;
   if (!tc_select_shape(cs, &kq)) return false;
   if (g.kernel_stride != 16 || g.kernel_size != 32) return false;
@@ -678,8 +687,11 @@ static cudaError_t launch_select_shape(const CallShape& cs, const void* q, int64
   using C = SelCfg<G, D>;
   constexpr int kQ = C::kQ;
   p.kq = kQ;
-  p.first_t0 = cs.start / kQ * kQ;
-  const int64_t last = cs.start + cs.n - 1;
+  p.bcast = cs.bcast;
+  p.bpos = cs.start;
+  if (cs.bcast) p.start = 0;          // unit coordinates are row indices; every row at position bpos
+  p.first_t0 = p.start / kQ * kQ;
+  const int64_t last = p.start + cs.n - 1;
   p.units_per_group = (last - p.first_t0) / kQ + 1;
   p.n_units = p.units_per_group * cs.hkv;
   p.zscale = 1.4426950408889634f / sqrtf((float)D);

@@ -17,10 +17,18 @@ bool dense_tc_supported(const CallShape& cs);
 cudaError_t launch_dense_tc(const CallShape& cs, const void* q, int64_t q_row_stride, const void* k_cache,
                             const void* v_cache, int64_t cap, void* out, int out_f32, float* lse,
                             cudaStream_t stream);
+// Tree-draft rows for stage 2 (infllm2_forward_tree): cache rows [row0, row0 + n)
+// hold the draft nodes' K/V; row i of the call admits tree row j iff bit j of
+// words[i * words_per_row + j / 64] is set.
+struct TreeArgs {
+  const uint64_t* words;
+  int n, words_per_row;
+  int64_t row0;
+};
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q,
                              int64_t q_row_stride, const void* k_cache, const void* v_cache,
                              int64_t cap, const int32_t* selection, void* out, int out_f32,
-                             float* lse, int p_split, cudaStream_t stream);
+                             float* lse, int p_split, cudaStream_t stream, const TreeArgs* tree = nullptr);
 size_t decode_table_bytes(int n_seq);
 int decode_table_build(const infllm2_seq_desc* host, const int64_t* lens, int n_seq, int hkv, int d,
                        void* table_dev, cudaStream_t stream);

@@ -16,9 +16,18 @@ Definition (sparse backend): node i's attention is the log-sum-exp merge of
       position ``base - 1`` (it sees every cached row), and
   (b) dense attention over its ancestor-or-self tree rows;
 which is exactly dense attention over prefix ∪ ancestors when (a) selects every
-block.  (a) is one ``infllm2_forward_at`` call for all nodes (every row at the
-same position: shared candidates and forced set; float64 scorer, tensor-core
-stage 2); (b) is a tiny masked float64 attention.
+block.
+
+Default path: ONE ``infllm2_forward_tree`` call (the n x n
+tree mask travels to the kernel bit-packed in uint64 words).  The draft rows'
+K/V are written into the cache at [length, length + n) without advancing its
+length; stage 1 scores every node at the broadcast position length - 1 on the
+tensor cores (units of 16 nodes share candidates and forced set); stage 2
+gathers each node's selected prefix blocks, then the tree rows, admitting tree
+row j for node i iff bit j of ``words[i]`` is set - (a) and (b) in one online
+softmax, no separate merge.  ``exact=True`` keeps the float64 verifier path:
+``infllm2_forward_at`` (float64 scorer) + a float64 masked tree attention merged
+by log-sum-exp on the host side of the device.
 """
 
 from __future__ import annotations
@@ -102,6 +111,8 @@ def tree_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: SparseAt
     if layer.length == 0:
         raise ValidationError("tree scoring needs a non-empty prefix cache")
     mask.validate()
+    if not exact and _kernel_shape_ok(q.shape[1], layer.n_kv_heads, layer.head_dim, config, n):
+        return _tree_attention_kernel(q, layer, config, k_tree, v_tree, mask, split_p, return_selection)
     dev = layer.device
     base = layer.length
     hq, d = q.shape[1], q.shape[2]
@@ -127,6 +138,54 @@ def tree_attention(q: torch.Tensor, layer: BlockizedLayerCache, config: SparseAt
     m = torch.maximum(l_p, l_t)
     wp, wt = torch.exp(l_p - m), torch.exp(l_t - m)
     out = ((o_p * wp[..., None] + o_t * wt[..., None]) / (wp + wt)[..., None]).float()
+    if return_selection:
+        return out, sel
+    return out
+
+
+def _kernel_shape_ok(hq: int, hkv: int, d: int, config: SparseAttentionConfig, n: int) -> bool:
+    """infllm2_forward_tree's envelope: the tensor-core head geometries
+    (G = 16 / D = 128, G = 8 / D = 64), 64-row blocks, <= 80 selected blocks,
+    <= 1024 nodes.  Other shapes (e.g. the reference's tiny test models) take
+    the float64 path."""
+    if hkv <= 0 or hq % hkv:
+        return False
+    return ((hq // hkv, d) in ((16, 128), (8, 64)) and config.block_size == 64 and config.max_selected <= 80
+            and n <= 1024)
+
+
+def _tree_attention_kernel(q, layer, config, k_tree, v_tree, mask, split_p, return_selection):
+    """infllm2_forward_tree: tcgen05 stage 1 at the broadcast position and one
+    stage-2 pass over the selected prefix blocks plus the mask-admitted tree
+    rows (packed words consumed on the device)."""
+    dev = layer.device
+    n = q.shape[0]
+    base = layer.length
+    hq, d = q.shape[1], q.shape[2]
+    hkv = layer.n_kv_heads
+    if hq % hkv or d != layer.head_dim or k_tree.shape[1:] != (hkv, d):
+        raise ValidationError("tree node heads / head_dim disagree with the cache")
+    lib = _lib.load()
+    layer._reserve(base + n)
+    kt = k_tree.to(device=dev).contiguous()
+    vt = v_tree.to(device=dev, dtype=kt.dtype).contiguous()
+    if kt.dtype not in (torch.bfloat16, torch.float32):
+        kt, vt = kt.float(), vt.float()
+    # the draft rows go to [base, base + n): scratch past the cache length
+    _lib.check(lib.infllm2_append_kv(_ptr(layer._k), _ptr(layer._v), layer._cap, hkv, d, _ptr(kt), _ptr(vt), n,
+                                     hkv * d, 1 if kt.dtype == torch.float32 else 0, base, _stream(dev)), "tree rows")
+    words = torch.as_tensor(np.ascontiguousarray(mask.words).view(np.int64), device=dev)
+    qb = q.to(device=dev, dtype=torch.bfloat16).contiguous()
+    geom = config.geometry()
+    sel = torch.empty((n, hkv, config.max_selected), dtype=torch.int32, device=dev)
+    out = torch.empty((n, hq, d), dtype=torch.float32, device=dev)
+    kc, vc, cap, fine, hi, lo, mcap = layer._device_args()
+    ws = _workspace(dev, lib.infllm2_forward_tree_workspace_bytes(ctypes.byref(geom), n, hq, hkv, d, base))
+    flags = _lib.FLAG_OUT_F32 | (_lib.FLAG_P_SPLIT if split_p else 0)
+    _lib.check(lib.infllm2_forward_tree(ctypes.byref(geom), _ptr(qb), qb.stride(0), n, hq, hkv, d, _ptr(kc), _ptr(vc),
+                                        cap, base, _ptr(fine), _ptr(hi), _ptr(lo), mcap, _ptr(words),
+                                        words.shape[1], _ptr(sel), None, _ptr(out), None, _ptr(ws), ws.numel(),
+                                        flags, _stream(dev)), "tree_attention")
     if return_selection:
         return out, sel
     return out

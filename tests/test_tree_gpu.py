@@ -133,3 +133,37 @@ def test_tree_validation():
     bad = P.PackedMask(words=np.zeros((2, 1), np.uint64), n_nodes=2)
     with pytest.raises(P.ValidationError):
         bad.validate()
+
+
+@pytest.mark.parametrize("n,base,top_k,seed", [(10, 3000, 8, 1), (40, 5000, 16, 2), (100, 4097, 16, 3),
+                                                (130, 9000, 8, 4)])
+def test_tree_kernel_packed_mask_vs_oracle(n, base, top_k, seed):
+    """infllm2_forward_tree (tcgen05 stage 1 at the broadcast position, packed
+    uint64 mask consumed in stage 2) vs the oracle composition and vs the
+    float64 verifier path: selections identical, outputs within the
+    tensor-core bar; > 64 nodes span several mask words and tree tiles."""
+    hq, hkv, d = 32, 2, 128
+    rng = np.random.default_rng(seed)
+    parents = [-1] + [int(rng.integers(-1, i)) for i in range(1, n)]
+    mask = P.PackedMask.from_parents(parents)
+    cfg = P.SparseAttentionConfig(top_k=top_k)
+    geom = O.Geometry(top_k=top_k)
+    _, k, v = make_qkv(600 + seed, base, 1, hq, hkv, d)
+    q, kt, vt = make_qkv(700 + seed, n, n, hq, hkv, d)
+    layer = P.BlockizedLayerCache(hkv, d, cfg)
+    layer.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd, ktd, vtd = (torch.from_numpy(x).cuda() for x in (q, kt, vt))
+    out, sel = P.tree_attention(qd, layer, cfg, ktd, vtd, mask, return_selection=True)
+    assert layer.length == base
+    out_x, sel_x = P.tree_attention(qd, layer, cfg, ktd, vtd, mask, exact=True, return_selection=True)
+    assert torch.equal(sel, sel_x)
+    assert bool(((out - out_x).abs() <= OUT_ABS + OUT_REL * out_x.abs()).all())
+    fine = O.window_means(k, geom.kernel_size, geom.kernel_stride)
+    pick = sorted({0, n - 1, n // 2, min(n - 1, 65)})
+    ref_out, ref_sel = _oracle_tree(q[pick], k, v, fine, geom, kt, vt, mask.to_dense()[pick])
+    assert np.array_equal(sel.cpu().numpy()[pick], ref_sel)
+    got = out.cpu().numpy()[pick]
+    assert np.all(np.abs(got - ref_out) <= OUT_ABS + OUT_REL * np.abs(ref_out))
+    # split_p: the tight bar
+    out_s = P.tree_attention(qd, layer, cfg, ktd, vtd, mask, split_p=True).cpu().numpy()[pick]
+    assert np.max(np.abs(out_s - ref_out)) <= 5e-5
