@@ -53,7 +53,8 @@ def launches(tag):
         a[2] += m.get("dram__bytes_read.sum", 0.0)
         a[3] += m.get("dram__bytes_write.sum", 0.0)
     total = sum(a[1] for a in agg.values())
-    lines = [f"# ncu launch list — `bench.py --seq 32768 --layers 2 --steps 1 --warmup 1 --no-cpu --no-e2e` ({tag})", "",
+    lines = [f"# ncu launch list — `bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-approx --no-decode` "
+             f"(128K, 32 layers; first 700 launches) ({tag})", "",
              "Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
              "--clock-control none -c 400 --csv` (cold-cache, serialised: compare shares, not absolutes).", "",
              "| kernel | launches | total µs | share | DRAM read MB | DRAM write MB |", "|---|---|---|---|---|---|"]
@@ -76,11 +77,13 @@ def raw(rep):
 def ncu_summary(tag):
     lines = [f"# ncu --set full summaries ({tag})", "",
              "Captured with `tools/full_profile.sh` (one 128K prefill layer: `tools/profile_one.py 131072`; one "
-             "batched-decode layer step: `tools/decode_probe.py 8 131072 1`).  ncu-serialised (cold L2): compare "
+             "batched-decode layer step: `tools/decode_probe.py 8 131072 1`; K1: `tools/compress_time.py 131072`, "
+             "first launch = the 128K append + compress, second = a re-sync pass).  ncu-serialised (cold L2): compare "
              "against the bench only as shares.", ""]
     traffic = {"source": f"profiles/{tag}_ncu.md: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per "
                          "launch (tools/full_profile.sh)"}
-    for rep, label in (("prefill128k.ncu-rep", "prefill128k"), ("decode_cluster.ncu-rep", "decode")):
+    for rep, label in (("prefill128k.ncu-rep", "prefill128k"), ("decode_cluster.ncu-rep", "decode"),
+                       ("compress.ncu-rep", "k1")):
         path = os.path.join(OUT, rep)
         if not os.path.exists(path):
             continue
@@ -101,6 +104,9 @@ def ncu_summary(tag):
                 traffic["select_tc_kernel (stage-1)"] = {"bytes_per_launch": tot, "launch": "one 131072-row layer"}
             elif "attend_tc" in name:
                 traffic["attend (stage-2)"] = {"bytes_per_launch": tot, "launch": "one 131072-row layer"}
+            elif "stream_compress" in name and "stream_compress_kernel" not in traffic:
+                traffic["stream_compress_kernel"] = {"bytes_per_launch": tot,
+                                                     "launch": "128K-row prefill append + fine/coarse means"}
             elif "decode_cluster" in name:
                 traffic["decode_cluster_kernel"] = {"bytes_per_launch": tot,
                                                     "launch": "one layer step, 8 sequences x 128K"}
