@@ -302,6 +302,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   float* red = reinterpret_cast<float*>(smem + Smem::red);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // q rows and outputs stream through L2 once; the gathered K/V blocks are
+  // re-read by many items: keep them (DRAM re-fetches of evicted K/V were
+  // ~0.85 GB per 128K layer, ncu r1)
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   ATT_T0(t_kernel);
 #ifdef ATT_PROFILE
   long long att_acc[24];
@@ -370,7 +374,8 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
         mbar_arrive_expect_tx(q_full + qb, kQBytes);
         uint8_t* qd = smem + Smem::q + qb * kQBytes;
 #pragma unroll
-        for (int hh = 0; hh < C::kDH; ++hh) tma_load_3d(qd + hh * kG * 128, &tm_q, q_full + qb, 64 * hh, grp * kG, (int)i);
+        for (int hh = 0; hh < C::kDH; ++hh)
+          tma_load_3d_hint(qd + hh * kG * 128, &tm_q, q_full + qb, 64 * hh, grp * kG, (int)i, pol_stream);
       }
       for (int c = c0; c < c1; ++c) {
         const int nt = tl.blocks(c);
@@ -388,7 +393,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const uint32_t off = x * kM * 128;
 #pragma unroll
             for (int hh = 0; hh < C::kDH; ++hh)
-              tma_load_3d(dst + hh * kHalfBytes + off, mm, ring_full + stage, 64 * hh, row0, grp);
+              tma_load_3d_hint(dst + hh * kHalfBytes + off, mm, ring_full + stage, 64 * hh, row0, grp, pol_keep);
           }
         }
         __syncwarp();
@@ -786,11 +791,11 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       } else if (p.out_f32) {
         float* out = static_cast<float*>(p.out);
 #pragma unroll
-        for (int h = 0; h < kG; ++h) out[obase + h * kD] = o[h] / l[h];
+        for (int h = 0; h < kG; ++h) st_global_hint(out + obase + h * kD, o[h] / l[h], pol_stream);
       } else {
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
 #pragma unroll
-        for (int h = 0; h < kG; ++h) out[obase + h * kD] = __float2bfloat16_rn(o[h] / l[h]);
+        for (int h = 0; h < kG; ++h) st_global_hint(out + obase + h * kD, __float2bfloat16_rn(o[h] / l[h]), pol_stream);
       }
       if (p.lse && quad == 0 && lane < kG)
         p.lse[i * p.hq + grp * kG + lane] = (st[64 + lane] + log2f(lsum_exact(lane))) * 0.6931471805599453f;
