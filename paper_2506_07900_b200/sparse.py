@@ -141,6 +141,7 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 
 
 _WS: dict = {}
+_WS_PER_DEVICE = 4          # scratch buffers kept per device (most recently used streams)
 _WS_CAPTURED: list = []     # buffers a captured CUDA graph may reference: never released
 
 
@@ -157,6 +158,14 @@ def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         _WS[key] = ws
+    else:
+        _WS.pop(key)
+        _WS[key] = ws            # most recently used last
+    # bound the cache when callers churn through streams: a dropped buffer was
+    # allocated on (and is only reused by) its own stream, so freeing is ordered
+    same_dev = [k for k in _WS if k[:2] == key[:2]]
+    for k in same_dev[:-_WS_PER_DEVICE]:
+        del _WS[k]
     if capturing and not any(w is ws for w in _WS_CAPTURED):
         _WS_CAPTURED.append(ws)
     return ws
