@@ -57,7 +57,9 @@ constexpr int kRowsT = 128;            // rows per tile (two blocks)
 #ifndef ATT_KSTAGES
 #define ATT_KSTAGES 2   // K ring 2 + V ring 4: 12.24 vs 12.34 ms (3 + 3) per 128K layer
 #endif
-constexpr int kThreads = 512;          // 0 K TMA, 1 QK, 2..9 softmax, 10 PV, 11..14 epilogue, 15 V TMA
+#ifndef ATT_HS
+#define ATT_HS 2   // softmax head groups per tile row (8B shape): 2 -> 8 softmax warps, 4 -> 16
+#endif
 #ifndef ATT_SLOTS
 #define ATT_SLOTS 6   // 4 / 5 / 6 measured 12.75 / 12.61 / 12.59 ms per 128K layer
 #endif
@@ -96,7 +98,15 @@ struct AttCfg {
   // [kColO + 2Gb, kColO + 2Gb + 2G).
   static constexpr uint32_t kColO = kSlots * 2 * G;
   static constexpr uint32_t kTmemCols = (kSlots + 2) * 2 * G <= 64 ? 64 : (kSlots + 2) * 2 * G <= 128 ? 128 : 256;
-  static constexpr int kSH = G / 2;                               // heads per softmax thread
+  // softmax: kHS head groups x 4 TMEM lane quadrants = 4*kHS warps, kSH heads per thread
+  static constexpr int kHS = G == 16 ? ATT_HS : 2;
+  static constexpr int kSH = G / kHS;                             // heads per softmax thread
+  static constexpr int kSoftWarps = 4 * kHS;
+  // warp roles: 0 K TMA, 1 QK issuer, [2, 2 + kSoftWarps) softmax, then the PV
+  // issuer, 4 epilogue warps (one per TMEM lane quadrant of O^T), the V TMA warp
+  static constexpr int kPvWarp = 2 + kSoftWarps;
+  static constexpr int kVWarp = kPvWarp + 5;
+  static constexpr int kThreads = 32 * (kVWarp + 1);
   struct Smem {
     static constexpr uint32_t kv = 0;
     // D = 64: PV runs M = 128 over a half-width V tile, so the last stage's V
@@ -104,8 +114,8 @@ struct AttCfg {
     static constexpr uint32_t q = kv + (kKStages + kVStages) * kTileBytes + (kDH == 1 ? kHalfBytes : 0);   // 2 buffers
     static constexpr uint32_t p = q + 2 * kQBytes;                // 2 buffers
     static constexpr uint32_t stats = p + 2 * kPBytes;            // [2] x ([4 warps][16] l, [16] M, [4][16] l exact)
-    static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [8 warps][16] reduction scratch
-    static constexpr uint32_t flags = red + 8 * 16 * 4;           // (unused)
+    static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;       // [softmax warps][16] reduction scratch
+    static constexpr uint32_t flags = red + kSoftWarps * 16 * 4;  // (unused)
     static constexpr uint32_t bars = flags + 2 * 8 * 4;
     static constexpr uint32_t total = bars + 88 * 8;
   };
@@ -262,7 +272,7 @@ struct SelPrefetch {
 
 
 template <int G, int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(AttCfg<G, D>::kThreads, 1)
 attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = AttCfg<G, D>;
@@ -318,14 +328,14 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
-      mbar_init(p_full + i, 8);
+      mbar_init(p_full + i, C::kSoftWarps);
       mbar_init(p_empty + i, 1);
       mbar_init(o_full + i, 1);
       mbar_init(o_empty + i, 4);
-      mbar_init(st_full + i, 8);
+      mbar_init(st_full + i, C::kSoftWarps);
       mbar_init(st_empty + i, 4);
     }
-    for (int i = 0; i < kSlots; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, 8); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, C::kSoftWarps); }
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
@@ -340,7 +350,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   pdl_wait();                             // no-op unless launched as a dependent
   const int64_t items = p.n * p.hkv * p.parts;   // work units (item, part)
 
-  if (warp == 0 || warp == 15) {
+  if (warp == 0 || warp == C::kVWarp) {
     // -------------------------------------------------------------- producers
     // warp 0: Q + K tiles into the K ring; warp 15: V tiles into the V ring
     const bool is_k = warp == 0;
@@ -454,7 +464,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       ++it;
     }
-  } else if (warp == 10) {
+  } else if (warp == C::kPvWarp) {
     // -------------------------------------------------------------- PV issuer
     const uint32_t idesc_pv = idesc_bf16_f32_major(128, kG, 1, 1);
     int stage = 0;
@@ -518,12 +528,12 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       }
       ++it;
     }
-  } else if (warp < 10) {
+  } else if (warp < C::kPvWarp) {
     // -------------------------------------------------------------- softmax
     // 8 warps: warps w and w+4 share TMEM lane quadrant w%4 (tile rows); the
     // first four take heads 0..7, the others heads 8..15 of every row.
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;                 // head group 0..kHS-1 (its own 128-thread barrier)
     const int h0 = kSH * half;
     const int ws = warp - 2;                           // scratch row
     const int row = quad * 32 + lane;                  // tile row == TMEM lane
@@ -608,7 +618,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           }
           // the half's 128-thread barrier ORs the votes (bar.red)
           ATT_T0(s1);
-          need = named_bar_or(half ? 3 : 2, 128, over);
+          need = named_bar_or(2 + half, 128, over);
           if (warp == 2 && lane == 0) ATT_ADD(9, s1);
         }
         ATT_T0(s2);
@@ -620,7 +630,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             const float v = warp_reduce_n<kSH>(zz, lane, [](float a, float b) { return fmaxf(a, b); });
             if (reduce_writer_n<kSH>(lane)) red[ws * 16 + reduce_head_n<kSH>(lane)] = v;
           }
-          if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+          named_bar_sync(2 + half, 128);
           float corr[kSH];
           bool any_corr = false;
 #pragma unroll
@@ -635,7 +645,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
             lsx[h] *= (mrun[h] == -INFINITY) ? 0.f : corr[h];
             mrun[h] = mnew;
           }
-          if (half) named_bar_sync(3, 128); else named_bar_sync(2, 128);
+          named_bar_sync(2 + half, 128);
           if (c > c0 && any_corr) {
             // rescale this thread's 8 O^T columns (d lane == row): wait for
             // PV(c-1), whose completion is the next phase of p_empty[its buffer]
@@ -808,7 +818,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   __syncthreads();
 #ifdef ATT_PROFILE
   if (lane == 0 && warp == 1) ATT_ADD(0, t_kernel);
-  if (lane == 0 && warp == 10) ATT_ADD(3, t_kernel);
+  if (lane == 0 && warp == C::kPvWarp) ATT_ADD(3, t_kernel);
   if (lane == 0 && warp == 2) ATT_ADD(7, t_kernel);
   if (lane == 0 && warp == 0) ATT_ADD(14, t_kernel);
 #ifdef ATT_PROFILE
@@ -922,7 +932,7 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(AttCfg<16, 128>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cfg.attrs = attr;
@@ -985,7 +995,7 @@ static cudaError_t launch_attend_prefill(const CallShape& cs, const void* q, int
   if (ctas_cap > 0 && ctas_cap < sms) sms = ctas_cap;
   const int grid = (int)(items < sms ? items : sms);
   count_launch();
-  attend_tc_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  attend_tc_kernel<G, D><<<grid, AttCfg<G, D>::kThreads, smem, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
