@@ -60,6 +60,9 @@ constexpr int kStages = 2;
 #ifndef SEL_POLY
 #define SEL_POLY 0   // of every 4 odd element pairs, how many take 2^x on the FMA pipe
 #endif
+#ifndef SEL_P2N256
+#define SEL_P2N256 1   // pass 2 as one N = 256 MMA per K-step: ~1 % faster than 2 x N = 128 (13.96 vs 14.11 ms per 128K layer)
+#endif
 #ifndef SEL_SPLIT
 #define SEL_SPLIT 1   // 2 (16 epilogue warps, 80 registers): stage 1 alone -6 %, full step equal (clocks drop under sw_power_cap)
 #endif
@@ -255,6 +258,7 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc1 = idesc_bf16_f32(128, 128);
+    [[maybe_unused]] const uint32_t idesc2 = idesc_bf16_f32(128, 256);
     const uint32_t q_addr = smem_u32(sq);
     const uint32_t mu_addr = smem_u32(smu);
     int stage = 0, buf = 0;
@@ -294,12 +298,18 @@ select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
                   umma_f16_ss(d0, sdesc_k_sw128(q_k), sdesc_k_sw128(mu_k), idesc1, acc);
                   umma_f16_ss(d0 + 128, sdesc_k_sw128(q_k + 128 * 128), sdesc_k_sw128(mu_k), idesc1, acc);
                 } else {
+#if SEL_P2N256
+                  // one N = 256 MMA: the mu tile (A) is fetched once per K-step
+                  // instead of twice (12 KB of SMEM operands instead of 16)
+                  umma_f16_ss(d0, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc2, acc);
+#else
                   // N = 256 split into two independent N = 128 accumulators
                   // (columns 0-127 / 128-255), issued alternately: a dependent
                   // N = 256 chain costs ~190 cycles per MMA, two interleaved
                   // N = 128 chains ~75 each (tools/mma_bench.cu)
                   umma_f16_ss(d0, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc1, acc);
                   umma_f16_ss(d0 + 128, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k + 128 * 128), idesc1, acc);
+#endif
                 }
               }
             }
