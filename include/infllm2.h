@@ -91,6 +91,10 @@ int32_t infllm2_max_selected(const infllm2_geometry* g);
 /* Number of kernel launches this library has enqueued since load (host counter;
  * lets callers report how many of the library's kernels ran in a region). */
 uint64_t infllm2_launch_count(void);
+/* Number of batched-decode steps launched with the early means stream (the
+ * stream's previous decode step used another layer's table, so the lengths and
+ * the means tiles are fetched before griddepcontrol.wait; DESIGN §4 K4). */
+uint64_t infllm2_decode_early_count(void);
 
 /* Append n_new rows to the blockized cache at rows [l_old, l_old+n_new).
  * k_new/v_new are (n_new, HKV, D), rows `src_row_stride` elements apart,

@@ -42,6 +42,7 @@ SIGNATURES = {
     "infllm2_validate_geometry": (ctypes.c_int, [ctypes.POINTER(Geometry)]),
     "infllm2_max_selected": (c_i32, [ctypes.POINTER(Geometry)]),
     "infllm2_launch_count": (ctypes.c_uint64, []),
+    "infllm2_decode_early_count": (ctypes.c_uint64, []),
     "infllm2_append_kv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_i64,
                                          c_i32, c_i64, c_vp]),
     "infllm2_compress": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_i64, c_i64, c_i64, c_i32, c_i32,

@@ -71,6 +71,10 @@ int make_shape(const infllm2_geometry* g, int64_t n, int64_t start, int32_t hq, 
 
 }  // namespace
 
+namespace infllm2 {
+long long decode_early_launches();
+}
+
 extern "C" {
 
 const char* infllm2_strerror(int code) {
@@ -92,6 +96,8 @@ const char* infllm2_strerror(int code) {
 int infllm2_version(void) { return 100; }
 
 uint64_t infllm2_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+uint64_t infllm2_decode_early_count(void) { return (uint64_t)infllm2::decode_early_launches(); }
 
 int infllm2_validate_geometry(const infllm2_geometry* g) {
   if (!g) return INFLLM2_ERR_CONFIG;

@@ -18,6 +18,8 @@
 #include <float.h>
 #include <string.h>
 
+#include <mutex>
+#include <unordered_map>
 #include <utility>
 
 #include "common.cuh"
@@ -39,7 +41,7 @@ size_t decode_fused_workspace_bytes(int n_seq, int hkv);
 bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int share);
 int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
                       const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
-                      int out_f32, float* lse, void* ws, cudaStream_t stream, int share);
+                      int out_f32, float* lse, void* ws, cudaStream_t stream, int share, int early);
 
 namespace {
 
@@ -561,6 +563,27 @@ size_t decode_workspace_bytes(const infllm2_geometry& g, int n_seq, int hkv, int
   return decode_ws_layout(g, n_seq, hkv, max_len, nullptr).bytes;
 }
 
+// Which fused decode table the stream's last decode launch used (nullptr: the
+// five-launch path, whose kernels trigger their dependents before their own
+// pdl_wait).  A fused step may read its lengths and means before pdl_wait only
+// when the previous decode launch on the stream was a fused step of ANOTHER
+// table: that step triggers its dependents after its own pdl_wait, so every
+// kernel before it — including this table's previous step — has completed, and
+// it does not write this table.  Kernels of other kinds in between only delay
+// the launch (the append kernels do not use PDL; stage 2 writes no cache).
+static long long g_early_launches = 0;
+static int note_decode_launch(cudaStream_t stream, const void* table) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, const void*> last;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = last.find(stream);
+  const int early = table != nullptr && it != last.end() && it->second != nullptr && it->second != table;
+  last[stream] = table;
+  g_early_launches += early;
+  return early;
+}
+long long decode_early_launches() { return g_early_launches; }
+
 int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv, int d,
                 const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32,
                 float* lse, void* ws, size_t ws_bytes, cudaStream_t stream, int share) {
@@ -568,9 +591,11 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
   const int max_sel = infllm2_max_selected(&g);
   const TableView tvd = table_view(table, n_seq);
-  if (decode_fused_supported(g, n_seq, hkv, max_len_after, share))
+  const bool fused = decode_fused_supported(g, n_seq, hkv, max_len_after, share);
+  const int early = note_decode_launch(stream, fused ? table : nullptr);
+  if (fused)
     return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
-                             lse, w.fused, stream, share);
+                             lse, w.fused, stream, share, early);
   // 1. append + compress (3 CTAs per sequence)
   if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,
                  static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),

@@ -54,10 +54,13 @@ for _ in range(3):
         b.advance(1)
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (ctypes.c_ulonglong * (4 * 160 * 16))()
-lib.infllm2_debug_decode_trace(buf, 4 * 160 * 16)
-ring = np.array(buf, dtype=np.float64).reshape(4, 160, 16)
+buf = (ctypes.c_ulonglong * (4 * 160 * 24))()
+lib.infllm2_debug_decode_trace(buf, 4 * 160 * 24)
+ring = np.array(buf, dtype=np.float64).reshape(4, 160, 24)
 smid = ring[3, :, 11].copy()
+early = ring[:, :, 21].copy()
+print("early flag per launch (CTA 0):", early[:, 0])
+ring[:, :, 21] = 0
 ring[ring == 0] = np.nan
 for i in range(3):
     gap = np.nanmin(ring[i + 1, :, 0]) - np.nanmax(ring[i, :, 10])
@@ -71,9 +74,10 @@ print(f"SM clock inside the kernel: median {np.median(mhz):.0f} MHz (min {mhz.mi
 names = ["start", "prod: stage-1 TMA issued", "epi: stage-1 partial", "epi: segment stage-1 complete",
          "epi: block scores", "epi: local top-k", "merge published", "prod: selection seen",
          "epi: first stage-2 partial", "epi: segment done", "CTA end", "(smid)", "epi: first z tile", "epi: append done",
-         "combine start (after x3)", "-"]
+         "combine start (after x3)", "-", "lengths read", "prod: past pdl_wait", "mma: q ready",
+         "mma: tile 0 ready", "epi: past pdl_wait"]
 for i, n in enumerate(names):
-    if i in (11, 15):
+    if i in (11, 15, 21):
         continue
     col = (t[:, i] - t0) / 1e3
     col = col[~np.isnan(col)]
@@ -91,8 +95,8 @@ fin = np.nan_to_num(t[:144, 2] - t0, nan=0) / 1e3
 cb = (ctypes.c_longlong * (160 * 32))()
 lib.infllm2_debug_decode_cycles(cb, 160 * 32)
 cy = np.array(cb, dtype=np.float64).reshape(160, 32)[:8, :18]
-steps = ["x1->LSE", "LSE->S_j", "S_j->R_b", "R_b->localtopk", "topk->x2", "x2->merge loads", "loads->tau",
-         "tau->filter", "filter->rank", "rank->sel_s", "sel_s->s2_full", "s2_full->tilemax", "tilemax->o_full",
+steps = ["x1->LSE", "LSE->S_j", "S_j->R_b", "R_b->localtopk", "topk->x2", "x2->merge loads", "loads->rank",
+         "(7)", "(8)", "rank->sel_s", "sel_s->s2_full", "s2_full->tilemax", "tilemax->o_full",
          "o_full->partial(unused)", "tiles->x3", "x3->combine loads", "loads->end"]
 d = np.diff(cy, axis=1)
 print("cycles per phase (cluster 0, pieces 0..7):")
