@@ -337,6 +337,20 @@ def run_ours(args):
     roof["stage1_tflops"] = round(sel_tflops, 2)
     roof["stage2_tflops"] = round(att_tflops, 2)
     roof["stage2_gather_GBps"] = round(rows2 * layers * D * 2 * 2 / (t_att / 1e3) / 1e9, 1)
+    # what bounds each stage: stage 1 EXECUTES 4x the algorithmic
+    # MMA work (two passes x the bf16 hi + lo split of the means, for exact
+    # selections); stage 2 moves every gathered K/V byte through shared memory
+    # twice (TMA write + tcgen05 operand read) for only G = 16 heads: 8 FLOP per
+    # shared-memory byte at 128 B/clk/SM caps it at 1024 FLOP/clk/SM
+    sm_mhz = clocks.summary().get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    ceil2 = 1024.0 * n_sm * sm_mhz * 1e6 / 1e12
+    roof["stage1_executed"] = {"mma_work_factor": 4, "tflops": round(4 * sel_tflops, 1),
+                               "frac_of_peak": round(4 * sel_tflops / peak_t, 4)}
+    roof["stage2_smem_ceiling"] = {"tflops": round(ceil2, 1), "at_sm_mhz": sm_mhz,
+                                   "frac_of_ceiling": round(att_tflops / ceil2, 4),
+                                   "model": "128 KB of shared-memory traffic (64 KB TMA writes + 64 KB MMA "
+                                            "operand reads) per 128-key tile of 1.05 MFLOP, 128 B/clk/SM"}
 
     # ---- secondary: the opt-in approx-LSE selection mode,
     # same workload; not the headline (it selects differently from the reference)
