@@ -106,9 +106,7 @@ struct Params {
   int trace;
   int prefetch;            // 1: L2-prefetch the linked next layer's means (infllm2_decode_table_link)
   int early;               // 1: the stream's previous kernel is a fused decode step of ANOTHER table (host-tracked):
-                           // lengths + the means stream may be read before griddepcontrol.wait
-  int early_l2;            // with early: also L2-prefetch the piece's means beyond the shared-memory ring
-  int kv_prefetch;         // L2-prefetch the K/V blocks of each piece's best local candidates (count)
+                           // the lengths and the first means tiles are read before griddepcontrol.wait
 };
 
 // One piece's view of one segment.
@@ -182,7 +180,7 @@ __device__ __forceinline__ int tile_block(const Info& I, const int* sel_s, int t
 // phase of the first segment, read back with infllm2_debug_decode_trace
 // (tools/decode_trace.py).  `on` = launch number + 1; the last kTraceRing
 // launches are kept.
-constexpr int kTracePts = 24;
+constexpr int kTracePts = 16;
 constexpr int kTraceRing = 4;
 constexpr int kTraceCtas = 160;
 __device__ unsigned long long g_trace[kTraceRing * kTraceCtas * kTracePts];
@@ -281,16 +279,8 @@ __device__ void local_topk(const float* r, int64_t base, int lo, int hi, int bud
   const int n = hi - lo;
   if (n <= budget) {
     for (int x = lane; x < budget; x += 32) {
-      if (x < n) {
-        const float v = r[lo + x];
-        int rank = 0;
-        for (int y = 0; y < n; ++y) rank += topk::better(r[lo + y], (int)(base + lo + y), v, (int)(base + lo + x)) ? 1 : 0;
-        out[2 * rank] = v;
-        out[2 * rank + 1] = __int_as_float((int)(base + lo + x));
-      } else {
-        out[2 * x] = -1.f;
-        out[2 * x + 1] = __int_as_float(-1);
-      }
+      out[2 * x] = x < n ? r[lo + x] : -1.f;
+      out[2 * x + 1] = __int_as_float(x < n ? (int)(base + lo + x) : -1);
     }
     return;
   }
@@ -310,14 +300,24 @@ __device__ void local_topk(const float* r, int64_t base, int lo, int hi, int bud
   }
   __syncwarp();
   if (cnt <= cap) {
-    // written sorted: out[2 * rank] (the merge binary-searches the lists)
-    for (int x = lane; x < cnt; x += 32) {
-      const float rk = lkey[x];
-      const int bk = lid[x];
-      int rank = 0;
+    int taken = 0;
+    for (int x0 = 0; x0 < cnt; x0 += 32) {
+      const int x = x0 + lane;
+      bool keep = false;
+      float rk = 0.f;
+      int bk = -1;
+      if (x < cnt) {
+        rk = lkey[x];
+        bk = lid[x];
+        int rank = 0;
 #pragma unroll 8
-      for (int f = 0; f < cnt; ++f) rank += topk::better(lkey[f], lid[f], rk, bk) ? 1 : 0;
-      if (rank < budget) { out[2 * rank] = rk; out[2 * rank + 1] = __int_as_float(bk); }
+        for (int f = 0; f < cnt; ++f) rank += topk::better(lkey[f], lid[f], rk, bk) ? 1 : 0;
+        keep = rank < budget;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      const int pos = taken + __popc(mask & ((1u << lane) - 1u));
+      if (keep) { out[2 * pos] = rk; out[2 * pos + 1] = __int_as_float(bk); }
+      taken += __popc(mask);
     }
   } else {
     // pathological ties: iterative order statistics
@@ -353,18 +353,10 @@ __device__ bool cta_topk(const float* r, int64_t base, int lo, int hi, int budge
   float* lk = scratch + 128;                              // [cap][2]
   const int cap = 256;
   if (n <= budget) {
-    // fewer candidates than the budget: all of them, sorted (the merge binary-searches the lists)
+    // fewer candidates than the budget: all of them (order irrelevant: list not full)
     for (int x = tid; x < budget; x += 128) {
-      if (x < n) {
-        const float v = r[lo + x];
-        int rank = 0;
-        for (int y = 0; y < n; ++y) rank += topk::better(r[lo + y], (int)(base + lo + y), v, (int)(base + lo + x)) ? 1 : 0;
-        out[2 * rank] = v;
-        out[2 * rank + 1] = __int_as_float((int)(base + lo + x));
-      } else {
-        out[2 * x] = -1.f;
-        out[2 * x + 1] = __int_as_float(-1);
-      }
+      out[2 * x] = x < n ? r[lo + x] : -1.f;
+      out[2 * x + 1] = __int_as_float(x < n ? (int)(base + lo + x) : -1);
     }
     return true;
   }
@@ -467,28 +459,31 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
   cluster_sync_all();                    // barrier inits visible to the cluster before any remote arrival
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // Programmatic dependent launch.  Nothing of this step's inputs (q, k_new,
-  // v_new) is read before pdl_wait(); with p.early the lengths and the means
-  // tiles below the dirty window (this table is not written by the previous
-  // kernel, and every earlier kernel has completed: each decode step triggers
-  // its dependents only after its own pdl_wait) are fetched before it, so the
-  // means stream overlaps the previous kernel's dependent tail.  Dependents are
-  // triggered once this CTA's stage-1 stream is consumed (below).
-  if (!p.early) pdl_wait();
+  // Programmatic dependent launch.  No input of this step (q, k_new, v_new)
+  // is read before pdl_wait().  With p.early the lengths and the first means
+  // tiles below the dirty window are read before it: this layer's table is not
+  // written by the previous kernel, and every kernel before that one has
+  // completed (each decode step triggers its dependents only after its own
+  // pdl_wait).
+  if (!p.early) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
   for (int s = threadIdx.x; s < p.n_seq; s += blockDim.x) len_s[s] = tv.len[s];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // the last CTA to read the lengths advances them (every CTA of the grid is
-    // co-resident and reads them once, here): no serial work at kernel exit
+  if (threadIdx.x == 160) {
+    // the last CTA to read the lengths advances them (the grid is co-resident
+    // and every CTA reads them once, above): no serial work at kernel exit
     int* started = tv.fused + 4 * nseg;
     if (publish_arrive(started) == (int)gridDim.x - 1) {
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       *started = 0;
       for (int s = 0; s < p.n_seq; ++s) tv.len[s] = len_s[s] + 1;
     }
-    trace(p.trace, 16);
-    if (p.trace && blockIdx.x < kTraceCtas)
-      g_trace[(((p.trace - 1) % kTraceRing) * kTraceCtas + blockIdx.x) * kTracePts + 21] = p.early;
+  }
+  if (p.early && warp != 0) {
+    pdl_wait();
+    pdl_launch_dependents();
   }
 
   if (warp == 0) {
@@ -498,40 +493,29 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       uint32_t phase = 0;
       int it = 0;
       int pre = 0;                                     // stage-1 tiles of the first segment issued before pdl_wait
-      if (p.early && cid < nseg) {
-        Info I;
-        seg_info(p, len_s, cid, rank, P, I);
-        const CUtensorMap* mhi = tv.maps + (int64_t)kMaps * I.s + 2;
-        const CUtensorMap* mlo = tv.maps + (int64_t)kMaps * I.s + 3;
-        tma_prefetch(mhi);
-        tma_prefetch(mlo);
-        for (int t = 0; t < I.ntiles && t < kStages && t != I.dirty_tile; ++t, ++pre) {
-          mbar_wait(empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(full + stage, kStageBytes);
-          uint8_t* dst = smem + Smem::ring + stage * kStageBytes;
-          const int row = (int)(I.r0 + 128 * t);
-          tma_load_3d(dst, mhi, full + stage, 0, row, I.g);
-          tma_load_3d(dst + kHalf, mhi, full + stage, 64, row, I.g);
-          tma_load_3d(dst + 2 * kHalf, mlo, full + stage, 0, row, I.g);
-          tma_load_3d(dst + 3 * kHalf, mlo, full + stage, 64, row, I.g);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        }
-        // the rest of this piece's means into L2 (a stale dirty window is
-        // harmless there: the append's stores update the L2 lines)
-        const SeqDesc ds = tv.desc[I.s];
-        const int64_t row0 = I.r0 + 128 * (int64_t)pre;
-        if (p.early_l2 && row0 < I.r1) {
-          const int64_t off = ((int64_t)I.g * ds.means_cap + row0) * kD;
-          const int64_t bytes = (I.r1 - row0) * kD * 2;
-          for (int64_t b = 0; b < bytes; b += 32768) {
-            const uint32_t nb = (uint32_t)(bytes - b < 32768 ? bytes - b : 32768);
-            l2_prefetch_bulk(reinterpret_cast<const uint8_t*>(ds.hi + off) + b, nb);
-            l2_prefetch_bulk(reinterpret_cast<const uint8_t*>(ds.lo + off) + b, nb);
+      if (p.early) {
+        if (cid < nseg) {
+          Info I;
+          seg_info(p, len_s, cid, rank, P, I);
+          const CUtensorMap* mhi = tv.maps + (int64_t)kMaps * I.s + 2;
+          const CUtensorMap* mlo = tv.maps + (int64_t)kMaps * I.s + 3;
+          tma_prefetch(mhi);
+          tma_prefetch(mlo);
+          for (int t = 0; t < I.ntiles && t < kStages && t != I.dirty_tile; ++t, ++pre) {
+            mbar_wait(empty + stage, phase ^ 1);
+            mbar_arrive_expect_tx(full + stage, kStageBytes);
+            uint8_t* dst = smem + Smem::ring + stage * kStageBytes;
+            const int row = (int)(I.r0 + 128 * t);
+            tma_load_3d(dst, mhi, full + stage, 0, row, I.g);
+            tma_load_3d(dst + kHalf, mhi, full + stage, 64, row, I.g);
+            tma_load_3d(dst + 2 * kHalf, mlo, full + stage, 0, row, I.g);
+            tma_load_3d(dst + 3 * kHalf, mlo, full + stage, 64, row, I.g);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
+        pdl_wait();
+        pdl_launch_dependents();
       }
-      pdl_wait();
-      trace(p.trace, 17);
       void* next_table = p.prefetch ? *tv.next : nullptr;
       for (int sg = cid; sg < nseg; sg += ncl, ++it) {
         Info I;
@@ -562,10 +546,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           tma_load_3d(dst + 3 * kHalf, mlo, full + stage, 64, row, I.g);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (it == 0) {
-          trace(p.trace, 1);
-          pdl_launch_dependents();
-        }
+        if (it == 0) trace(p.trace, 1);
         if (next_table != nullptr) {
           // this CTA's stream is issued: pull the SAME piece of the next
           // layer's means (hi + lo rows [r0, r1) of this segment) into L2 while
@@ -606,6 +587,9 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
+    } else if (p.early) {
+      pdl_wait();
+      pdl_launch_dependents();
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -617,17 +601,14 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
     uint32_t phase = 0;
     int i2 = 0;
     int it = 0;
-    pdl_wait();
     for (int sg = cid; sg < nseg; sg += ncl, ++it) {
       Info I;
       seg_info(p, len_s, sg, rank, P, I);
       const uint32_t par = it & 1;
       mbar_wait(q_full, par);
-      if (it == 0 && elect_one()) trace(p.trace, 18);
       if (it > 0) mbar_wait(z_free, par ^ 1);      // previous segment's z tiles have been read
       for (int t = 0; t < I.ntiles; ++t) {
         mbar_wait(full + stage, phase);
-        if (it == 0 && t == 0 && elect_one()) trace(p.trace, 19);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t mu_s = smem_u32(smem + Smem::ring + stage * kStageBytes);
@@ -643,7 +624,6 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-      if (it == 0) pdl_launch_dependents();
       int ti = 0;                                      // this piece's tile index within the segment
       for (int t = 0; t < I.t2; ++t) {
         if (tile_owner(I, t) != (int)rank) continue;
@@ -718,17 +698,14 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         // numpy reduce order)
         const int64_t jlo = I.dlo > I.r0 ? I.dlo : I.r0;
         if (jlo < I.r1) {
+          const float knew = __bfloat162float(p.k_new[knew_idx]);
           const int64_t row0 = jlo * kS;
           float x[kP + kS];
-          // the cached rows are not the predecessor's output: with p.early
-          // their loads overlap griddepcontrol.wait
 #pragma unroll
           for (int i = 0; i < kP + kS; ++i) {
             const int64_t r = row0 + i;
             x[i] = r < L && r != I.pos ? __bfloat162float(__ldg(&kg[r * kD + d])) : 0.f;   // LDG, not generic
           }
-          if (it == 0) pdl_wait();
-          const float knew = __bfloat162float(p.k_new[knew_idx]);
 #pragma unroll
           for (int i = 0; i < kP + kS; ++i)
             if (row0 + i == I.pos) x[i] = knew;
@@ -748,10 +725,6 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           };
           emit(jlo, x);
           if (jlo + 1 < I.r1) emit(jlo + 1, x + kS);
-        }
-        if (it == 0) {
-          pdl_wait();
-          if (threadIdx.x == 64) trace(p.trace, 20);
         }
         fence_proxy_async_global();
         mbar_arrive(appended);
@@ -799,7 +772,6 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
             }
           }
         }
-        if (it == 0) pdl_launch_dependents();          // this CTA's means stream is consumed
         warp_reduce16_lse(m, sm, lane);
         if ((lane & 1) == 0) {
           const int h = reduce_head(lane);
@@ -913,16 +885,6 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         }
       }
       named_bar_sync(1, 128);
-      if (!dense && warp == 2 && lane < p.kv_prefetch && lane < I.budget) {
-        // opt-in: the local list's best blocks are the likely global picks;
-        // pull their K/V rows into L2 while the lists are exchanged and merged
-        const int b = __float_as_int(xcand[2 * lane + 1]);
-        if (b >= 0) {
-          const int64_t off = ((int64_t)I.g * ds.cap + (int64_t)b * kM) * kD;
-          l2_prefetch_bulk(ds.k + off, kM * kD * 2);
-          l2_prefetch_bulk(ds.v + off, kM * kD * 2);
-        }
-      }
       if (tid == 0) {
         trace(tr, 5);
         CYC(4);
@@ -1035,33 +997,47 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           lk[2 * x] = kv.x;
           lk[2 * x + 1] = kv.y;
         }
+        if (tid == 0) s_cnt = 0;
         named_bar_sync(1, 128);
         CYC(6);
-        // global rank of every candidate in the union of the P sorted local
-        // lists = its index in its own list + the entries of every other list
-        // that beat it (binary search: a list is sorted best-first, -1 padding
-        // last).  Ids are distinct across lists, so the top `budget` ranks are
-        // exactly 0 .. budget-1 (the union holds the global top-budget).
-        for (int x = tid; x < n; x += 128) {
-          const float key = lk[2 * x];
-          const int id = __float_as_int(lk[2 * x + 1]);
-          if (id < 0) continue;
-          const int own = x / I.budget;
-          int rnk = x - own * I.budget;
-#pragma unroll
-          for (int l = 0; l < kMaxCl; ++l) {
-            if (l >= P || l == own) continue;
-            const float* lst = lk + 2 * l * I.budget;
-            int lo = 0, hi = I.budget;
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              const int bid = __float_as_int(lst[2 * mid + 1]);
-              if (bid >= 0 && topk::better(lst[2 * mid], bid, key, id)) lo = mid + 1;
-              else hi = mid;
-            }
-            rnk += lo;
+        // a full local list's worst key tau_i is <= the global B-th best (that
+        // list alone has B keys >= tau_i): keys < max_i tau_i cannot be chosen
+        float tau = -INFINITY;
+        if (tid < (dense ? 0 : P)) {
+          float mn = INFINITY;
+          bool full_list = true;
+          for (int k = 0; k < I.budget; ++k) {
+            full_list &= __float_as_int(lk[2 * (tid * I.budget + k) + 1]) >= 0;
+            mn = fminf(mn, lk[2 * (tid * I.budget + k)]);
           }
-          if (rnk < I.budget) chosen[rnk] = id;
+          if (full_list) tau = mn;
+        }
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, off));
+        if (tid == 0) red_m[0] = tau;
+        named_bar_sync(1, 128);
+        tau = red_m[0];
+        CYC(7);
+        float* fl = rarr;                                          // filtered (key, id) pairs
+        for (int x = tid; x < n; x += 128) {
+          const float k = lk[2 * x];
+          const int id = __float_as_int(lk[2 * x + 1]);
+          if (id >= 0 && k >= tau) {
+            const int slot = atomicAdd(&s_cnt, 1);
+            fl[2 * slot] = k;
+            fl[2 * slot + 1] = lk[2 * x + 1];
+          }
+        }
+        named_bar_sync(1, 128);
+        const int m = s_cnt;
+        CYC(8);
+        for (int x = tid; x < m; x += 128) {
+          const float rk = fl[2 * x];
+          const int bk = __float_as_int(fl[2 * x + 1]);
+          int rnk = 0;
+#pragma unroll 8
+          for (int y = 0; y < m; ++y) rnk += topk::better(fl[2 * y], __float_as_int(fl[2 * y + 1]), rk, bk) ? 1 : 0;
+          if (rnk < I.budget) chosen[rnk] = bk;          // ranks are distinct: exactly budget writers
         }
         named_bar_sync(1, 128);
         CYC(9);
@@ -1267,11 +1243,6 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t
   Params p;
   static const bool no_early = getenv("INFLLM2_DECODE_NOEARLY") != nullptr;   // diagnostic
   p.early = early && !no_early;
-  static const bool early_l2 = getenv("INFLLM2_DECODE_EARLY_L2") != nullptr;   // diagnostic (A/B)
-  p.early_l2 = early_l2 ? 1 : 0;
-  // diagnostic: measured neutral (stage-2 gathers are not on the critical path)
-  static const int kvpf = getenv("INFLLM2_DECODE_KVPF") ? atoi(getenv("INFLLM2_DECODE_KVPF")) : 0;
-  p.kv_prefetch = kvpf;
   p.table = table;
   p.n_seq = n_seq;
   p.hkv = hkv;
