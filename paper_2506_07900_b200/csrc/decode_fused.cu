@@ -180,7 +180,7 @@ __device__ __forceinline__ int tile_block(const Info& I, const int* sel_s, int t
 // phase of the first segment, read back with infllm2_debug_decode_trace
 // (tools/decode_trace.py).  `on` = launch number + 1; the last kTraceRing
 // launches are kept.
-constexpr int kTracePts = 16;
+constexpr int kTracePts = 24;
 constexpr int kTraceRing = 4;
 constexpr int kTraceCtas = 160;
 __device__ unsigned long long g_trace[kTraceRing * kTraceCtas * kTracePts];
