@@ -1007,10 +1007,50 @@ bool tc_attend_supported(const infllm2_geometry& g, const CallShape& cs) {
   return cs.n > 0;
 }
 
+bool attend_share_range(const infllm2_geometry& g, const CallShape& cs, int p_split, bool tree, int64_t* row0,
+                        int64_t* row1);
+cudaError_t launch_attend_share(const CallShape& cs, int64_t row0, int64_t row1, const void* q, int64_t q_row_stride,
+                                const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
+                                void* out, int out_f32, float* lse, cudaStream_t stream);
+
+static cudaError_t launch_attend_rows(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                                     int64_t q_row_stride, const void* k_cache, const void* v_cache, int64_t cap,
+                                     const int32_t* selection, void* out, int out_f32, float* lse, int p_split,
+                                     cudaStream_t stream, const TreeArgs* tree);
+
 cudaError_t launch_attend_tc(const infllm2_geometry& g, const CallShape& cs, const void* q, int64_t q_row_stride,
                              const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
                              void* out, int out_f32, float* lse, int p_split, cudaStream_t stream,
                              const TreeArgs* tree) {
+  // prefill rows at positions >= 256 of the MiniCPM4 geometry: forced blocks
+  // shared by 4 rows (attend_share.cu); the rows around them here
+  int64_t r0, r1;
+  if (attend_share_range(g, cs, p_split, tree != nullptr, &r0, &r1)) {
+    const size_t ob = out_f32 ? 4 : 2;
+    auto part = [&](int64_t a, int64_t b) -> cudaError_t {
+      if (b <= a) return cudaSuccess;
+      CallShape c2 = cs;
+      c2.start = cs.start + a;
+      c2.n = b - a;
+      return launch_attend_rows(g, c2, static_cast<const __nv_bfloat16*>(q) + a * q_row_stride, q_row_stride,
+                                k_cache, v_cache, cap, selection + a * cs.hkv * cs.max_sel,
+                                static_cast<uint8_t*>(out) + a * cs.hq * cs.d * ob, out_f32,
+                                lse ? lse + a * cs.hq : nullptr, p_split, stream, nullptr);
+    };
+    cudaError_t e = part(0, r0);
+    if (e != cudaSuccess) return e;
+    e = launch_attend_share(cs, r0, r1, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32, lse, stream);
+    if (e != cudaSuccess) return e;
+    return part(r1, cs.n);
+  }
+  return launch_attend_rows(g, cs, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32, lse, p_split,
+                            stream, tree);
+}
+
+static cudaError_t launch_attend_rows(const infllm2_geometry& g, const CallShape& cs, const void* q,
+                                     int64_t q_row_stride, const void* k_cache, const void* v_cache, int64_t cap,
+                                     const int32_t* selection, void* out, int out_f32, float* lse, int p_split,
+                                     cudaStream_t stream, const TreeArgs* tree) {
   Params p;
   p.n = cs.n;
   p.start = cs.start;
