@@ -82,7 +82,7 @@ struct Smem {
   // warp 8 heads x (rounded row sum, exact row sum) of the shared pass
   static constexpr uint32_t stash = red + kSoftWarps * 16 * 4;
   static constexpr uint32_t bars = (stash + kU * (kG + 2 * kSoftWarps * kSH) * 4 + 7) / 8 * 8;
-  static constexpr uint32_t total = bars + 48 * 8;
+  static constexpr uint32_t total = bars + 56 * 8;
 };
 static_assert(Smem::total + 1024 <= 232448, "attend_share shared memory");
 static_assert(2 * kPRow == 64 * kNS * 2, "P^T of the half tile B fills the two row buffers");
@@ -178,13 +178,16 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   uint64_t* st_full = bars + 30;    // [2]
   uint64_t* st_empty = bars + 32;   // [2]
   uint64_t* o_empty = bars + 34;    // [2]
-  uint64_t* o_full = bars + 36;     // one phase per row
+  // O of row u in buffer b is complete: one barrier per (buffer, row), so the
+  // PV issuer (gated per buffer by o_empty) is never two phases ahead of the
+  // epilogue on any of them
+  uint64_t* o_full = bars + 44;     // [2][kU]
   uint64_t* ssh_full = bars + 37;   // shared S^T A and B written
   uint64_t* ssh_empty = bars + 38;  // shared S^T read by the softmax
   uint64_t* psh_full = bars + 39;   // shared P^T (A and B) written
   uint64_t* psh_empty = bars + 40;  // PV of tile A done with P^T A
   uint64_t* osh_done = bars + 41;   // shared PVs done (O of the unit initialised)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 52);
   float* stats = reinterpret_cast<float*>(smem + Smem::stats);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
   float* stash = reinterpret_cast<float*>(smem + Smem::stash);
@@ -204,7 +207,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       mbar_init(o_empty + i, 4);
     }
     for (int i = 0; i < kSlots; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, kSoftWarps); }
-    mbar_init(o_full, 1);
+    for (int i = 0; i < 2 * kU; ++i) mbar_init(o_full + i, 1);
     mbar_init(ssh_full, 1);
     mbar_init(ssh_empty, kSoftWarps);
     mbar_init(psh_full, kSoftWarps);
@@ -399,12 +402,12 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
             umma_commit(v_empty + stage);
             umma_commit(p_empty + pbuf);
-            if (k == tiles - 1) umma_commit(o_full);
+            if (k == tiles - 1) umma_commit(o_full + ob * kU + u);
           }
           __syncwarp();
           if (++stage == kVSt) { stage = 0; vphase ^= 1; }
         }
-        if (tiles == 0 && elect_one()) umma_commit(o_full);   // a row without chosen blocks (budget 0)
+        if (tiles == 0 && elect_one()) umma_commit(o_full + ob * kU + u);   // a row without chosen blocks (budget 0)
         __syncwarp();
       }
     }
@@ -659,7 +662,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const int ob = it & 1;
       for (int u = 0; u < kU; ++u, ++rcount) {
         const int sb = rcount & 1;
-        mbar_wait(o_full, rcount & 1);
+        mbar_wait(o_full + ob * kU + u, (it >> 1) & 1);
         mbar_wait(st_full + sb, (rcount >> 1) & 1);
         tc_fence_after();
         float o[kG], o2[kG];

@@ -102,8 +102,10 @@ def ncu_summary(tag):
             tot = int(nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"))
             if "select_tc" in name:
                 traffic["select_tc_kernel (stage-1)"] = {"bytes_per_launch": tot, "launch": "one 131072-row layer"}
-            elif "attend_tc" in name:
-                traffic["attend (stage-2)"] = {"bytes_per_launch": tot, "launch": "one 131072-row layer"}
+            elif "attend_tc" in name or "attend_share" in name:
+                traffic["attend (stage-2)"] = {"bytes_per_launch": tot, "launch": "one 131072-row layer (rows >= 2048 "
+                                               "on attend_share_kernel)" if "attend_share" in name else
+                                               "one 131072-row layer"}
             elif "stream_compress" in name and "stream_compress_kernel" not in traffic:
                 traffic["stream_compress_kernel"] = {"bytes_per_launch": tot,
                                                      "launch": "128K-row prefill append + fine/coarse means"}
