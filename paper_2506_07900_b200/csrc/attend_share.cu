@@ -47,8 +47,15 @@ constexpr int kD = 128;
 constexpr int kM = 64;
 constexpr int kU = 4;                         // rows per unit (divides kM)
 constexpr int kNS = kG * kU;                  // shared-tile MMA N
-constexpr int kKSt = 2, kVSt = 3;             // K / V ring stages (32 KB each)
-constexpr int kSlots = 6;                     // row-tile S^T slots (16 columns each)
+#ifndef SHARE_KST
+#define SHARE_KST 2
+#endif
+constexpr int kKSt = SHARE_KST, kVSt = 5 - SHARE_KST;   // K / V ring stages (32 KB each)
+#ifndef SHARE_SLOTS
+#define SHARE_SLOTS 6
+#endif
+constexpr int kSlots = SHARE_SLOTS;           // row-tile S^T slots (16 columns each, <= 8)
+static_assert(kSlots <= 8, "S^T slots: TMEM columns [0, 128) and 8 barrier pairs");
 constexpr int kSoftWarps = 8;
 constexpr int kSH = 8;                        // heads per softmax thread
 constexpr int kPvWarp = 2 + kSoftWarps;       // 10
@@ -64,10 +71,10 @@ constexpr uint32_t kQB = 2 * kQHalf;          // 16 KB per Q buffer
 constexpr uint32_t kPRow = 128 * kG * 2;      // 4 KB: P^T of a row tile (128 keys x 16)
 constexpr uint32_t kPSh = 128 * kNS * 2;      // 16 KB: P^T of shared tile A (128 keys x 64)
 
-// TMEM columns: row S^T slots [0, 96), shared S^T A [96, 160), B [160, 224),
+// TMEM columns: row S^T slots [0, 16 kSlots), shared S^T A [128, 192), B [192, 256),
 // O^T double buffer [256, 512): buffer b = [256 + 128 b, +128), O_a(u) at +16u,
 // O_b(u) at +64 + 16u (even / odd K-steps, summed by the epilogue).
-constexpr uint32_t kColSA = kSlots * kG;
+constexpr uint32_t kColSA = 8 * kG;
 constexpr uint32_t kColSB = kColSA + kNS;
 constexpr uint32_t kColO = 256;
 
@@ -82,7 +89,7 @@ struct Smem {
   // warp 8 heads x (rounded row sum, exact row sum) of the shared pass
   static constexpr uint32_t stash = red + kSoftWarps * 16 * 4;
   static constexpr uint32_t bars = (stash + kU * (kG + 2 * kSoftWarps * kSH) * 4 + 7) / 8 * 8;
-  static constexpr uint32_t total = bars + 56 * 8;
+  static constexpr uint32_t total = bars + 80 * 8;
 };
 static_assert(Smem::total + 1024 <= 232448, "attend_share shared memory");
 static_assert(2 * kPRow == 64 * kNS * 2, "P^T of the half tile B fills the two row buffers");
@@ -165,14 +172,14 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
-  uint64_t* k_full = bars + 0;      // [2]
-  uint64_t* k_empty = bars + 2;     // [2]
-  uint64_t* v_full = bars + 4;      // [3]
-  uint64_t* v_empty = bars + 7;     // [3]
+  uint64_t* k_full = bars + 0;      // [kKSt]
+  uint64_t* k_empty = bars + 4;     // [kKSt]
+  uint64_t* v_full = bars + 54;     // [kVSt <= 4]
+  uint64_t* v_empty = bars + 58;    // [kVSt <= 4]
   uint64_t* q_full = bars + 10;     // [2]
   uint64_t* q_empty = bars + 12;    // [2]
-  uint64_t* s_full = bars + 14;     // [6]
-  uint64_t* s_empty = bars + 20;    // [6]
+  uint64_t* s_full = bars + 64;     // [kSlots]
+  uint64_t* s_empty = bars + 72;    // [kSlots]
   uint64_t* p_full = bars + 26;     // [2]
   uint64_t* p_empty = bars + 28;    // [2]
   uint64_t* st_full = bars + 30;    // [2]
