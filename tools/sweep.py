@@ -79,9 +79,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--shapes", default="8B,0.5B")
+    ap.add_argument("--lengths", default="")
+    ap.add_argument("--topks", default="8,16,32,64")
     args = ap.parse_args()
     lengths = [4096, 16384, 65536] if args.quick else [4096, 8192, 16384, 32768, 65536, 131072]
-    ks = [8, 16, 32, 64]
+    if args.lengths:
+        lengths = [int(x) for x in args.lengths.split(",")]
+    ks = [int(x) for x in args.topks.split(",")]
     print("| shape | L | top-k | dense regime | stage 1 ms | stage 2 ms | ms/layer | tok/s (32 layers) |")
     print("|---|---|---|---|---|---|---|---|")
     for name, (hq, hkv, d) in SHAPES.items():
