@@ -351,7 +351,10 @@ def run_ours(args):
     roof["stage2_smem_ceiling"] = {"tflops": round(ceil2, 1), "at_sm_mhz": sm_mhz,
                                    "frac_of_ceiling": round(att_tflops / ceil2, 4),
                                    "model": "128 KB of shared-memory traffic (64 KB TMA writes + 64 KB MMA "
-                                            "operand reads) per 128-key tile of 1.05 MFLOP, 128 B/clk/SM"}
+                                            "operand reads) per 128-key tile of 1.05 MFLOP, 128 B/clk/SM: the "
+                                            "ceiling of a per-row gather (attend_tc); rows >= 2048 share their "
+                                            "forced blocks across 4 rows (attend_share), which lowers the bytes "
+                                            "per FLOP below this model"}
 
     # ---- secondary: the opt-in approx-LSE selection mode,
     # same workload; not the headline (it selects differently from the reference)
