@@ -42,57 +42,68 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kG = 16;
-constexpr int kD = 128;
 constexpr int kM = 64;
-constexpr int kU = 4;                         // rows per unit (divides kM)
-constexpr int kNS = kG * kU;                  // shared-tile MMA N
+constexpr int kNS = 64;                       // shared-tile MMA N = U * G (both geometries)
 #ifndef SHARE_KST
 #define SHARE_KST 2
 #endif
-constexpr int kKSt = SHARE_KST, kVSt = 5 - SHARE_KST;   // K / V ring stages (32 KB each)
 #ifndef SHARE_SLOTS
 #define SHARE_SLOTS 6
 #endif
-constexpr int kSlots = SHARE_SLOTS;           // row-tile S^T slots (16 columns each, <= 8)
+constexpr int kSlots = SHARE_SLOTS;           // row-tile S^T slots (G columns each, <= 8)
 static_assert(kSlots <= 8, "S^T slots: TMEM columns [0, 128) and 8 barrier pairs");
 constexpr int kSoftWarps = 8;
-constexpr int kSH = 8;                        // heads per softmax thread
 constexpr int kPvWarp = 2 + kSoftWarps;       // 10
 constexpr int kVWarp = kPvWarp + 5;           // 15
 constexpr int kThreads = 32 * (kVWarp + 1);   // 512
 constexpr int kMaxSel = 80;
 constexpr int64_t kShareFrom = 2048;          // first position on this kernel
-
 constexpr uint32_t kHalf = 128 * 128;         // 16 KB: 128 rows x 64 d (bf16)
-constexpr uint32_t kTile = 2 * kHalf;         // 32 KB: K or V tile
-constexpr uint32_t kQHalf = kNS * 128;        // 8 KB: U x 16 rows x 64 d
-constexpr uint32_t kQB = 2 * kQHalf;          // 16 KB per Q buffer
-constexpr uint32_t kPRow = 128 * kG * 2;      // 4 KB: P^T of a row tile (128 keys x 16)
-constexpr uint32_t kPSh = 128 * kNS * 2;      // 16 KB: P^T of shared tile A (128 keys x 64)
 
-// TMEM columns: row S^T slots [0, 16 kSlots), shared S^T A [128, 192), B [192, 256),
-// O^T double buffer [256, 512): buffer b = [256 + 128 b, +128), O_a(u) at +16u,
-// O_b(u) at +64 + 16u (even / odd K-steps, summed by the epilogue).
-constexpr uint32_t kColSA = 8 * kG;
+// TMEM columns: row S^T slots [0, G kSlots), shared S^T A [128, 192), B [192, 256),
+// O^T double buffer [256, 512): buffer b = [256 + 128 b, +128), O_a(u) at +G u,
+// O_b(u) at +64 + G u (even / odd K-steps, summed by the epilogue).
+constexpr uint32_t kColSA = 128;
 constexpr uint32_t kColSB = kColSA + kNS;
 constexpr uint32_t kColO = 256;
 
-struct Smem {
-  static constexpr uint32_t kv = 0;                                   // K ring, then V ring
-  static constexpr uint32_t q = kv + (kKSt + kVSt) * kTile;           // [2] Q buffers
-  static constexpr uint32_t prow = q + 2 * kQB;                       // [2] row P^T; P^T of tile B aliases both
-  static constexpr uint32_t psh = prow + 2 * kPRow;                   // P^T of tile A
-  static constexpr uint32_t stats = psh + kPSh;                       // [2] x 9 x 16 floats (as attend_tc.cu)
-  static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;             // [8 warps][16]
-  // per row u of the unit: m[16] (shared-pass max per head), then per softmax
-  // warp 8 heads x (rounded row sum, exact row sum) of the shared pass
-  static constexpr uint32_t stash = red + kSoftWarps * 16 * 4;
-  static constexpr uint32_t bars = (stash + kU * (kG + 2 * kSoftWarps * kSH) * 4 + 7) / 8 * 8;
-  static constexpr uint32_t total = bars + 80 * 8;
+// Per-geometry constants: (G, D) = (16, 128) MiniCPM4-8B, (8, 64) MiniCPM4-0.5B.
+// U = 64 / G rows per unit keep the shared tiles at N = 64.
+template <int G, int D>
+struct SC {
+  static constexpr int kG = G, kD = D;
+  static constexpr int kU = kNS / G;                             // 4 / 8
+  static constexpr int kDH = D / 64;                             // 64-d halves per row
+  static constexpr int kSH = G / 2;                              // heads per softmax thread (two head halves)
+  static constexpr uint32_t kTile = kDH * kHalf;                 // K or V tile (128 rows)
+  // ring: 8B 2 + 3 stages of 32 KB; 0.5B 4 + 6 of 16 KB (+ a 16 KB pad: PV runs
+  // M = 128 over a half-width V tile, its operand spans kHalf past the ring)
+  static constexpr int kKSt = D == 128 ? SHARE_KST : 4;
+  static constexpr int kVSt = D == 128 ? 5 - SHARE_KST : 6;
+  static constexpr uint32_t kPad = D == 64 ? kHalf : 0;
+  static constexpr uint32_t kQHalf = kNS * 128;                  // 8 KB: U x G rows x 64 d
+  static constexpr uint32_t kQB = kDH * kQHalf;
+  static constexpr uint32_t kPRow = 128 * G * 2;                 // P^T of a row tile (128 keys x G)
+  static constexpr uint32_t kPSh = 128 * kNS * 2;                // 16 KB: P^T of shared tile A
+  static constexpr uint32_t kPB = 64 * kNS * 2;                  // 8 KB: P^T of shared tile B (64 keys)
+  static constexpr bool kPBAlias = 2 * kPRow == kPB;             // 8B: B aliases the two row buffers
+  struct Smem {
+    static constexpr uint32_t kv = 0;                                 // K ring, then V ring (+ pad)
+    static constexpr uint32_t q = kv + (kKSt + kVSt) * kTile + kPad;  // [2] Q buffers
+    static constexpr uint32_t prow = q + 2 * kQB;                     // [2] row P^T
+    static constexpr uint32_t pb = kPBAlias ? prow : prow + 2 * kPRow;
+    static constexpr uint32_t psh = pb + (kPBAlias ? 2 * kPRow : kPB);
+    static constexpr uint32_t stats = psh + kPSh;                     // [2] x 9 x 16 floats (as attend_tc.cu)
+    static constexpr uint32_t red = stats + 2 * 9 * 16 * 4;           // [8 warps][16]
+    // per row u of the unit: m[G] (shared-pass max per head), then per softmax
+    // warp kSH heads x (rounded row sum, exact row sum) of the shared pass
+    static constexpr uint32_t stash_row = G + 2 * kSoftWarps * kSH;   // floats
+    static constexpr uint32_t stash = red + kSoftWarps * 16 * 4;
+    static constexpr uint32_t bars = (stash + kU * stash_row * 4 + 7) / 8 * 8;
+    static constexpr uint32_t total = bars + 96 * 8;
+  };
+  static_assert(Smem::total + 1024 <= 232448, "attend_share shared memory");
 };
-static_assert(Smem::total + 1024 <= 232448, "attend_share shared memory");
-static_assert(2 * kPRow == 64 * kNS * 2, "P^T of the half tile B fills the two row buffers");
 
 struct Params {
   int64_t n, start;          // rows [start, start + n): start % U == 0, n % U == 0, start >= kShareFrom
@@ -107,6 +118,7 @@ struct Params {
 // each of the U rows, and each row's chosen-block count.  A row's selection is
 // [0, chosen (ascending, all in [1, qb-1)), qb-1, qb] (force_blocks +
 // select_topk with n_init = 1, n_local = 2), so chosen entry j is index 1 + j.
+template <int kU>
 struct UnitRows {
   int r[kU][3];
   int nch[kU];
@@ -131,17 +143,19 @@ struct UnitRows {
   __device__ __forceinline__ int tiles(int u) const { return (nchosen(u) + 1) >> 1; }
 };
 
+template <int kU>
 __device__ __forceinline__ void unit_of(const Params& p, int64_t w, int* grp, int64_t* i0) {
   const int64_t per = p.n / kU;
   *grp = (int)(w / per);
   *i0 = (w - (int64_t)(*grp) * per) * kU;
 }
 
-__device__ __forceinline__ UnitRows load_unit(const Params& p, int64_t w, int lane) {
+template <int kU>
+__device__ __forceinline__ UnitRows<kU> load_unit(const Params& p, int64_t w, int lane) {
   int grp;
   int64_t i0;
-  unit_of(p, w, &grp, &i0);
-  UnitRows ur;
+  unit_of<kU>(p, w, &grp, &i0);
+  UnitRows<kU> ur;
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const int32_t* s = p.sel + ((i0 + u) * p.hkv + grp) * p.max_sel;
@@ -159,42 +173,51 @@ __device__ __forceinline__ UnitRows load_unit(const Params& p, int64_t w, int la
 }
 
 // Row tile c (0-based, after the two shared tiles) of a unit -> (row u, tile k of that row).
-__device__ __forceinline__ void row_tile(const UnitRows& ur, int c, int* u, int* k) {
+template <int kU>
+__device__ __forceinline__ void row_tile(const UnitRows<kU>& ur, int c, int* u, int* k) {
   int uu = 0;
   while (uu < kU - 1 && c >= ur.tiles(uu)) { c -= ur.tiles(uu); ++uu; }
   *u = uu;
   *k = c;
 }
 
+template <int G, int D>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  using C = SC<G, D>;
+  using Smem = typename C::Smem;
+  constexpr int kG = G, kD = D, kU = C::kU, kDH = C::kDH, kSH = C::kSH;
+  constexpr int kKSt = C::kKSt, kVSt = C::kVSt;
+  constexpr uint32_t kTile = C::kTile, kQHalf = C::kQHalf, kQB = C::kQB, kPRow = C::kPRow;
+  using URows = UnitRows<kU>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
-  uint64_t* k_full = bars + 0;      // [kKSt]
-  uint64_t* k_empty = bars + 4;     // [kKSt]
-  uint64_t* v_full = bars + 54;     // [kVSt <= 4]
-  uint64_t* v_empty = bars + 58;    // [kVSt <= 4]
-  uint64_t* q_full = bars + 10;     // [2]
-  uint64_t* q_empty = bars + 12;    // [2]
-  uint64_t* s_full = bars + 64;     // [kSlots]
-  uint64_t* s_empty = bars + 72;    // [kSlots]
-  uint64_t* p_full = bars + 26;     // [2]
-  uint64_t* p_empty = bars + 28;    // [2]
-  uint64_t* st_full = bars + 30;    // [2]
-  uint64_t* st_empty = bars + 32;   // [2]
-  uint64_t* o_empty = bars + 34;    // [2]
+  uint64_t* v_full = bars + 0;      // [kVSt <= 8]
+  uint64_t* v_empty = bars + 8;     // [kVSt <= 8]
+  uint64_t* k_full = bars + 16;     // [kKSt <= 8]
+  uint64_t* k_empty = bars + 24;    // [kKSt <= 8]
+  uint64_t* q_full = bars + 32;     // [2]
+  uint64_t* q_empty = bars + 34;    // [2]
+  uint64_t* s_full = bars + 36;     // [kSlots <= 8]
+  uint64_t* s_empty = bars + 44;    // [kSlots <= 8]
+  uint64_t* p_full = bars + 52;     // [2]
+  uint64_t* p_empty = bars + 54;    // [2]
+  uint64_t* st_full = bars + 56;    // [2]
+  uint64_t* st_empty = bars + 58;   // [2]
+  uint64_t* o_empty = bars + 60;    // [2]
+  uint64_t* ssh_full = bars + 62;   // shared S^T A and B written
+  uint64_t* ssh_empty = bars + 63;  // shared S^T read by the softmax
+  uint64_t* psh_full = bars + 64;   // shared P^T (A and B) written
+  uint64_t* psh_empty = bars + 65;  // PV of tile A done with P^T A
+  uint64_t* pb_empty = bars + 66;   // PV of tile B done with P^T B (0.5B: its own buffer)
+  uint64_t* osh_done = bars + 67;   // shared PVs done (O of the unit initialised)
   // O of row u in buffer b is complete: one barrier per (buffer, row), so the
   // PV issuer (gated per buffer by o_empty) is never two phases ahead of the
   // epilogue on any of them
-  uint64_t* o_full = bars + 44;     // [2][kU]
-  uint64_t* ssh_full = bars + 37;   // shared S^T A and B written
-  uint64_t* ssh_empty = bars + 38;  // shared S^T read by the softmax
-  uint64_t* psh_full = bars + 39;   // shared P^T (A and B) written
-  uint64_t* psh_empty = bars + 40;  // PV of tile A done with P^T A
-  uint64_t* osh_done = bars + 41;   // shared PVs done (O of the unit initialised)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 52);
+  uint64_t* o_full = bars + 68;     // [2][kU <= 8]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 84);
   float* stats = reinterpret_cast<float*>(smem + Smem::stats);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
   float* stash = reinterpret_cast<float*>(smem + Smem::stash);
@@ -219,6 +242,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     mbar_init(ssh_empty, kSoftWarps);
     mbar_init(psh_full, kSoftWarps);
     mbar_init(psh_empty, 1);
+    mbar_init(pb_empty, 1);
     mbar_init(osh_done, 1);
     fence_barrier_init();
     tma_prefetch(&tm_q);
@@ -245,16 +269,17 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     for (int64_t w = blockIdx.x; w < p.units; w += gridDim.x, ++it) {
       int grp;
       int64_t i0;
-      unit_of(p, w, &grp, &i0);
-      const UnitRows ur = load_unit(p, w, lane);
+      unit_of<kU>(p, w, &grp, &i0);
+      const URows ur = load_unit<kU>(p, w, lane);
       const int64_t qb = (p.start + i0) / kM;
       if (is_k && lane == 0) {
         const int qbuf = it & 1;
         mbar_wait(q_empty + qbuf, ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(q_full + qbuf, kQB);
         uint8_t* qd = smem + Smem::q + qbuf * kQB;
-        tma_load_3d_hint(qd, &tm_q, q_full + qbuf, 0, grp * kG, (int)i0, pol_stream);
-        tma_load_3d_hint(qd + kQHalf, &tm_q, q_full + qbuf, 64, grp * kG, (int)i0, pol_stream);
+#pragma unroll
+        for (int hh = 0; hh < kDH; ++hh)
+          tma_load_3d_hint(qd + hh * kQHalf, &tm_q, q_full + qbuf, 64 * hh, grp * kG, (int)i0, pol_stream);
       }
       int total = 2;
 #pragma unroll
@@ -265,20 +290,21 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         else if (c == 1) { b0 = (int)qb; nt = 1; }
         else {
           int u, k;
-          row_tile(ur, c - 2, &u, &k);
+          row_tile<kU>(ur, c - 2, &u, &k);
           b0 = ur.chosen(u, 2 * k);
           nt = 2 * k + 1 < ur.nchosen(u) ? 2 : 1;
           if (nt == 2) b1 = ur.chosen(u, 2 * k + 1);
         }
         if (lane == 0) {
           mbar_wait(ring_empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(ring_full + stage, nt * 2 * (kM * 128));
+          mbar_arrive_expect_tx(ring_full + stage, nt * kDH * (kM * 128));
           uint8_t* dst = ring + stage * kTile;
           for (int x = 0; x < nt; ++x) {
             const int row0 = (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
-            tma_load_3d_hint(dst + off, mm, ring_full + stage, 0, row0, grp, pol_keep);
-            tma_load_3d_hint(dst + kHalf + off, mm, ring_full + stage, 64, row0, grp, pol_keep);
+#pragma unroll
+            for (int hh = 0; hh < kDH; ++hh)
+              tma_load_3d_hint(dst + hh * kHalf + off, mm, ring_full + stage, 64 * hh, row0, grp, pol_keep);
           }
         }
         __syncwarp();
@@ -294,7 +320,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint32_t tcount = 0;
     int it = 0;
     for (int64_t w = blockIdx.x; w < p.units; w += gridDim.x, ++it) {
-      const UnitRows ur = load_unit(p, w, lane);
+      const URows ur = load_unit<kU>(p, w, lane);
       const int qbuf = it & 1;
       mbar_wait(q_full + qbuf, (it >> 1) & 1);
       const uint32_t qa = smem_u32(smem + Smem::q + qbuf * kQB);
@@ -324,7 +350,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       for (int u = 0; u < kU; ++u) total += ur.tiles(u);
       for (int c = 0; c < total; ++c, ++tcount) {
         int u, k;
-        row_tile(ur, c, &u, &k);
+        row_tile<kU>(ur, c, &u, &k);
         const int slot = tcount % kSlots;
         mbar_wait(k_full + stage, phase);
         mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1);
@@ -356,7 +382,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint32_t pcount = 0;
     int it = 0;
     for (int64_t w = blockIdx.x; w < p.units; w += gridDim.x, ++it) {
-      const UnitRows ur = load_unit(p, w, lane);
+      const URows ur = load_unit<kU>(p, w, lane);
       const int ob = it & 1;
       const uint32_t obase = tmem + kColO + 128 * ob;
       mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
@@ -368,7 +394,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + (kKSt + stage) * kTile), kHalf, 1024);
-          const uint64_t dp = sdesc_interleave(smem_u32(smem + (x ? Smem::prow : Smem::psh)), 16 * kNS, 128);
+          const uint64_t dp = sdesc_interleave(smem_u32(smem + (x ? Smem::pb : Smem::psh)), 16 * kNS, 128);
           const int ksteps = x ? 4 : 8;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -380,8 +406,12 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           if (x == 0) {
             umma_commit(psh_empty);
           } else {
-            umma_commit(p_empty + 0);    // P^T B occupied both row buffers
-            umma_commit(p_empty + 1);
+            if (C::kPBAlias) {
+              umma_commit(p_empty + 0);    // P^T B occupied both row buffers
+              umma_commit(p_empty + 1);
+            } else {
+              umma_commit(pb_empty);       // P^T B buffer free
+            }
             umma_commit(osh_done);
           }
         }
@@ -436,24 +466,28 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     for (int64_t w = blockIdx.x; w < p.units; w += gridDim.x, ++it) {
       int grp;
       int64_t i0;
-      unit_of(p, w, &grp, &i0);
-      const UnitRows ur = load_unit(p, w, lane);
+      unit_of<kU>(p, w, &grp, &i0);
+      const URows ur = load_unit<kU>(p, w, lane);
       const int64_t qb = (p.start + i0) / kM;
       // ---- shared pass: rows u = 0..U-1 over tiles A (keys of blocks 0,
       // qb-1: all visible) and B (block qb: key row <= the row's position)
       mbar_wait(ssh_full, it & 1);
       mbar_wait(psh_empty, (it & 1) ^ 1);
-      // P^T B aliases both row P buffers: their previous PVs must be done
-      mbar_wait(p_empty + 0, p_ph[0] ^ 1);
-      p_ph[0] ^= 1;
-      mbar_wait(p_empty + 1, p_ph[1] ^ 1);
-      p_ph[1] ^= 1;
+      if (C::kPBAlias) {
+        // P^T B aliases both row P buffers: their previous PVs must be done
+        mbar_wait(p_empty + 0, p_ph[0] ^ 1);
+        p_ph[0] ^= 1;
+        mbar_wait(p_empty + 1, p_ph[1] ^ 1);
+        p_ph[1] ^= 1;
+      } else {
+        mbar_wait(pb_empty, (it & 1) ^ 1);
+      }
       tc_fence_after();
       for (int u = 0; u < kU; ++u) {
         const int64_t pos = p.start + i0 + u;
         float za[kSH], zb[kSH];
-        tmem_ld8(tmem + lane_base + kColSA + u * kG + h0, za);
-        tmem_ld8(tmem + lane_base + kColSB + u * kG + h0, zb);
+        tmem_ld_n<kSH>(tmem + lane_base + kColSA + u * kG + h0, za);
+        tmem_ld_n<kSH>(tmem + lane_base + kColSB + u * kG + h0, zb);
         tmem_wait_ld();
         const bool vb = row < kM && qb * kM + row <= pos;
 #pragma unroll
@@ -499,16 +533,21 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // P^T A: 8-key groups 16 * 64 bytes apart, 8-column groups 128 B apart; column = u * 16 + h
         {
           const int col = u * kG + h0;
-          const uint32_t base = (row >> 3) * (16 * kNS) + (row & 7) * 16 + 128 * (col >> 3);
-          *reinterpret_cast<uint4*>(smem + Smem::psh + base) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-          if (row < kM)
-            *reinterpret_cast<uint4*>(smem + Smem::prow + base) = make_uint4(pbv[0], pbv[1], pbv[2], pbv[3]);
+          const uint32_t base = (row >> 3) * (16 * kNS) + (row & 7) * 16 + 128 * (col >> 3) + 2 * (col & 7);
+          if constexpr (kSH == 8) {
+            *reinterpret_cast<uint4*>(smem + Smem::psh + base) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+            if (row < kM)
+              *reinterpret_cast<uint4*>(smem + Smem::pb + base) = make_uint4(pbv[0], pbv[1], pbv[2], pbv[3]);
+          } else {
+            *reinterpret_cast<uint2*>(smem + Smem::psh + base) = make_uint2(pa[0], pa[1]);
+            if (row < kM) *reinterpret_cast<uint2*>(smem + Smem::pb + base) = make_uint2(pbv[0], pbv[1]);
+          }
         }
         // stash: the max per head and this warp's partial row sums
         {
           const float v = warp_reduce_n<kSH>(ls, lane, [](float a, float b) { return a + b; });
           const float vx = warp_reduce_n<kSH>(lx, lane, [](float a, float b) { return a + b; });
-          float* su = stash + u * (kG + 2 * kSoftWarps * kSH);
+          float* su = stash + u * Smem::stash_row;
           if (reduce_writer_n<kSH>(lane)) {
             su[kG + (ws * kSH + reduce_head_n<kSH>(lane)) * 2] = v;
             su[kG + (ws * kSH + reduce_head_n<kSH>(lane)) * 2 + 1] = vx;
@@ -531,7 +570,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       named_bar_sync(2 + half, 128);                    // the stash of this head half is complete
       // ---- row pass: each row's chosen tiles, online softmax from the stash
       for (int u = 0; u < kU; ++u) {
-        const float* su = stash + u * (kG + 2 * kSoftWarps * kSH);
+        const float* su = stash + u * Smem::stash_row;
         float mrun[kSH], mst[kSH], lsum[kSH], lsx[kSH];
 #pragma unroll
         for (int h = 0; h < kSH; ++h) { mst[h] = su[h0 + h]; mrun[h] = mst[h]; lsum[h] = 0.f; lsx[h] = 0.f; }
@@ -544,7 +583,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           ++tcount;
           tc_fence_after();
           float z[kSH];
-          tmem_ld8(tmem + lane_base + sslot * kG + h0, z);
+          tmem_ld_n<kSH>(tmem + lane_base + sslot * kG + h0, z);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
@@ -588,13 +627,13 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
               else mbar_wait(p_empty + (pbuf ^ 1), p_ph[pbuf ^ 1] ^ 1);
               tc_fence_after();
               float o[kSH], o2[kSH];
-              tmem_ld8(oa, o);
-              tmem_ld8(oa + kNS, o2);
+              tmem_ld_n<kSH>(oa, o);
+              tmem_ld_n<kSH>(oa + kNS, o2);
               tmem_wait_ld();
 #pragma unroll
               for (int h = 0; h < kSH; ++h) { o[h] *= corr[h]; o2[h] *= corr[h]; }
-              tmem_st8(oa, o);
-              tmem_st8(oa + kNS, o2);
+              tmem_st_n<kSH>(oa, o);
+              tmem_st_n<kSH>(oa + kNS, o2);
               tmem_wait_st();
               tc_fence_before();
             }
@@ -613,8 +652,9 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             upk2(fadd2(pk2(lsum[h], lsum[h + 1]), pk2(__low2float(hi2), __high2float(hi2))), lsum[h], lsum[h + 1]);
           }
           uint8_t* pb = smem + Smem::prow + pbuf * kPRow;
-          const uint32_t base = (row >> 3) * (16 * kG) + (row & 7) * 16 + 128 * (h0 >> 3);
-          *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
+          const uint32_t base = (row >> 3) * (16 * kG) + (row & 7) * 16 + 128 * (h0 >> 3) + 2 * (h0 & 7);
+          if constexpr (kSH == 8) *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
+          else *reinterpret_cast<uint2*>(pb + base) = make_uint2(phi[0], phi[1]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full + pbuf);
@@ -665,7 +705,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     for (int64_t w = blockIdx.x; w < p.units; w += gridDim.x, ++it) {
       int grp;
       int64_t i0;
-      unit_of(p, w, &grp, &i0);
+      unit_of<kU>(p, w, &grp, &i0);
       const int ob = it & 1;
       for (int u = 0; u < kU; ++u, ++rcount) {
         const int sb = rcount & 1;
@@ -673,8 +713,8 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         mbar_wait(st_full + sb, (rcount >> 1) & 1);
         tc_fence_after();
         float o[kG], o2[kG];
-        tmem_ld16(tmem + lane_base + kColO + 128 * ob + u * kG, o);
-        tmem_ld16(tmem + lane_base + kColO + 128 * ob + kNS + u * kG, o2);
+        tmem_ld_n<kG>(tmem + lane_base + kColO + 128 * ob + u * kG, o);
+        tmem_ld_n<kG>(tmem + lane_base + kColO + 128 * ob + kNS + u * kG, o2);
         tmem_wait_ld();
 #pragma unroll
         for (int h = 0; h < kG; ++h) o[h] += o2[h];
@@ -684,7 +724,9 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int h = 0; h < kG; ++h) l[h] = st[h] + st[16 + h] + st[32 + h] + st[48 + h];
         const int64_t i = i0 + u;
         const int64_t obase = (i * p.hq + (int64_t)grp * kG) * kD + d;
-        if (p.out_f32) {
+        if (d >= kD) {
+          // O^T lanes >= D (D = 64 runs PV with M = 128 over a half-width V tile): unused
+        } else if (p.out_f32) {
           float* out = static_cast<float*>(p.out);
 #pragma unroll
           for (int h = 0; h < kG; ++h) st_global_hint(out + obase + h * kD, o[h] / l[h], pol_stream);
@@ -714,8 +756,9 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 }  // namespace
 
 // Rows [row0, row1) of a prefill call that the shared-forced-block kernel
-// covers: positions >= 2048, U-aligned, MiniCPM4 forced-block layout, plain
-// prefill (no tree rows, no broadcast position, no hi + lo weights).
+// covers: positions >= 2048, U-aligned, MiniCPM4 forced-block layout and head
+// geometry (8B: G = 16, D = 128; 0.5B: G = 8, D = 64), plain prefill (no tree
+// rows, no broadcast position, no hi + lo weights).
 bool attend_share_range(const infllm2_geometry& g, const CallShape& cs, int p_split, bool tree, int64_t* row0,
                         int64_t* row1) {
   static const bool off = [] {
@@ -723,23 +766,31 @@ bool attend_share_range(const infllm2_geometry& g, const CallShape& cs, int p_sp
     return e && e[0] == '0';
   }();
   if (off || p_split || tree || cs.bcast) return false;
-  if (cs.group != kG || cs.d != kD || g.block_size != kM || g.n_init_blocks != 1 || g.n_local_blocks != 2) return false;
+  const bool shape_ok = (cs.group == 16 && cs.d == 128) || (cs.group == 8 && cs.d == 64);
+  if (!shape_ok || g.block_size != kM || g.n_init_blocks != 1 || g.n_local_blocks != 2) return false;
   if (cs.max_sel > kMaxSel) return false;
+  // 0.5B: eight rows per unit pay off while the forced blocks are a large share
+  // of a row's blocks (measured: k = 8 / 16 -40 / -16 % stage-2 time at 128K,
+  // k = 32 neutral, k = 64 +14 %)
+  if (cs.group == 8 && cs.max_sel > 19) return false;
+  const int u = kNS / cs.group;
   // rows below position 2048 attend at most 32 blocks and carry the largest
   // relative bf16-weight rounding error: they stay on attend_tc.cu (whose
   // rows below 256 use hi + lo weights), so the two kernels share one envelope
   int64_t a = cs.start > kShareFrom ? cs.start : kShareFrom;
-  a = (a + kU - 1) / kU * kU;
-  const int64_t b = (cs.start + cs.n) / kU * kU;
-  if (b - a < 2 * kU * kNumSMs) return false;   // too few units to pay for a second launch
+  a = (a + u - 1) / u * u;
+  const int64_t b = (cs.start + cs.n) / u * u;
+  if (b - a < 2 * u * kNumSMs) return false;   // too few units to pay for a second launch
   *row0 = a - cs.start;
   *row1 = b - cs.start;
   return true;
 }
 
-cudaError_t launch_attend_share(const CallShape& cs, int64_t row0, int64_t row1, const void* q, int64_t q_row_stride,
+template <int G, int D>
+static cudaError_t launch_share(const CallShape& cs, int64_t row0, int64_t row1, const void* q, int64_t q_row_stride,
                                 const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
                                 void* out, int out_f32, float* lse, cudaStream_t stream) {
+  using C = SC<G, D>;
   const int64_t n = row1 - row0;
   Params p;
   p.n = n;
@@ -749,33 +800,43 @@ cudaError_t launch_attend_share(const CallShape& cs, int64_t row0, int64_t row1,
   p.max_sel = cs.max_sel;
   p.out_f32 = out_f32;
   p.sel = selection + row0 * cs.hkv * cs.max_sel;
-  p.out = static_cast<uint8_t*>(out) + row0 * cs.hq * kD * (out_f32 ? 4 : 2);
+  p.out = static_cast<uint8_t*>(out) + row0 * cs.hq * D * (out_f32 ? 4 : 2);
   p.lse = lse ? lse + row0 * cs.hq : nullptr;
-  p.units = cs.hkv * (n / kU);
+  p.units = cs.hkv * (n / C::kU);
   const __nv_bfloat16* qr = static_cast<const __nv_bfloat16*>(q) + row0 * q_row_stride;
   CUtensorMap tq, tk, tv;
   {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.hq, (uint64_t)n};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)q_row_stride * 2};
-    const uint32_t box[3] = {64, (uint32_t)kG, (uint32_t)kU};
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.hq, (uint64_t)n};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};
+    const uint32_t box[3] = {64, (uint32_t)G, (uint32_t)C::kU};
     if (!encode_tmap_3d_bf16(&tq, qr, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cs.cache_len, (uint64_t)cs.hkv};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)cap * kD * 2};
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)cs.cache_len, (uint64_t)cs.hkv};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)cap * D * 2};
     const uint32_t box[3] = {64, (uint32_t)kM, 1};
     if (!encode_tmap_3d_bf16(&tk, k_cache, dims, strides, box)) return cudaErrorInvalidValue;
     if (!encode_tmap_3d_bf16(&tv, v_cache, dims, strides, box)) return cudaErrorInvalidValue;
   }
-  const size_t smem = Smem::total + 1024;
-  cudaError_t e = smem_attr_once((const void*)attend_share_kernel, (int)smem);
+  const size_t smem = C::Smem::total + 1024;
+  cudaError_t e = smem_attr_once((const void*)attend_share_kernel<G, D>, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(p.units < sms ? p.units : sms);
   count_launch();
-  attend_share_kernel<<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  attend_share_kernel<G, D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_attend_share(const CallShape& cs, int64_t row0, int64_t row1, const void* q, int64_t q_row_stride,
+                                const void* k_cache, const void* v_cache, int64_t cap, const int32_t* selection,
+                                void* out, int out_f32, float* lse, cudaStream_t stream) {
+  if (cs.group == 8 && cs.d == 64)
+    return launch_share<8, 64>(cs, row0, row1, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32, lse,
+                               stream);
+  return launch_share<16, 128>(cs, row0, row1, q, q_row_stride, k_cache, v_cache, cap, selection, out, out_f32, lse,
+                               stream);
 }
 
 }  // namespace infllm2

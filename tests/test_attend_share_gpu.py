@@ -24,20 +24,25 @@ from bars import LSE_TC, OUT_ABS, OUT_REL  # noqa: E402
 SHARE_FROM = 2048
 
 
-def _layer(length, seed, topk=16):
+def _layer(length, seed, topk=16, shape=(32, 2, 128)):
+    hq, hkv, d = shape
     cfg = P.SparseAttentionConfig(top_k=topk)
     g = torch.Generator(device="cuda").manual_seed(seed)
-    q = torch.randn((length, 32, 128), generator=g, device="cuda").to(torch.bfloat16)
-    k = torch.randn((length, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
-    v = torch.randn((length, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
-    layer = P.BlockizedLayerCache(2, 128, cfg, capacity=length)
+    q = torch.randn((length, hq, d), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((length, hkv, d), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((length, hkv, d), generator=g, device="cuda").to(torch.bfloat16)
+    layer = P.BlockizedLayerCache(hkv, d, cfg, capacity=length)
     layer.append(k, v)
     return cfg, q, layer
 
 
-@pytest.mark.parametrize("length,topk", [(8192, 16), (12000, 32), (9000, 64)])
-def test_shared_kernel_vs_float64_verifier(length, topk):
-    cfg, q, layer = _layer(length, 11 + length, topk)
+@pytest.mark.parametrize("length,topk,shape", [(8192, 16, (32, 2, 128)), (12000, 32, (32, 2, 128)),
+                                               (9000, 64, (32, 2, 128)), (8192, 16, (16, 2, 64)),
+                                               (10000, 8, (16, 2, 64))], ids=["8B-k16", "8B-k32", "8B-k64",
+                                                                               "0.5B-k16", "0.5B-k8"])
+def test_shared_kernel_vs_float64_verifier(length, topk, shape):
+    cfg, q, layer = _layer(length, 11 + length, topk, shape)
+    group = shape[0] // shape[1]
     lib = _lib.load()
     n0 = lib.infllm2_launch_count()
     o, s, l = P.two_stage_attention(q, layer, cfg, 0, return_selection=True, return_lse=True,
@@ -50,7 +55,7 @@ def test_shared_kernel_vs_float64_verifier(length, topk):
     same = (s == s2).all(-1)
     assert same.float().mean().item() > 0.999          # near-ties only
     rows = torch.arange(SHARE_FROM, length, device="cuda")
-    ok = same[rows].repeat_interleave(16, dim=1)
+    ok = same[rows].repeat_interleave(group, dim=1)
     err = (o[rows] - o2[rows]).abs()
     bar = OUT_ABS + OUT_REL * o2[rows].abs()
     assert bool((err <= bar)[ok].all()), f"max |dO| {err[ok].max().item():.3e}"
