@@ -769,6 +769,10 @@ bool attend_share_range(const infllm2_geometry& g, const CallShape& cs, int p_sp
   const bool shape_ok = (cs.group == 16 && cs.d == 128) || (cs.group == 8 && cs.d == 64);
   if (!shape_ok || g.block_size != kM || g.n_init_blocks != 1 || g.n_local_blocks != 2) return false;
   if (cs.max_sel > kMaxSel) return false;
+  // a selection of little more than the forced blocks (forced_consume_budget
+  // with top-k <= 4) attends too few keys for bf16 weights: attend_tc.cu's
+  // hi + lo weights serve it
+  if (g.forced_consume_budget && g.top_k <= 4) return false;
   // 0.5B: eight rows per unit pay off while the forced blocks are a large share
   // of a row's blocks (measured: k = 8 / 16 -40 / -16 % stage-2 time at 128K,
   // k = 32 neutral, k = 64 +14 %)

@@ -72,8 +72,11 @@ constexpr bool kQkSplit = ATT_QK_SPLIT;  // S^T as two interleaved accumulators 
 constexpr int kMaxSel = 80;
 // Rows at positions below this attend few keys, where bf16 softmax weights
 // would cost up to 2^-9 |v0 - v1| (two keys): they always carry the weights as
-// bf16 hi + lo (a second PV MMA per k-step on <= 2 tiles per item)
+// bf16 hi + lo (a second PV MMA per k-step on <= 2 tiles per item); so do rows
+// of any position that attend at most kSplitPBlocks blocks (a budget-0
+// forced_consume_budget selection: the forced blocks alone)
 constexpr int64_t kSplitPBelow = 256;
+constexpr int kSplitPBlocks = 4;
 
 constexpr uint32_t kHalfBytes = kRowsT * 128;           // 16 KB: 128 rows x 64 d (bf16)
 
@@ -502,7 +505,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
           const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::p + pbuf * kPBytes), 16 * kG, 128);
           const uint32_t ocol = tmem + kColO + ob * 2 * kG;
           const uint32_t acc0 = c > c0 ? 1u : 0u;
-          if (p.p_split || pos < kSplitPBelow) {      // hi -> O_a, lo -> O_b
+          if (p.p_split || pos < kSplitPBelow || tl.nb <= kSplitPBlocks) {      // hi -> O_a, lo -> O_b
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               if (k < ksteps) {
@@ -558,7 +561,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       tile_range(p, part, tl.total(), &c0, &c1);
       if (c0 >= c1) continue;
       const int ob = it & 1;
-      const bool splitp = p.p_split || pos < kSplitPBelow;
+      const bool splitp = p.p_split || pos < kSplitPBelow || tl.nb <= kSplitPBlocks;
       float mrun[kSH], lsum[kSH], lsx[kSH];     // lsum: weights as used by PV; lsx: unrounded (LSE)
 #pragma unroll
       for (int h = 0; h < kSH; ++h) { mrun[h] = -INFINITY; lsum[h] = 0.f; lsx[h] = 0.f; }

@@ -24,9 +24,9 @@ from bars import LSE_TC, OUT_ABS, OUT_REL  # noqa: E402
 SHARE_FROM = 2048
 
 
-def _layer(length, seed, topk=16, shape=(32, 2, 128)):
+def _layer(length, seed, topk=16, shape=(32, 2, 128), consume=False):
     hq, hkv, d = shape
-    cfg = P.SparseAttentionConfig(top_k=topk)
+    cfg = P.SparseAttentionConfig(top_k=topk, forced_consume_budget=consume)
     g = torch.Generator(device="cuda").manual_seed(seed)
     q = torch.randn((length, hq, d), generator=g, device="cuda").to(torch.bfloat16)
     k = torch.randn((length, hkv, d), generator=g, device="cuda").to(torch.bfloat16)
@@ -61,6 +61,24 @@ def test_shared_kernel_vs_float64_verifier(length, topk, shape):
     assert bool((err <= bar)[ok].all()), f"max |dO| {err[ok].max().item():.3e}"
     dl = (l[rows] - l2[rows]).abs()[ok]
     assert dl.max().item() <= LSE_TC, f"max |dLSE| {dl.max().item():.3e}"
+
+
+@pytest.mark.parametrize("topk", [3, 16], ids=["budget0", "budget13"])
+def test_consume_budget_rows(topk):
+    """forced_consume_budget: top-k 3 leaves no chosen block (rows made of the
+    shared tiles alone), top-k 16 an odd 13 (a half tile per row)."""
+    length = 6000
+    cfg, q, layer = _layer(length, 31 + topk, topk, consume=True)
+    o, s, l = P.two_stage_attention(q, layer, cfg, 0, return_selection=True, return_lse=True,
+                                    out_dtype=torch.float32)
+    o2, s2, l2 = P.two_stage_attention(q, layer, cfg, 0, return_selection=True, return_lse=True,
+                                       out_dtype=torch.float32, exact=True)
+    rows = torch.arange(SHARE_FROM, length, device="cuda")
+    ok = (s == s2).all(-1)[rows].repeat_interleave(16, dim=1)
+    assert ok.float().mean().item() > 0.999
+    err = (o[rows] - o2[rows]).abs()
+    assert bool((err <= OUT_ABS + OUT_REL * o2[rows].abs())[ok].all()), f"max |dO| {err[ok].max().item():.3e}"
+    assert (l[rows] - l2[rows]).abs()[ok].max().item() <= LSE_TC
 
 
 def test_bf16_output_matches_float32():
