@@ -81,6 +81,29 @@ def test_consume_budget_rows(topk):
     assert (l[rows] - l2[rows]).abs()[ok].max().item() <= LSE_TC
 
 
+def test_four_kv_groups_and_strided_q():
+    """HKV = 4 (HQ = 64) and q rows taken from a wider packed buffer (row
+    stride > HQ * D): the shared kernel's tensor maps follow the strides."""
+    length = 7000
+    cfg = P.SparseAttentionConfig(top_k=16)
+    g = torch.Generator(device="cuda").manual_seed(77)
+    qkv = torch.randn((length, 64 + 8, 128), generator=g, device="cuda").to(torch.bfloat16)
+    q = qkv[:, :64]                                     # (L, 64, 128) view, row stride 72 * 128
+    k, v = qkv[:, 64:68].contiguous(), qkv[:, 68:72].contiguous()
+    layer = P.BlockizedLayerCache(4, 128, cfg, capacity=length)
+    layer.append(k, v)
+    o, s, l = P.two_stage_attention(q, layer, cfg, 0, return_selection=True, return_lse=True,
+                                    out_dtype=torch.float32)
+    o2, s2, l2 = P.two_stage_attention(q.contiguous(), layer, cfg, 0, return_selection=True, return_lse=True,
+                                       out_dtype=torch.float32, exact=True)
+    rows = torch.arange(SHARE_FROM, length, device="cuda")
+    ok = (s == s2).all(-1)[rows].repeat_interleave(16, dim=1)
+    assert ok.float().mean().item() > 0.999
+    err = (o[rows] - o2[rows]).abs()
+    assert bool((err <= OUT_ABS + OUT_REL * o2[rows].abs())[ok].all()), f"max |dO| {err[ok].max().item():.3e}"
+    assert (l[rows] - l2[rows]).abs()[ok].max().item() <= LSE_TC
+
+
 def test_bf16_output_matches_float32():
     cfg, q, layer = _layer(6000, 5)
     o32 = P.two_stage_attention(q, layer, cfg, 0, out_dtype=torch.float32)
