@@ -226,8 +226,25 @@ def run_ours(args):
         append in natural order and compress (paper_2506_07900_b200.sharding)."""
         S.fill_layer_cache(caches[layer], k_in[layer], v_in[layer], world)
 
+    # a rank's two chunks are independent rows of one layer: each runs on its own
+    # stream, so one call's kernel tails (the last partial wave of the
+    # persistent grids) overlap the other call's kernels; layers stay ordered
+    chunk_streams = [torch.cuda.Stream(dev) for _ in chunks]
+
     def attend(layer, timed=False, outs=None, lse="exact"):
         cache = caches[layer]
+        if not timed and os.environ.get("INFLLM2_BENCH_CHUNK_STREAMS", "1") == "1":
+            cur = torch.cuda.current_stream(dev)
+            res = []
+            for (lo, hi), q, st in zip(chunks, q_in[layer], chunk_streams):
+                st.wait_stream(cur)
+                with torch.cuda.stream(st):
+                    res.append(P.two_stage_attention(q, cache, cfg, lo, lse=lse))
+            for st in chunk_streams:
+                cur.wait_stream(st)
+            if outs is not None:
+                outs.extend(res)
+            return
         for h, (lo, hi) in enumerate(chunks):
             q = q_in[layer][h]
             if timed:
@@ -440,6 +457,7 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
     my_rows = sum(hi - lo for lo, hi in chunks)
     out_host = torch.empty((my_rows, HQ, D), dtype=torch.bfloat16).pin_memory()   # every row of the last layer
     copy_stream = torch.cuda.Stream(dev)
+    chunk_streams = [torch.cuda.Stream(dev) for _ in chunks]
     h2d_bytes = sum(t.numel() * t.element_size() for grp in host[0] for t in grp) * layers
 
     def step():
@@ -463,10 +481,15 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
             qd, kd, vd = dbuf[layer % nbuf]
             cache = caches[layer]
             S.fill_layer_cache(cache, kd, vd, world)
-            for h, (lo, hi) in enumerate(chunks):
-                o = P.two_stage_attention(qd[h], cache, cfg, lo)
+            for h, (lo, hi) in enumerate(chunks):          # the chunks on their own streams, as step()
+                chunk_streams[h].wait_stream(stream)
+                with torch.cuda.stream(chunk_streams[h]):
+                    o = P.two_stage_attention(qd[h], cache, cfg, lo)
                 if layer == layers - 1:
+                    o.record_stream(stream)          # read back on the main stream
                     outs.append(o)
+            for st in chunk_streams:
+                stream.wait_stream(st)
             done[layer].record(stream)
         r0 = 0
         for o in outs:                  # D2H of this rank's full last-layer output
