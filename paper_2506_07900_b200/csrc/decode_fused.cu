@@ -61,7 +61,7 @@ constexpr int kD = 128;
 constexpr int kS = 16;
 constexpr int kM = 64;
 constexpr int kMaxCl = 8;                     // CTAs per cluster = pieces per segment (runtime 3..8)
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;                 // warps 0 TMA, 1 MMA, 2..5 epilogue, 6 append
 constexpr int kStages = 3;
 constexpr int kMaxTiles = 28;                 // z tiles resident in TMEM (16 columns each)
 constexpr int kMaxRows = kMaxTiles * 128;     // kernels per piece
@@ -402,7 +402,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
   uint64_t* empty = bars + 3;            // [3]
   uint64_t* q_full = bars + 6;
   uint64_t* q_empty = bars + 7;
-  uint64_t* appended = bars + 8;         // 128 epilogue arrivals
+  uint64_t* appended = bars + 8;         // 32 append-warp arrivals: dirty windows + K/V row stored
   uint64_t* z_free = bars + 9;           // 128 epilogue arrivals: z tiles read, TMEM reusable
   uint64_t* s2_full = bars + 10;
   uint64_t* s2_empty = bars + 11;        // 4 warps
@@ -438,7 +438,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
     for (int i = 0; i < kStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    mbar_init(appended, 128);
+    mbar_init(appended, 32);
     mbar_init(z_free, 128);
     mbar_init(s2_full, 1);
     mbar_init(s2_empty, 4);
@@ -481,7 +481,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       for (int s = 0; s < p.n_seq; ++s) tv.len[s] = len_s[s] + 1;
     }
   }
-  if (p.early && warp != 0) {
+  if (p.early && warp != 0 && warp != 6) {
     pdl_wait();
     pdl_launch_dependents();
   }
@@ -667,6 +667,109 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       if (elect_one()) umma_commit(q_empty);          // every MMA reading this segment's Q is issued
       __syncwarp();
     }
+  } else if (warp == 6) {
+    // ============================================================ append (32 threads)
+    // The kernel windows that contain the new row (at most two fine windows in
+    // this piece's row range, nk - dlo <= 2) are recomputed bitwise as
+    // build_kernels (sparse.py:70-91, 116-127, F18 clip) by every piece whose
+    // range holds them; piece P-1 also writes the K/V row and the dirty coarse
+    // windows.  A warp of its own: the epilogue starts reducing z tiles at
+    // once instead of waiting out this work's load round trip (the producer
+    // holds only the dirty tile's TMA until `appended`).  Lane = 4 dims, 8-byte
+    // loads: the <= 48 rows of a window pair are one round of loads.
+    const int d0 = lane * 4;
+    int it = 0;
+    for (int sg = cid; sg < nseg; sg += ncl, ++it) {
+      Info I;
+      seg_info(p, len_s, sg, rank, P, I);
+      const SeqDesc ds = tv.desc[I.s];
+      const int64_t L = I.pos + 1;
+      const __nv_bfloat16* kg = ds.k + (int64_t)I.g * ds.cap * kD;
+      const int64_t knew_idx = ((int64_t)I.s * p.hkv + I.g) * kD + d0;
+      const int64_t jlo = I.dlo > I.r0 ? I.dlo : I.r0;
+      const bool dirty = jlo < I.r1;
+      // the raw bf16 quads stay packed until summed (96 registers, not 192)
+      uint2 raw[kP + kS];
+      if (dirty) {
+        const int64_t row0 = jlo * kS;
+#pragma unroll
+        for (int i = 0; i < kP + kS; ++i) {
+          const int64_t r = row0 + i;
+          raw[i] = (r < L && r != I.pos) ? __ldg(reinterpret_cast<const uint2*>(kg + r * kD + d0)) : make_uint2(0u, 0u);
+        }
+      }
+      if (it == 0 && p.early) {                      // k_new / v_new: this step's inputs
+        pdl_wait();
+        pdl_launch_dependents();
+      }
+      const uint2 kraw = *reinterpret_cast<const uint2*>(p.k_new + knew_idx);
+      float knew[4];
+      {
+        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&kraw.x);
+        const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&kraw.y);
+        knew[0] = __low2float(a);
+        knew[1] = __high2float(a);
+        knew[2] = __low2float(b);
+        knew[3] = __high2float(b);
+      }
+      if (dirty) {
+        const int64_t row0 = jlo * kS;
+#pragma unroll
+        for (int i = 0; i < kP + kS; ++i)
+          if (row0 + i == I.pos) raw[i] = kraw;
+        auto val = [&](int i, int e) {
+          const uint32_t w = e < 2 ? raw[i].x : raw[i].y;
+          return __uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
+        };
+        auto emit = [&](int64_t j, int i0) {
+          const int64_t w64 = L - j * kS;
+          const int w = (int)(w64 < kP ? w64 : kP);
+          float mu[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            double acc = (double)val(i0, e);
+#pragma unroll
+            for (int r = 1; r < kP; ++r)
+              if (r < w) acc += (double)val(i0 + r, e);   // sequential, as numpy's reduce
+            mu[e] = __double2float_rn(acc / (double)w);
+          }
+          const int64_t dst = ((int64_t)I.g * ds.means_cap + j) * kD + d0;
+          *reinterpret_cast<float4*>(ds.fine + dst) = make_float4(mu[0], mu[1], mu[2], mu[3]);
+          __nv_bfloat16 h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            h[e] = __float2bfloat16_rn(mu[e]);
+            l[e] = __float2bfloat16_rn(mu[e] - __bfloat162float(h[e]));
+          }
+          *reinterpret_cast<uint2*>(ds.hi + dst) = *reinterpret_cast<const uint2*>(h);
+          *reinterpret_cast<uint2*>(ds.lo + dst) = *reinterpret_cast<const uint2*>(l);
+        };
+        emit(jlo, 0);
+        if (jlo + 1 < I.r1) emit(jlo + 1, kS);
+      }
+      if ((int)rank == P - 1) {                       // the new K/V row (read by the forced tiles after x1)
+        const int64_t dst = ((int64_t)I.g * ds.cap + I.pos) * kD + d0;
+        *reinterpret_cast<uint2*>(ds.k + dst) = kraw;
+        *reinterpret_cast<uint2*>(ds.v + dst) = *reinterpret_cast<const uint2*>(p.v_new + knew_idx);
+      }
+      fence_proxy_async_global();
+      mbar_arrive(appended);
+      if (lane == 0 && it == 0) trace(p.trace, 13);
+      if ((int)rank == P - 1) {
+        // every dirty coarse window (two when coarse_stride < kernel_size): not
+        // read by this step's stages
+        const int cs = p.coarse_stride;
+        int64_t first = I.pos < kP ? 0 : (I.pos - kP) / cs + 1;
+        const int64_t count_old = I.pos / cs, count = L / cs;
+        if (first > count_old) first = count_old;
+        for (int64_t j = first; j < count; ++j)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float mu = window_mean(kg, kD, j, cs, L, d0 + e, I.pos, knew[e]);
+            ds.coarse[((int64_t)I.g * ds.coarse_cap + j) * kD + d0 + e] = mu;
+          }
+      }
+    }
   } else {
     // ============================================================ epilogue (128 threads)
     const int tid = threadIdx.x - 64;
@@ -688,62 +791,6 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       const int tr = it == 0 ? p.trace : 0;
       const SeqDesc ds = tv.desc[I.s];
       const int64_t L = I.pos + 1;
-      // ---- A. append: dirty windows in [r0, r1) (+ K/V row and coarse window on piece 7)
-      const int d = tid;
-      const __nv_bfloat16* kg = ds.k + (int64_t)I.g * ds.cap * kD;
-      const int64_t knew_idx = ((int64_t)I.s * p.hkv + I.g) * kD + d;
-      {
-        // at most two fine windows change (nk - dlo <= 2): their <= 48 rows are
-        // loaded in ONE round, summed as window_mean does (sequential float64,
-        // numpy reduce order)
-        const int64_t jlo = I.dlo > I.r0 ? I.dlo : I.r0;
-        if (jlo < I.r1) {
-          const float knew = __bfloat162float(p.k_new[knew_idx]);
-          const int64_t row0 = jlo * kS;
-          float x[kP + kS];
-#pragma unroll
-          for (int i = 0; i < kP + kS; ++i) {
-            const int64_t r = row0 + i;
-            x[i] = r < L && r != I.pos ? __bfloat162float(__ldg(&kg[r * kD + d])) : 0.f;   // LDG, not generic
-          }
-#pragma unroll
-          for (int i = 0; i < kP + kS; ++i)
-            if (row0 + i == I.pos) x[i] = knew;
-          auto emit = [&](int64_t j, const float* xs) {
-            const int64_t w64 = L - j * kS;
-            const int w = (int)(w64 < kP ? w64 : kP);
-            double acc = (double)xs[0];
-#pragma unroll
-            for (int r = 1; r < kP; ++r)
-              if (r < w) acc += (double)xs[r];
-            const float mu = __double2float_rn(acc / (double)w);
-            const int64_t dst = ((int64_t)I.g * ds.means_cap + j) * kD + d;
-            ds.fine[dst] = mu;
-            const __nv_bfloat16 h = __float2bfloat16_rn(mu);
-            ds.hi[dst] = h;
-            ds.lo[dst] = __float2bfloat16_rn(mu - __bfloat162float(h));
-          };
-          emit(jlo, x);
-          if (jlo + 1 < I.r1) emit(jlo + 1, x + kS);
-        }
-        fence_proxy_async_global();
-        mbar_arrive(appended);
-        if (tid == 0) trace(tr, 13);
-        if ((int)rank == P - 1) {   // not needed by stage 1: after the arrival
-          const float knew = __bfloat162float(p.k_new[knew_idx]);
-          ds.k[((int64_t)I.g * ds.cap + I.pos) * kD + d] = p.k_new[knew_idx];
-          ds.v[((int64_t)I.g * ds.cap + I.pos) * kD + d] = p.v_new[knew_idx];
-          const int cs = p.coarse_stride;
-          int64_t first = I.pos < kP ? 0 : (I.pos - kP) / cs + 1;
-          const int64_t count_old = I.pos / cs, count = L / cs;
-          if (first > count_old) first = count_old;
-          // every dirty coarse window (two when coarse_stride < kernel_size)
-          for (int64_t j = first; j < count; ++j) {
-            const float mu = window_mean(kg, kD, j, cs, L, d, I.pos, knew);
-            ds.coarse[((int64_t)I.g * ds.coarse_cap + j) * kD + d] = mu;
-          }
-        }
-      }
       // ---- B. stage-1 partial (max, sum 2^z) over owned kernels [4*b0, r1)
       const int64_t own0 = 4 * I.b0;
       {
@@ -793,6 +840,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       }
       named_bar_sync(1, 128);
       if (tid == 0) trace(tr, 2);
+      mbar_wait(appended, par);                      // the append warp's stores precede this CTA's x1 arrival
       if (warp == 2) arrive_all(x1, lane, P);
       mbar_wait_cluster(x1, par);
       if (tid == 0) trace(tr, 3);
