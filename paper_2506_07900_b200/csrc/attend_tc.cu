@@ -785,8 +785,10 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
       auto lsum_exact = [&](int h) { return st[80 + h] + st[96 + h] + st[112 + h] + st[128 + h]; };
       if (p.split) {
         float* po = p.part_o + w * (kG * kD) + d;
+        if (d < kD) {     // D = 64: O^T lanes >= D unused
 #pragma unroll
-        for (int h = 0; h < kG; ++h) po[h * kD] = o[h];
+          for (int h = 0; h < kG; ++h) po[h * kD] = o[h];
+        }
         if (quad == 0 && lane < kG) {
           float lh = l[0];
 #pragma unroll
@@ -837,6 +839,7 @@ attend_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant
 // Merge split-K partials of each (row, group) item: O = sum_p O_p 2^(m_p - M) /
 // sum_p l_p 2^(m_p - M).  One CTA per item; part weights computed once into
 // shared memory, then thread (h, d-slice) streams the parts with independent loads.
+template <int kG, int kD>
 __global__ void __launch_bounds__(512) attend_combine_kernel(const float* __restrict__ part_o,
                                                              const float* __restrict__ part_ml, int64_t parts, int hq,
                                                              int hkv, void* out, int out_f32, float* lse,
@@ -890,10 +893,11 @@ size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel) {
 
 // Batched decode: one query row per sequence, per-sequence K/V tensor maps in
 // device memory (maps[stride*s + 0] = K, + 1 = V), positions seq_len[s] - 1.
-cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
-                                    const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
-                                    const int32_t* selection, void* out, int out_f32, float* lse,
-                                    float* split_ws, cudaStream_t stream) {
+template <int G, int D>
+static cudaError_t attend_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
+                                 const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
+                                 const int32_t* selection, void* out, int out_f32, float* lse, float* split_ws,
+                                 cudaStream_t stream) {
   Params p;
   p.n = n_seq;
   p.start = 0;
@@ -914,17 +918,17 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   p.group_major = 0;
   p.parts = split_ws ? (max_sel + 1) / 2 : 1;
   p.part_o = split_ws;
-  p.part_ml = split_ws ? split_ws + n_seq * hkv * p.parts * (kG * kD) : nullptr;
+  p.part_ml = split_ws ? split_ws + n_seq * hkv * p.parts * (G * D) : nullptr;
   p.tree_words = nullptr;
   p.tree_n = p.tree_nw = 0;
   p.tree_row0 = 0;
   CUtensorMap tq;
-  const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
-  const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
-  const uint32_t box[3] = {64, (uint32_t)kG, 1};
+  const uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)n_seq};
+  const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)hq * D * 2};
+  const uint32_t box[3] = {64, (uint32_t)G, 1};
   if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return cudaErrorInvalidValue;
-  const size_t smem = AttCfg<16, 128>::Smem::total + 1024;
-  cudaError_t e = smem_attr_once((const void*)attend_tc_kernel<16, 128>, (int)smem);
+  const size_t smem = AttCfg<G, D>::Smem::total + 1024;
+  cudaError_t e = smem_attr_once((const void*)attend_tc_kernel<G, D>, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t items = n_seq * hkv * p.parts;
   int dev = 0, sms = kNumSMs;
@@ -935,24 +939,37 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(AttCfg<16, 128>::kThreads);
+  cfg.blockDim = dim3(AttCfg<G, D>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   count_launch();
-  e = cudaLaunchKernelEx(&cfg, attend_tc_kernel<16, 128>, tq, tq, tq, p);
+  e = cudaLaunchKernelEx(&cfg, attend_tc_kernel<G, D>, tq, tq, tq, p);
   if (e != cudaSuccess) return e;
   if (split_ws) {
     cfg.gridDim = dim3((unsigned)(n_seq * hkv));
     cfg.blockDim = dim3(512);
     cfg.dynamicSmemBytes = 0;
     count_launch();
-    e = cudaLaunchKernelEx(&cfg, attend_combine_kernel, (const float*)p.part_o, (const float*)p.part_ml, p.parts, hq,
-                           hkv, out, out_f32, lse, const_cast<int64_t*>(seq_len));
+    e = cudaLaunchKernelEx(&cfg, attend_combine_kernel<G, D>, (const float*)p.part_o, (const float*)p.part_ml,
+                           p.parts, hq, hkv, out, out_f32, lse, const_cast<int64_t*>(seq_len));
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_attend_tc_decode(int hq, int hkv, int d, int max_sel, int64_t n_seq, const void* q,
+                                    const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
+                                    const int32_t* selection, void* out, int out_f32, float* lse,
+                                    float* split_ws, cudaStream_t stream) {
+  if (hq / hkv == 16 && d == 128)
+    return attend_decode<16, 128>(hq, hkv, max_sel, n_seq, q, kv_maps, map_stride, seq_len, selection, out, out_f32,
+                                  lse, split_ws, stream);
+  if (hq / hkv == 8 && d == 64)
+    return attend_decode<8, 64>(hq, hkv, max_sel, n_seq, q, kv_maps, map_stride, seq_len, selection, out, out_f32,
+                                lse, split_ws, stream);
+  return cudaErrorInvalidValue;
 }
 
 static int group_major_enabled() {

@@ -32,7 +32,7 @@ namespace infllm2 {
 
 using namespace dec;
 
-cudaError_t launch_attend_tc_decode(int hq, int hkv, int max_sel, int64_t n_seq, const void* q,
+cudaError_t launch_attend_tc_decode(int hq, int hkv, int d, int max_sel, int64_t n_seq, const void* q,
                                     const CUtensorMap* kv_maps, int map_stride, const int64_t* seq_len,
                                     const int32_t* selection, void* out, int out_f32, float* lse,
                                     float* split_ws, cudaStream_t stream);
@@ -120,17 +120,24 @@ __global__ void __launch_bounds__(256) decode_append_compress_kernel(void* table
 // ------------------------------------------------------------------ 2. stage-1 (tcgen05, split-K)
 
 constexpr int kS1Stages = 3;
-constexpr uint32_t kMuHalf = kTile * 128;          // 16 KB
-constexpr uint32_t kMuStage = 4 * kMuHalf;         // hi h0,h1, lo h0,h1
-constexpr uint32_t kQB = 2 * kG * 128;             // 4 KB
+constexpr uint32_t kMuHalf = kTile * 128;          // 16 KB: 128 kernels x 64 dims
 constexpr int kS1Threads = 192;                     // 0 TMA, 1 MMA, 2..5 epilogue
 
-struct S1Smem {
-  static constexpr uint32_t mu = 0;
-  static constexpr uint32_t q = mu + kS1Stages * kMuStage;
-  static constexpr uint32_t red = q + 2 * kQB;                    // [128][16] m, [128][16] s
-  static constexpr uint32_t bars = red + 2 * 128 * kG * 4;
-  static constexpr uint32_t total = bars + 32 * 8;
+// Head geometries: (G, D) = (16, 128) MiniCPM4-8B, (8, 64) MiniCPM4-0.5B.
+// Workspace strides are sized for G = 16 (kG) and shared by both.
+template <int G, int D>
+struct S1Cfg {
+  static constexpr int kDH = D / 64;                          // 64-dim halves
+  static constexpr uint32_t kMuStage = 2 * kDH * kMuHalf;     // hi halves, then lo halves
+  static constexpr uint32_t kQB = G * D * 2;                  // one query row's group (4 KB / 1 KB)
+  static constexpr uint32_t kQHalf = G * 128;                 // one 64-dim half of it
+  struct Smem {
+    static constexpr uint32_t mu = 0;
+    static constexpr uint32_t q = mu + kS1Stages * kMuStage;
+    static constexpr uint32_t red = q + 2 * kQB;              // [G][4] m, [G][4] s
+    static constexpr uint32_t bars = red + 2 * 128 * G * 4;
+    static constexpr uint32_t total = bars + 32 * 8;
+  };
 };
 
 struct S1Params {
@@ -155,8 +162,11 @@ __device__ __forceinline__ void s1_item(const S1Params& p, const TableView& tv, 
   *j1 = e < nk ? e : nk;
 }
 
+template <int G, int D>
 __global__ void __launch_bounds__(kS1Threads, 1)
 decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p) {
+  using C = S1Cfg<G, D>;
+  using S1Smem = typename C::Smem;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by pointer arithmetic on the __shared__ array (a uintptr_t round trip
   // loses the address space: every access would compile to generic LD/ST)
@@ -170,7 +180,7 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
   uint64_t* s_empty = bars + 12;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   float* red_m = reinterpret_cast<float*>(smem + S1Smem::red);
-  float* red_s = red_m + 128 * kG;
+  float* red_s = red_m + 128 * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TableView tv = table_view(p.table, p.n_seq);
   if (threadIdx.x == 0) {
@@ -205,27 +215,26 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
         if (j0 >= j1) continue;
         const int qb = it & 1;
         mbar_wait(q_empty + qb, ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full + qb, kQB);
-        uint8_t* qd = smem + S1Smem::q + qb * kQB;
-        tma_load_3d(qd, &tm_q, q_full + qb, 0, g * kG, s);
-        tma_load_3d(qd + kQB / 2, &tm_q, q_full + qb, 64, g * kG, s);
+        mbar_arrive_expect_tx(q_full + qb, C::kQB);
+        uint8_t* qd = smem + S1Smem::q + qb * C::kQB;
+        for (int hh = 0; hh < C::kDH; ++hh) tma_load_3d(qd + hh * C::kQHalf, &tm_q, q_full + qb, 64 * hh, g * G, s);
         const CUtensorMap* mhi = tv.maps + (int64_t)kMaps * s + 2;
         const CUtensorMap* mlo = tv.maps + (int64_t)kMaps * s + 3;
         for (int64_t t0 = j0; t0 < j1; t0 += kTile) {
           mbar_wait(mu_empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(mu_full + stage, kMuStage);
-          uint8_t* dst = smem + S1Smem::mu + stage * kMuStage;
-          tma_load_3d(dst, mhi, mu_full + stage, 0, (int)t0, g);
-          tma_load_3d(dst + kMuHalf, mhi, mu_full + stage, 64, (int)t0, g);
-          tma_load_3d(dst + 2 * kMuHalf, mlo, mu_full + stage, 0, (int)t0, g);
-          tma_load_3d(dst + 3 * kMuHalf, mlo, mu_full + stage, 64, (int)t0, g);
+          mbar_arrive_expect_tx(mu_full + stage, C::kMuStage);
+          uint8_t* dst = smem + S1Smem::mu + stage * C::kMuStage;
+          for (int hh = 0; hh < C::kDH; ++hh) {
+            tma_load_3d(dst + hh * kMuHalf, mhi, mu_full + stage, 64 * hh, (int)t0, g);
+            tma_load_3d(dst + (C::kDH + hh) * kMuHalf, mlo, mu_full + stage, 64 * hh, (int)t0, g);
+          }
           if (++stage == kS1Stages) { stage = 0; phase ^= 1; }
         }
         ++it;
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_bf16_f32(128, kG);
+    const uint32_t idesc = idesc_bf16_f32(128, G);
     int stage = 0, slot = 0;
     uint32_t phase = 0;
     uint32_t s_ph[2] = {0, 0};
@@ -237,20 +246,20 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
       if (j0 >= j1) continue;
       const int qb = it & 1;
       mbar_wait(q_full + qb, (it >> 1) & 1);
-      const uint32_t q_addr = smem_u32(smem + S1Smem::q + qb * kQB);
+      const uint32_t q_addr = smem_u32(smem + S1Smem::q + qb * C::kQB);
       for (int64_t t0 = j0; t0 < j1; t0 += kTile) {
         mbar_wait(mu_full + stage, phase);
         mbar_wait(s_empty + slot, s_ph[slot] ^ 1);
         s_ph[slot] ^= 1;
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t mu_s = smem_u32(smem + S1Smem::mu + stage * kMuStage);
+          const uint32_t mu_s = smem_u32(smem + S1Smem::mu + stage * C::kMuStage);
           for (int part = 0; part < 2; ++part) {
-            for (int k = 0; k < kD / 16; ++k) {
+            for (int k = 0; k < D / 16; ++k) {
               const uint32_t koff = (k & 3) * 32;
-              const uint32_t mu_k = mu_s + part * 2 * kMuHalf + (k >> 2) * kMuHalf + koff;
-              const uint32_t q_k = q_addr + (k >> 2) * (kQB / 2) + koff;
-              umma_f16_ss(tmem + slot * kG, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc, (part | k) ? 1u : 0u);
+              const uint32_t mu_k = mu_s + part * C::kDH * kMuHalf + (k >> 2) * kMuHalf + koff;
+              const uint32_t q_k = q_addr + (k >> 2) * C::kQHalf + koff;
+              umma_f16_ss(tmem + slot * 16, sdesc_k_sw128(mu_k), sdesc_k_sw128(q_k), idesc, (part | k) ? 1u : 0u);
             }
           }
           umma_commit(mu_empty + stage);
@@ -274,21 +283,21 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
       int s, g;
       int64_t j0, j1;
       s1_item(p, tv, item, &s, &g, &j0, &j1);
-      float* ps = p.pstat + item * (2 * kG);
+      float* ps = p.pstat + item * (2 * G);
       if (j0 >= j1) {
-        if (etid < kG) { ps[2 * etid] = -INFINITY; ps[2 * etid + 1] = 0.f; }
+        if (etid < G) { ps[2 * etid] = -INFINITY; ps[2 * etid + 1] = 0.f; }
         continue;
       }
-      float m[kG], sm[kG];
+      float m[G], sm[G];
 #pragma unroll
-      for (int h = 0; h < kG; ++h) { m[h] = -INFINITY; sm[h] = 0.f; }
+      for (int h = 0; h < G; ++h) { m[h] = -INFINITY; sm[h] = 0.f; }
       float* zg = p.zbuf + ((int64_t)s * p.hkv + g) * p.zstride;
       for (int64_t t0 = j0; t0 < j1; t0 += kTile) {
         mbar_wait(s_full + slot, s_ph[slot]);
         s_ph[slot] ^= 1;
         tc_fence_after();
-        float v[kG];
-        tmem_ld16(tmem + lane_base + slot * kG, v);
+        float v[G];
+        tmem_ld_n<G>(tmem + lane_base + slot * 16, v);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -297,12 +306,12 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
         const int64_t j = t0 + row;
         if (j < j1) {
 #pragma unroll
-          for (int h = 0; h < kG; ++h) v[h] *= p.zscale;
-          float4* dst = reinterpret_cast<float4*>(zg + j * kG);
+          for (int h = 0; h < G; ++h) v[h] *= p.zscale;
+          float4* dst = reinterpret_cast<float4*>(zg + j * G);
 #pragma unroll
-          for (int x = 0; x < 4; ++x) dst[x] = make_float4(v[4 * x], v[4 * x + 1], v[4 * x + 2], v[4 * x + 3]);
+          for (int x = 0; x < G / 4; ++x) dst[x] = make_float4(v[4 * x], v[4 * x + 1], v[4 * x + 2], v[4 * x + 3]);
 #pragma unroll
-          for (int h = 0; h < kG; ++h) {
+          for (int h = 0; h < G; ++h) {
             if (v[h] > m[h]) {
               sm[h] = sm[h] * ex2(m[h] - v[h]) + 1.f;
               m[h] = v[h];
@@ -314,7 +323,7 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
       }
       // (max, sum) per head: warp butterfly, then the 4 warps through smem
 #pragma unroll
-      for (int h = 0; h < kG; ++h) {
+      for (int h = 0; h < G; ++h) {
         float mm = m[h], ss = sm[h];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -327,7 +336,7 @@ decode_stage1_kernel(const __grid_constant__ CUtensorMap tm_q, const S1Params p)
         if (lane == 0) { red_m[h * 4 + quad] = mm; red_s[h * 4 + quad] = ss; }
       }
       named_bar_sync(1, 128);
-      if (etid < kG) {
+      if (etid < G) {
         float M = -INFINITY;
         for (int x = 0; x < 4; ++x) M = fmaxf(M, red_m[etid * 4 + x]);
         float S = 0.f;
@@ -362,8 +371,9 @@ struct ScoreParams {
 // Block scores for 64 blocks of one (sequence, group); the last CTA of the
 // (sequence, group) to finish (device counter) then runs the top-k over all of
 // them, so selection needs no extra launch.
+template <int G>
 __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p) {
-  __shared__ float lse2[kG];
+  __shared__ float lse2[G];
   __shared__ float sk[kBlkChunk * 8 + 8];   // kernels of this block range (kpb <= 8)
   __shared__ float lkey[topk::kListCap];
   __shared__ int lid[topk::kListCap];
@@ -386,19 +396,20 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
   if (b0 >= n_cand) return;
   const int64_t b1 = b0 + kBlkChunk < n_cand ? b0 + kBlkChunk : n_cand;
   {
-    // per-head LSE from the chunk partials: 16 lanes per head, shuffle merge
-    const float* ps = p.pstat + sg * p.nchunk * (2 * kG);
-    const int h = threadIdx.x >> 4, sub = threadIdx.x & 15;     // 256 threads = 16 heads x 16
+    // per-head LSE from the chunk partials: 256 / G lanes per head, shuffle merge
+    constexpr int kLanes = 256 / G;                             // 16 (G = 16) or 32 (G = 8)
+    const float* ps = p.pstat + sg * p.nchunk * (2 * G);
+    const int h = threadIdx.x / kLanes, sub = threadIdx.x % kLanes;
     float M = -INFINITY, S = 0.f;
-    for (int64_t c = sub; c < p.nchunk; c += 16) {
-      const float mm = ps[c * 2 * kG + 2 * h], ss = ps[c * 2 * kG + 2 * h + 1];
+    for (int64_t c = sub; c < p.nchunk; c += kLanes) {
+      const float mm = ps[c * 2 * G + 2 * h], ss = ps[c * 2 * G + 2 * h + 1];
       if (mm == -INFINITY) continue;
       const float nm = fmaxf(M, mm);
       S = (M == -INFINITY ? 0.f : S * ex2(M - nm)) + ss * ex2(mm - nm);
       M = nm;
     }
 #pragma unroll
-    for (int off = 8; off > 0; off >>= 1) {
+    for (int off = kLanes / 2; off > 0; off >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, M, off);
       const float os = __shfl_xor_sync(0xffffffffu, S, off);
       const float nm = fmaxf(M, om);
@@ -413,15 +424,15 @@ __global__ void __launch_bounds__(256) decode_scores_kernel(const ScoreParams p)
   jhi = b1 * p.kpb < nk_t ? b1 * p.kpb : nk_t;
   const float* zg = p.zbuf + sg * p.zstride;
   for (int64_t j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
-    const float4* z4 = reinterpret_cast<const float4*>(zg + j * kG);
+    const float4* z4 = reinterpret_cast<const float4*>(zg + j * G);
     float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
+    for (int x = 0; x < G / 4; ++x) {
       const float4 z = z4[x];
       a0 += ex2(z.x - lse2[4 * x]) + ex2(z.z - lse2[4 * x + 2]);
       a1 += ex2(z.y - lse2[4 * x + 1]) + ex2(z.w - lse2[4 * x + 3]);
     }
-    sk[j - jlo] = (a0 + a1) * (1.0f / kG);
+    sk[j - jlo] = (a0 + a1) * (1.0f / G);
   }
   __syncthreads();
   float* rrow = p.rbuf + sg * p.nb_cap;
@@ -555,7 +566,9 @@ static DecodeWs decode_ws_layout(const infllm2_geometry& g, int n_seq, int hkv, 
 }
 
 bool decode_supported(const infllm2_geometry& g, int hq, int hkv, int d) {
-  return hkv <= kMaxHkv && hq / hkv == kG && hq % hkv == 0 && d == kD && g.kernel_stride == kS && g.kernel_size == kP &&
+  const int G = hkv > 0 ? hq / hkv : 0;
+  return hkv > 0 && hkv <= kMaxHkv && hq % hkv == 0 && ((G == 16 && d == 128) || (G == 8 && d == 64)) &&
+         g.kernel_stride == kS && g.kernel_size == kP &&
          g.block_size == 64 && g.coarse_stride % kS == 0 && infllm2_max_selected(&g) <= 80;
 }
 
@@ -584,23 +597,11 @@ static int note_decode_launch(cudaStream_t stream, const void* table) {
 }
 long long decode_early_launches() { return g_early_launches; }
 
-int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv, int d,
-                const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32,
-                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream, int share) {
-  DecodeWs w = decode_ws_layout(g, n_seq, hkv, max_len_after, ws);
-  if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
-  const int max_sel = infllm2_max_selected(&g);
-  const TableView tvd = table_view(table, n_seq);
-  const bool fused = decode_fused_supported(g, n_seq, hkv, max_len_after, share);
-  const int early = note_decode_launch(stream, fused ? table : nullptr);
-  if (fused)
-    return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
-                             lse, w.fused, stream, share, early);
-  // 1. append + compress (3 CTAs per sequence)
-  if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,
-                 static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
-                 (int)g.coarse_stride) != cudaSuccess)
-    return INFLLM2_ERR_CUDA;
+// Launches 2-4 of the five-launch path for one head geometry.
+template <int G, int D>
+static int decode_select(const infllm2_geometry& g, void* table, int n_seq, int hq, int hkv, const void* q,
+                         int32_t* selection, const DecodeWs& w, int max_sel, cudaStream_t stream) {
+  using C = S1Cfg<G, D>;
   // 2. stage-1 split-K
   S1Params sp;
   sp.table = table;
@@ -610,22 +611,22 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   sp.zstride = w.zstride;
   sp.zbuf = w.zbuf;
   sp.pstat = w.pstat;
-  sp.zscale = 1.4426950408889634f / sqrtf((float)kD);
+  sp.zscale = 1.4426950408889634f / sqrtf((float)D);
   CUtensorMap tq;
   {
-    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
-    const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
-    const uint32_t box[3] = {64, (uint32_t)kG, 1};
+    const uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)n_seq};
+    const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)hq * D * 2};
+    const uint32_t box[3] = {64, (uint32_t)G, 1};
     if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
   }
-  const size_t smem1 = S1Smem::total + 1024;
-  if (smem_attr_once((const void*)decode_stage1_kernel, (int)smem1) != cudaSuccess)
+  const size_t smem1 = C::Smem::total + 1024;
+  if (smem_attr_once((const void*)decode_stage1_kernel<G, D>, (int)smem1) != cudaSuccess)
     return INFLLM2_ERR_CUDA;
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items1 = (int64_t)n_seq * hkv * w.nchunk;
-  if (launch_pdl(decode_stage1_kernel, dim3((unsigned)(items1 < sms ? items1 : sms)), dim3(kS1Threads), smem1, stream,
-                 tq, sp) != cudaSuccess)
+  if (launch_pdl(decode_stage1_kernel<G, D>, dim3((unsigned)(items1 < sms ? items1 : sms)), dim3(kS1Threads), smem1,
+                 stream, tq, sp) != cudaSuccess)
     return INFLLM2_ERR_CUDA;
   // 3. block scores + (last CTA) top-k
   ScoreParams scp;
@@ -649,13 +650,41 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   scp.selection = selection;
   const size_t sc_smem = sizeof(float) * (size_t)w.nb_cap;
   if (sc_smem > 40 * 1024 &&
-      smem_attr_once((const void*)decode_scores_kernel, (int)sc_smem) != cudaSuccess)
+      smem_attr_once((const void*)decode_scores_kernel<G>, (int)sc_smem) != cudaSuccess)
     return INFLLM2_ERR_UNSUPPORTED;
-  if (launch_pdl(decode_scores_kernel, dim3((unsigned)(n_seq * hkv * w.nbchunk)), dim3(256), sc_smem, stream, scp) !=
-      cudaSuccess)
+  if (launch_pdl(decode_scores_kernel<G>, dim3((unsigned)(n_seq * hkv * w.nbchunk)), dim3(256), sc_smem, stream,
+                 scp) != cudaSuccess)
     return INFLLM2_ERR_CUDA;
+  return INFLLM2_OK;
+}
+
+int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv, int d,
+                const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out, int out_f32,
+                float* lse, void* ws, size_t ws_bytes, cudaStream_t stream, int share) {
+  DecodeWs w = decode_ws_layout(g, n_seq, hkv, max_len_after, ws);
+  if (ws == nullptr || ws_bytes < w.bytes) return INFLLM2_ERR_WORKSPACE;
+  if (!decode_supported(g, hq, hkv, d)) return INFLLM2_ERR_UNSUPPORTED;
+  const int max_sel = infllm2_max_selected(&g);
+  const TableView tvd = table_view(table, n_seq);
+  const bool g16 = hq / hkv == kG && d == kD;     // else (8, 64): MiniCPM4-0.5B
+  // the one-launch cluster kernel covers the 8B geometry; the 0.5B geometry
+  // takes the five-launch path below
+  const bool fused = g16 && decode_fused_supported(g, n_seq, hkv, max_len_after, share);
+  const int early = note_decode_launch(stream, fused ? table : nullptr);
+  if (fused)
+    return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
+                             lse, w.fused, stream, share, early);
+  // 1. append + compress (3 CTAs per sequence)
+  if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,
+                 static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
+                 (int)g.coarse_stride) != cudaSuccess)
+    return INFLLM2_ERR_CUDA;
+  // 2-4. stage-1 scores, block scores, top-k
+  const int rc = g16 ? decode_select<16, 128>(g, table, n_seq, hq, hkv, q, selection, w, max_sel, stream)
+                     : decode_select<8, 64>(g, table, n_seq, hq, hkv, q, selection, w, max_sel, stream);
+  if (rc != INFLLM2_OK) return rc;
   // 5. stage 2
-  cudaError_t e = launch_attend_tc_decode(hq, hkv, max_sel, n_seq, q, tvd.maps, kMaps, tvd.len, selection, out,
+  cudaError_t e = launch_attend_tc_decode(hq, hkv, d, max_sel, n_seq, q, tvd.maps, kMaps, tvd.len, selection, out,
                                           out_f32, lse, w.split, stream);
   if (e != cudaSuccess) return INFLLM2_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? INFLLM2_OK : INFLLM2_ERR_CUDA;

@@ -94,16 +94,16 @@ class DecodeBatch:
         self._write_link()
 
     def _fused_ok(self, hq: int, hkv: int, d: int) -> bool:
-        """The library's own predicate (infllm2_decode_supported: G = 16, D = 128,
-        s = 16, p = 32, m = 64, max_selected <= 80); other geometries step each
-        sequence through the prefill kernels."""
+        """The library's own predicate (infllm2_decode_supported: (G, D) = (16, 128)
+        or (8, 64), s = 16, p = 32, m = 64, max_selected <= 80); other geometries
+        step each sequence through the prefill kernels."""
         return bool(self._lib.infllm2_decode_supported(ctypes.byref(self.config.geometry()), hq, hkv, d))
 
     def _step_per_sequence(self, q, k_new, v_new, return_selection, return_lse, out_dtype, bookkeep):
         """One decode step per sequence with the (n = 1) prefill kernels — same
         semantics (append, then attend the new row, model.py:434-444)."""
         if not bookkeep:
-            raise ValidationError("graph replay (bookkeep=False) needs the batched decode kernels (G = 16, D = 128)")
+            raise ValidationError("graph replay (bookkeep=False) needs the batched decode kernels (G, D = 16, 128 or 8, 64)")
         outs, sels, lses = [], [], []
         for i, layer in enumerate(self.layers):
             layer.append(k_new[i:i + 1], v_new[i:i + 1])

@@ -1,0 +1,157 @@
+"""Batched decode for the MiniCPM4-0.5B head geometry (G = 8 heads per KV
+group, D = 64): the five-launch decode path (csrc/decode.cu: append + compress,
+tcgen05 stage-1 split-K, block scores + top-k, stage 2 on attend_tc_kernel<8, 64>
+with per-sequence K/V maps, split-K combine) instead of stepping every sequence
+through the prefill kernels.
+
+Checks, per step (the reference's decode = append then attend n = 1,
+/root/reference/pkg/src/deskinfer/model.py:434-444):
+* selections identical to the float64 CUDA-core verifier on the same cache;
+* outputs / LSE within the tensor-core bars of it;
+* kernel means bitwise equal to a rebuild;
+* the launch count of a step does not grow with the number of sequences (the
+  batched kernels run, not the per-sequence fallback);
+* a captured CUDA graph replayed with ``advance`` equals eager stepping bitwise
+  and keeps host and device lengths equal;
+* the last step's selections equal the CPU oracle.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from bars import LSE_TC, OUT_ABS, OUT_REL
+from oracle import infllm2_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2506_07900_b200 as P  # noqa: E402
+from paper_2506_07900_b200 import _lib  # noqa: E402
+
+HQ, HKV, D = 16, 2, 64
+
+
+def _caches(lengths, cfg, seed, extra):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    layers = []
+    for L in lengths:
+        c = P.BlockizedLayerCache(HKV, D, cfg, capacity=L + extra)
+        c.append(torch.randn((L, HKV, D), generator=gen, device="cuda").to(torch.bfloat16),
+                 torch.randn((L, HKV, D), generator=gen, device="cuda").to(torch.bfloat16))
+        layers.append(c)
+    return layers, gen
+
+
+def _device_lengths(batch):
+    lib = _lib.load()
+    n = len(batch.layers)
+    buf = (ctypes.c_int64 * n)()
+    _lib.check(lib.infllm2_decode_table_lengths(batch._table.data_ptr(), n, buf,
+                                                torch.cuda.current_stream().cuda_stream), "lengths")
+    return list(buf)
+
+
+def _verify(batch, cfg, q, sel, out, lse):
+    for i, layer in enumerate(batch.layers):
+        o2, s2, l2 = P.two_stage_attention(q[i:i + 1], layer, cfg, layer.length - 1, exact=True,
+                                           return_selection=True, return_lse=True, out_dtype=torch.float32)
+        assert torch.equal(sel[i], s2[0]), (i, sel[i].tolist(), s2[0].tolist())
+        err = (out[i].float() - o2[0]).abs()
+        assert bool((err <= OUT_ABS + OUT_REL * o2[0].abs()).all()), err.max().item()
+        assert (lse[i] - l2[0]).abs().max().item() <= LSE_TC
+
+
+@pytest.mark.parametrize("lengths,topk", [([3000, 5000, 777, 8190], 16), ([127, 1000, 4093], 8),
+                                          ([64, 2111], 64), ([20000, 12000], 32)])
+def test_decode_05b_eager_vs_verifier(lengths, topk):
+    cfg = P.SparseAttentionConfig(top_k=topk)
+    steps = 4
+    layers, gen = _caches(lengths, cfg, 61 + topk, steps + 4)
+    lib = _lib.load()
+    assert lib.infllm2_decode_supported(ctypes.byref(cfg.geometry()), HQ, HKV, D) == 1
+    batch = P.DecodeBatch(layers, cfg)
+    S = len(lengths)
+    for st in range(steps):
+        q = torch.randn((S, HQ, D), generator=gen, device="cuda").to(torch.bfloat16)
+        kn = torch.randn((S, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+        vn = torch.randn((S, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+        n0 = lib.infllm2_launch_count()
+        out, sel, lse = batch.step(q, kn, vn, return_selection=True, return_lse=True, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert lib.infllm2_launch_count() - n0 <= 5, "0.5B decode fell back to the per-sequence path"
+        assert [l.length for l in layers] == [L + st + 1 for L in lengths]
+        assert _device_lengths(batch) == [l.length for l in layers]
+        _verify(batch, cfg, q, sel, out, lse)
+        for layer in layers:
+            fine, coarse = layer.rebuild_kernels()
+            assert torch.equal(layer.fine_means.contiguous(), fine.contiguous())
+            assert torch.equal(layer.coarse_means.contiguous(), coarse.contiguous())
+    # last step vs the CPU oracle (float64 dots)
+    geom = O.Geometry(top_k=topk)
+    for i in range(S):
+        k = layers[i].keys.float().cpu().numpy()
+        v = layers[i].values.float().cpu().numpy()
+        fine = O.window_means(k, 32, 16)
+        ref = O.two_stage_attention(q[i:i + 1].float().cpu().numpy(), k, v, fine, geom, layers[i].length - 1)
+        assert np.array_equal(sel[i].cpu().numpy(), ref.selection[0]), i
+        err = np.abs(out[i].cpu().numpy() - ref.out[0])
+        assert (err <= OUT_ABS + OUT_REL * np.abs(ref.out[0])).all(), err.max()
+
+
+def test_decode_05b_graph_replay_equals_eager():
+    cfg = P.SparseAttentionConfig(top_k=16)
+    lengths, steps = [9000, 20000, 4097], 5
+    extra = steps + 8
+    la, gen = _caches(lengths, cfg, 5, extra)
+    lb, _ = _caches(lengths, cfg, 5, extra)
+    S = len(lengths)
+    q = torch.randn((steps, S, HQ, D), generator=gen, device="cuda").to(torch.bfloat16)
+    kn = torch.randn((steps, S, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+    vn = torch.randn((steps, S, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+    bound = max(lengths) + extra
+    eager = P.DecodeBatch(la, cfg)
+    want = [eager.step(q[t], kn[t], vn[t], max_len=bound, return_selection=True, return_lse=True) for t in range(steps)]
+    batch = P.DecodeBatch(lb, cfg)
+    batch.reserve(extra)
+    o, s, l = batch.step(q[0], kn[0], vn[0], max_len=bound, return_selection=True, return_lse=True)
+    got = [(o, s, l)]
+    qb, kb, vb = q[1].clone(), kn[1].clone(), vn[1].clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            go, gs, gl = batch.step(qb, kb, vb, max_len=bound, bookkeep=False, return_selection=True,
+                                    return_lse=True)
+    torch.cuda.synchronize()
+    assert _device_lengths(batch) == [L + 1 for L in lengths]
+    for t in range(1, steps):
+        qb.copy_(q[t])
+        kb.copy_(kn[t])
+        vb.copy_(vn[t])
+        graph.replay()
+        batch.advance(1)
+        torch.cuda.synchronize()
+        assert _device_lengths(batch) == [x.length for x in lb]
+        got.append((go.clone(), gs.clone(), gl.clone()))
+    for t in range(steps):
+        for a, b in zip(got[t], want[t]):
+            assert torch.equal(a, b), t
+    for a, b in zip(la, lb):
+        assert torch.equal(a.keys, b.keys) and torch.equal(a.values, b.values)
+        assert torch.equal(a.fine_means, b.fine_means) and torch.equal(a.coarse_means, b.coarse_means)
+
+
+@pytest.mark.parametrize("top_k", [2, 3])
+def test_decode_05b_consume_budget_zero(top_k):
+    cfg = P.SparseAttentionConfig(top_k=top_k, forced_consume_budget=True)
+    layers, gen = _caches([5000, 777, 130], cfg, 9, 8)
+    batch = P.DecodeBatch(layers, cfg)
+    for st in range(3):
+        q = torch.randn((3, HQ, D), generator=gen, device="cuda").to(torch.bfloat16)
+        kn = torch.randn((3, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+        vn = torch.randn((3, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+        out, sel, lse = batch.step(q, kn, vn, return_selection=True, return_lse=True, out_dtype=torch.float32)
+        _verify(batch, cfg, q, sel, out, lse)

@@ -130,8 +130,9 @@ def test_fused_decode_matches_five_launch_path(lengths, monkeypatch):
 
 
 def test_decode_batch_small_model_shape():
-    """MiniCPM4-0.5B geometry (G = 8, D = 64): DecodeBatch steps each sequence
-    through the prefill kernels; equals an independently built cache."""
+    """MiniCPM4-0.5B geometry (G = 8, D = 64): the batched five-launch decode
+    path equals the prefill path on an independently built cache (selections
+    identical; outputs within float32 noise of the split-P prefill)."""
     cfg = P.SparseAttentionConfig(top_k=16)
     lengths = [1500, 3001]
     full = [make_qkv(91 + i, L + 3, 3, 16, 2, 64) for i, L in enumerate(lengths)]
@@ -151,6 +152,6 @@ def test_decode_batch_small_model_shape():
             ref = P.BlockizedLayerCache(2, 64, cfg)
             ref.append(torch.from_numpy(k[:n_now]).cuda(), torch.from_numpy(v[:n_now]).cuda())
             o2, s2 = P.two_stage_attention(qs[i:i + 1], ref, cfg, n_now - 1, return_selection=True,
-                                           out_dtype=torch.float32)
+                                           out_dtype=torch.float32, split_p=True)
             assert torch.equal(sel[i], s2[0])
-            assert (out[i] - o2[0]).abs().max().item() < 1e-5
+            assert (out[i] - o2[0]).abs().max().item() < 1e-4
