@@ -258,9 +258,9 @@ typedef struct infllm2_seq_desc {
   int64_t coarse_cap;
 } infllm2_seq_desc;
 
-/* 1 when infllm2_decode_step covers this geometry (G = 16, D = 128, s = 16,
- * p = 32, m = 64, max_selected <= 80), else 0: callers step other shapes
- * through infllm2_forward one sequence at a time. */
+/* 1 when infllm2_decode_step covers this geometry ((G, D) = (16, 128) or
+ * (8, 64), s = 16, p = 32, m = 64, max_selected <= 80), else 0: callers step
+ * other shapes through infllm2_forward one sequence at a time. */
 int infllm2_decode_supported(const infllm2_geometry* g, int32_t hq, int32_t hkv, int32_t d);
 /* Device table (descriptors, TMA tensor maps, device-resident lengths). */
 size_t infllm2_decode_table_bytes(int32_t n_seq);

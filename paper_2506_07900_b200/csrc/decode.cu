@@ -38,9 +38,10 @@ cudaError_t launch_attend_tc_decode(int hq, int hkv, int d, int max_sel, int64_t
                                     float* split_ws, cudaStream_t stream);
 size_t attend_split_workspace(int64_t n_seq, int hkv, int max_sel);
 size_t decode_fused_workspace_bytes(int n_seq, int hkv);
-bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int share);
+bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hq, int hkv, int d, int64_t max_len_after,
+                            int share);
 int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
-                      const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
+                      int d, const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
                       int out_f32, float* lse, void* ws, cudaStream_t stream, int share, int early);
 
 namespace {
@@ -667,12 +668,10 @@ int decode_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_l
   const int max_sel = infllm2_max_selected(&g);
   const TableView tvd = table_view(table, n_seq);
   const bool g16 = hq / hkv == kG && d == kD;     // else (8, 64): MiniCPM4-0.5B
-  // the one-launch cluster kernel covers the 8B geometry; the 0.5B geometry
-  // takes the five-launch path below
-  const bool fused = g16 && decode_fused_supported(g, n_seq, hkv, max_len_after, share);
+  const bool fused = decode_fused_supported(g, n_seq, hq, hkv, d, max_len_after, share);
   const int early = note_decode_launch(stream, fused ? table : nullptr);
   if (fused)
-    return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, q, k_new, v_new, selection, out, out_f32,
+    return decode_fused_step(g, table, n_seq, max_len_after, hq, hkv, d, q, k_new, v_new, selection, out, out_f32,
                              lse, w.fused, stream, share, early);
   // 1. append + compress (3 CTAs per sequence)
   if (launch_pdl(decode_append_compress_kernel, dim3(n_seq, 3), dim3(256), 0, stream, table, n_seq, hkv, d,

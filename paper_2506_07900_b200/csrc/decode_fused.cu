@@ -39,6 +39,9 @@
 //      row and its LSE.
 // Clusters loop over segments (the grid is co-resident); the last CTA to read
 // the lengths at the start bumps every sequence's device-side length.
+// Templated on the head geometry: (G, D) = (16, 128) (MiniCPM4-8B, described
+// above) and (8, 64) (MiniCPM4-0.5B: N = 8 heads per MMA, one 64-dim half per
+// operand, the combine merges 4 heads per pass).
 #include <float.h>
 #include <stdlib.h>
 
@@ -56,8 +59,6 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kG = 16;
-constexpr int kD = 128;
 constexpr int kS = 16;
 constexpr int kM = 64;
 constexpr int kMaxCl = 8;                     // CTAs per cluster = pieces per segment (runtime 3..8)
@@ -67,30 +68,41 @@ constexpr int kMaxTiles = 28;                 // z tiles resident in TMEM (16 co
 constexpr int kMaxRows = kMaxTiles * 128;     // kernels per piece
 constexpr int kMaxPieceBlocks = (kMaxRows - 1) / 4;
 constexpr int kMaxBudget = 32;
-constexpr int kPartStride = kG * kD + 2 * kG; // floats per stage-2 partial
 constexpr int kMaxSeq = 160;
 constexpr uint32_t kColS2 = 448;
 constexpr uint32_t kColO = 464;
 
 constexpr uint32_t kHalf = 128 * 128;         // 16 KB: 128 rows x 64 bf16
-constexpr uint32_t kStageBytes = 4 * kHalf;   // 64 KB: mu hi/lo tile, or K + V tile
-constexpr uint32_t kQB = 2 * kG * 128;        // 4 KB
-constexpr uint32_t kPHalf = 128 * kG * 2;     // 4 KB
+constexpr uint32_t kStageBytes = 4 * kHalf;   // 64 KB ring stage: mu hi/lo tile, or K + V tile
 
-struct Smem {
-  static constexpr uint32_t ring = 0;
-  static constexpr uint32_t q = ring + kStages * kStageBytes;
-  static constexpr uint32_t p = q + kQB;                         // P hi/lo; top-k lists / merge flags alias it
-  static constexpr uint32_t sarr = p + 2 * kPHalf;               // S_j; merge list; stage-2 partial slots
-  static constexpr uint32_t rarr = sarr + kMaxRows * 4;          // R_b; filtered merge list
-  static constexpr uint32_t xch = rarr + (kMaxPieceBlocks + 9) * 4;   // published: [32] LSE partial, [64] candidates
-  static constexpr uint32_t red = xch + (2 * kG + 2 * kMaxBudget) * 4;
-  static constexpr uint32_t bars = (red + (4 * kG * 2 + 2 * kG + 8) * 4 + 7) / 8 * 8;
-  static constexpr uint32_t total = bars + (kMaxTiles + 24) * 8 + 16;
+// Head geometry (G heads per KV group, head dim D): (16, 128) MiniCPM4-8B,
+// (8, 64) MiniCPM4-0.5B.  With D = 64 a stage holds one 64-dim half of each
+// operand (K at 0, V at 2 * kHalf); stage 2's PV still runs M = 128 over O^T
+// (lanes >= D read the unused upper half of the V slot and are never stored).
+template <int G, int D>
+struct FCfg {
+  static constexpr int kDH = D / 64;
+  static constexpr uint32_t kMuBytes = 2 * kDH * kHalf;        // one stage-1 tile: hi halves, then lo halves
+  static constexpr uint32_t kQB = G * D * 2;                    // 4 KB / 1 KB
+  static constexpr uint32_t kQHalf = G * 128;                   // one 64-dim half of Q
+  static constexpr uint32_t kPHalf = 128 * G * 2;               // P (hi or lo) of one 128-row tile
+  static constexpr int kPartStride = G * D + 2 * G;             // floats per stage-2 partial
+  struct Smem {
+    static constexpr uint32_t ring = 0;
+    static constexpr uint32_t q = ring + kStages * kStageBytes;
+    static constexpr uint32_t p = q + kQB;                       // P hi/lo; top-k lists / merge flags alias it
+    static constexpr uint32_t sarr = p + 2 * kPHalf;             // S_j; merge list; stage-2 partial slots
+    static constexpr uint32_t rarr = sarr + kMaxRows * 4;        // R_b; filtered merge list
+    static constexpr uint32_t xch = rarr + (kMaxPieceBlocks + 9) * 4;   // published: [2G] LSE partial, [64] candidates
+    static constexpr uint32_t red = xch + (2 * G + 2 * kMaxBudget) * 4;
+    static constexpr uint32_t bars = (red + (4 * G * 2 + 2 * G + 8) * 4 + 7) / 8 * 8;
+    static constexpr uint32_t total = bars + (kMaxTiles + 24) * 8 + 16;
+  };
+  static_assert(Smem::total + 1024 + 2048 <= 232448, "fused decode shared memory");
+  static_assert(topk::kListCap * 8 <= 2 * kPHalf, "top-k lists alias the P buffer");
+  static_assert((128 + 2 * 256) * 4 <= 2 * kPHalf, "cta_topk scratch aliases the P buffer");
+  static_assert(kPartStride * 4 <= Smem::xch - Smem::sarr, "the stage-2 partial fits the sarr/rarr region");
 };
-static_assert(Smem::total + 1024 + 2048 <= 232448, "fused decode shared memory");
-static_assert(topk::kListCap * 8 <= 2 * kPHalf, "top-k lists alias the P buffer");
-static_assert(kPartStride * 4 <= Smem::xch - Smem::sarr, "the stage-2 partial fits the sarr/rarr region");
 
 struct Params {
   void* table;
@@ -247,9 +259,12 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float om, float os
   s = (m == -INFINITY ? 0.f : s * ex2(m - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
   m = nm;
 }
-__device__ __forceinline__ void warp_reduce16_lse(float (&m)[16], float (&s)[16], int lane) {
+// (max, sum) pairs of N heads reduce-scattered across the warp: lane l ends
+// with head reduce_head_n<N>(l) (lanes sharing bits 4..(5 - log2 N) agree).
+template <int N>
+__device__ __forceinline__ void warp_reduce_lse_n(float (&m)[N], float (&s)[N], int lane) {
 #pragma unroll
-  for (int w = 8, off = 16; w >= 1; w >>= 1, off >>= 1) {
+  for (int w = N / 2, off = 16; w >= 1; w >>= 1, off >>= 1) {
     const bool up = (lane & off) != 0;
 #pragma unroll
     for (int i = 0; i < w; ++i) {
@@ -260,7 +275,9 @@ __device__ __forceinline__ void warp_reduce16_lse(float (&m)[16], float (&s)[16]
       s[i] = ks;
     }
   }
-  lse_merge(m[0], s[0], __shfl_xor_sync(0xffffffffu, m[0], 1), __shfl_xor_sync(0xffffffffu, s[0], 1));
+#pragma unroll
+  for (int off = 16 / N; off >= 1; off >>= 1)
+    lse_merge(m[0], s[0], __shfl_xor_sync(0xffffffffu, m[0], off), __shfl_xor_sync(0xffffffffu, s[0], off));
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -391,8 +408,16 @@ __device__ bool cta_topk(const float* r, int64_t base, int lo, int hi, int budge
   return true;
 }
 
+template <int G, int D>
 __global__ void __launch_bounds__(kThreads, 1)
 decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) {
+  using C = FCfg<G, D>;
+  using Smem = typename C::Smem;
+  constexpr int kG = G;
+  constexpr int kD = D;
+  constexpr int kDH = C::kDH;
+  constexpr uint32_t kQB = C::kQB;
+  constexpr uint32_t kPHalf = C::kPHalf;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by pointer arithmetic on the __shared__ array (a uintptr_t round trip
   // loses the address space: every access would compile to generic LD/ST)
@@ -416,7 +441,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
   uint64_t* s_full = bars + 24;          // [kMaxTiles], one phase per segment
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24 + kMaxTiles);
   float* red = reinterpret_cast<float*>(smem + Smem::red);
-  float* xpart = reinterpret_cast<float*>(smem + Smem::xch);          // [16][2] (max, sum 2^z)
+  float* xpart = reinterpret_cast<float*>(smem + Smem::xch);          // [G][2] (max, sum 2^z)
   float* xcand = xpart + 2 * kG;                                      // [budget][2] (key, id bits)
   __shared__ int sel_s[96];
   __shared__ int64_t len_s[kMaxSeq];
@@ -503,13 +528,14 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           tma_prefetch(mlo);
           for (int t = 0; t < I.ntiles && t < kStages && t != I.dirty_tile; ++t, ++pre) {
             mbar_wait(empty + stage, phase ^ 1);
-            mbar_arrive_expect_tx(full + stage, kStageBytes);
+            mbar_arrive_expect_tx(full + stage, C::kMuBytes);
             uint8_t* dst = smem + Smem::ring + stage * kStageBytes;
             const int row = (int)(I.r0 + 128 * t);
-            tma_load_3d(dst, mhi, full + stage, 0, row, I.g);
-            tma_load_3d(dst + kHalf, mhi, full + stage, 64, row, I.g);
-            tma_load_3d(dst + 2 * kHalf, mlo, full + stage, 0, row, I.g);
-            tma_load_3d(dst + 3 * kHalf, mlo, full + stage, 64, row, I.g);
+#pragma unroll
+            for (int hh = 0; hh < kDH; ++hh) {
+              tma_load_3d(dst + hh * kHalf, mhi, full + stage, 64 * hh, row, I.g);
+              tma_load_3d(dst + (kDH + hh) * kHalf, mlo, full + stage, 64 * hh, row, I.g);
+            }
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
@@ -532,18 +558,19 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         mbar_wait(q_empty, par ^ 1);
         mbar_arrive_expect_tx(q_full, kQB);
         uint8_t* qd = smem + Smem::q;
-        tma_load_3d(qd, &tm_q, q_full, 0, I.g * kG, I.s);
-        tma_load_3d(qd + kQB / 2, &tm_q, q_full, 64, I.g * kG, I.s);
+#pragma unroll
+        for (int hh = 0; hh < kDH; ++hh) tma_load_3d(qd + hh * C::kQHalf, &tm_q, q_full, 64 * hh, I.g * kG, I.s);
         for (int t = it == 0 ? pre : 0; t < I.ntiles; ++t) {
           if (t == I.dirty_tile) mbar_wait(appended, par);   // this CTA's window re-sync is in global memory
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(full + stage, kStageBytes);
+          mbar_arrive_expect_tx(full + stage, C::kMuBytes);
           uint8_t* dst = smem + Smem::ring + stage * kStageBytes;
           const int row = (int)(I.r0 + 128 * t);
-          tma_load_3d(dst, mhi, full + stage, 0, row, I.g);
-          tma_load_3d(dst + kHalf, mhi, full + stage, 64, row, I.g);
-          tma_load_3d(dst + 2 * kHalf, mlo, full + stage, 0, row, I.g);
-          tma_load_3d(dst + 3 * kHalf, mlo, full + stage, 64, row, I.g);
+#pragma unroll
+          for (int hh = 0; hh < kDH; ++hh) {
+            tma_load_3d(dst + hh * kHalf, mhi, full + stage, 64 * hh, row, I.g);
+            tma_load_3d(dst + (kDH + hh) * kHalf, mlo, full + stage, 64 * hh, row, I.g);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (it == 0) trace(p.trace, 1);
@@ -573,16 +600,17 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           const int nt = tile_blocks(I, t);
           const int b0 = tile_block(I, sel_s, t, 0), b1 = tile_block(I, sel_s, t, 1);
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(full + stage, nt * 4 * (kM * 128));
+          mbar_arrive_expect_tx(full + stage, nt * 2 * kDH * (kM * 128));
           uint8_t* kd = smem + Smem::ring + stage * kStageBytes;
           uint8_t* vd = kd + 2 * kHalf;
           for (int x = 0; x < nt; ++x) {
             const int row0 = (x ? b1 : b0) * kM;
             const uint32_t off = x * kM * 128;
-            tma_load_3d(kd + off, mk, full + stage, 0, row0, I.g);
-            tma_load_3d(kd + kHalf + off, mk, full + stage, 64, row0, I.g);
-            tma_load_3d(vd + off, mv, full + stage, 0, row0, I.g);
-            tma_load_3d(vd + kHalf + off, mv, full + stage, 64, row0, I.g);
+#pragma unroll
+            for (int hh = 0; hh < kDH; ++hh) {
+              tma_load_3d(kd + hh * kHalf + off, mk, full + stage, 64 * hh, row0, I.g);
+              tma_load_3d(vd + hh * kHalf + off, mv, full + stage, 64 * hh, row0, I.g);
+            }
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -615,8 +643,8 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           for (int part = 0; part < 2; ++part)
             for (int k = 0; k < kD / 16; ++k) {
               const uint32_t koff = (k & 3) * 32;
-              umma_f16_ss(tmem + t * kG, sdesc_k_sw128(mu_s + part * 2 * kHalf + (k >> 2) * kHalf + koff),
-                          sdesc_k_sw128(q_addr + (k >> 2) * (kQB / 2) + koff), idesc, (part | k) ? 1u : 0u);
+              umma_f16_ss(tmem + t * kG, sdesc_k_sw128(mu_s + part * kDH * kHalf + (k >> 2) * kHalf + koff),
+                          sdesc_k_sw128(q_addr + (k >> 2) * C::kQHalf + koff), idesc, (part | k) ? 1u : 0u);
             }
           umma_commit(empty + stage);
           umma_commit(s_full + t);
@@ -637,7 +665,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         if (elect_one()) {
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-            const uint32_t qoff = (k >> 2) * (kQB / 2) + (k & 3) * 32;
+            const uint32_t qoff = (k >> 2) * C::kQHalf + (k & 3) * 32;
             umma_f16_ss(tmem + kColS2, sdesc_k_sw128(k_addr + off), sdesc_k_sw128(q_addr + qoff), idesc,
                         k > 0 ? 1u : 0u);
           }
@@ -653,9 +681,10 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           const int ksteps = nt == 2 ? 8 : 4;
           for (int k = 0; k < ksteps; ++k) {
             const uint64_t vdesc = sdesc_mn_sw128(v_addr + k * 2048, kHalf, 1024);
-            umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + k * 512, 256, 128), idesc_pv,
+            umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + k * 32 * kG, 16 * kG, 128), idesc_pv,
                         (ti > 0 || k > 0) ? 1u : 0u);
-            umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + kPHalf + k * 512, 256, 128), idesc_pv, 1u);
+            umma_f16_ss(tmem + kColO, vdesc, sdesc_interleave(p_addr + kPHalf + k * 32 * kG, 16 * kG, 128),
+                        idesc_pv, 1u);
           }
           umma_commit(empty + stage);
           umma_commit(o_full);                         // after every PV: P buffer free, O stable
@@ -678,6 +707,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
     // holds only the dirty tile's TMA until `appended`).  Lane = 4 dims, 8-byte
     // loads: the <= 48 rows of a window pair are one round of loads.
     const int d0 = lane * 4;
+    const bool dact = d0 < kD;                       // D = 64: lanes 0..15 carry the dims
     int it = 0;
     for (int sg = cid; sg < nseg; sg += ncl, ++it) {
       Info I;
@@ -687,7 +717,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       const __nv_bfloat16* kg = ds.k + (int64_t)I.g * ds.cap * kD;
       const int64_t knew_idx = ((int64_t)I.s * p.hkv + I.g) * kD + d0;
       const int64_t jlo = I.dlo > I.r0 ? I.dlo : I.r0;
-      const bool dirty = jlo < I.r1;
+      const bool dirty = jlo < I.r1 && dact;
       // the raw bf16 quads stay packed until summed (96 registers, not 192)
       uint2 raw[kP + kS];
       if (dirty) {
@@ -702,7 +732,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         pdl_wait();
         pdl_launch_dependents();
       }
-      const uint2 kraw = *reinterpret_cast<const uint2*>(p.k_new + knew_idx);
+      const uint2 kraw = dact ? *reinterpret_cast<const uint2*>(p.k_new + knew_idx) : make_uint2(0u, 0u);
       float knew[4];
       {
         const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&kraw.x);
@@ -747,7 +777,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         emit(jlo, 0);
         if (jlo + 1 < I.r1) emit(jlo + 1, kS);
       }
-      if ((int)rank == P - 1) {                       // the new K/V row (read by the forced tiles after x1)
+      if ((int)rank == P - 1 && dact) {               // the new K/V row (read by the forced tiles after x1)
         const int64_t dst = ((int64_t)I.g * ds.cap + I.pos) * kD + d0;
         *reinterpret_cast<uint2*>(ds.k + dst) = kraw;
         *reinterpret_cast<uint2*>(ds.v + dst) = *reinterpret_cast<const uint2*>(p.v_new + knew_idx);
@@ -755,7 +785,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       fence_proxy_async_global();
       mbar_arrive(appended);
       if (lane == 0 && it == 0) trace(p.trace, 13);
-      if ((int)rank == P - 1) {
+      if ((int)rank == P - 1 && dact) {
         // every dirty coarse window (two when coarse_stride < kernel_size): not
         // read by this step's stages
         const int cs = p.coarse_stride;
@@ -802,7 +832,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           sfpar ^= 1u << t;
           tc_fence_after();
           float v[kG];
-          tmem_ld16(tmem + lane_base + t * kG, v);
+          tmem_ld_n<kG>(tmem + lane_base + t * kG, v);
           tmem_wait_ld();
           if (t == 0 && tid == 0) trace(tr, 12);
           const int64_t j = I.r0 + 128 * t + row;
@@ -819,9 +849,9 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
             }
           }
         }
-        warp_reduce16_lse(m, sm, lane);
-        if ((lane & 1) == 0) {
-          const int h = reduce_head(lane);
+        warp_reduce_lse_n<kG>(m, sm, lane);
+        if (reduce_writer_n<kG>(lane)) {
+          const int h = reduce_head_n<kG>(lane);
           red_m[h * 4 + quad] = m[0];
           red_s[h * 4 + quad] = sm[0];
         }
@@ -847,9 +877,9 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       CYC(0);
       // ---- C. LSE (all pieces' partials over DSMEM), group scores, block scores, local top-k
       {
-        const int h = tid >> 3, r = tid & 7;           // 16 heads x 8 pieces
+        const int h = tid >> 3, r = tid & 7;           // G heads x 8 pieces (threads >= 8G idle)
         float M = -INFINITY, S = 0.f;
-        if (r < P) {
+        if (r < P && h < kG) {
           const float2 ms = ld_dsmem2(xpart + 2 * h, r);
           M = ms.x;
           S = ms.y;
@@ -862,7 +892,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           S = (M == -INFINITY ? 0.f : S * ex2(M - nm)) + (om == -INFINITY ? 0.f : os * ex2(om - nm));
           M = nm;
         }
-        if (r == 0) lse2[h] = M == -INFINITY ? INFINITY : M + log2f(S);
+        if (r == 0 && h < kG) lse2[h] = M == -INFINITY ? INFINITY : M + log2f(S);
       }
       named_bar_sync(1, 128);
       CYC(1);
@@ -874,8 +904,8 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         // two TMEM tiles per wait: the load latency is paid once per pair
         for (int t = 0; t < I.ntiles; t += 2) {
           float v[kG], w[kG];
-          tmem_ld16(tmem + lane_base + t * kG, v);
-          if (t + 1 < I.ntiles) tmem_ld16(tmem + lane_base + (t + 1) * kG, w);
+          tmem_ld_n<kG>(tmem + lane_base + t * kG, v);
+          if (t + 1 < I.ntiles) tmem_ld_n<kG>(tmem + lane_base + (t + 1) * kG, w);
           tmem_wait_ld();
           const int64_t jl = 128 * t + row;
           if (I.r0 + jl < I.r1) {
@@ -952,7 +982,7 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
         mbar_wait(s2_full, tp);
         tc_fence_after();
         float z[kG];
-        tmem_ld16(tmem + lane_base + kColS2, z);
+        tmem_ld_n<kG>(tmem + lane_base + kColS2, z);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -964,8 +994,8 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           float zz[kG];
 #pragma unroll
           for (int h = 0; h < kG; ++h) zz[h] = z[h];
-          const float v = warp_reduce16(zz, lane, [](float a, float b) { return fmaxf(a, b); });
-          if ((lane & 1) == 0) red_m[quad * kG + reduce_head(lane)] = v;
+          const float v = warp_reduce_n<kG>(zz, lane, [](float a, float b) { return fmaxf(a, b); });
+          if (reduce_writer_n<kG>(lane)) red_m[quad * kG + reduce_head_n<kG>(lane)] = v;
         }
         named_bar_sync(1, 128);
         float mnew[kG];
@@ -993,11 +1023,11 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           }
           if (any) {
             float o[kG];
-            tmem_ld16(tmem + lane_base + kColO, o);
+            tmem_ld_n<kG>(tmem + lane_base + kColO, o);
             tmem_wait_ld();
 #pragma unroll
             for (int h = 0; h < kG; ++h) o[h] *= corr[h];
-            tmem_st16(tmem + lane_base + kColO, o);
+            tmem_st_n<kG>(tmem + lane_base + kColO, o);
             tmem_wait_st();
             tc_fence_before();
           }
@@ -1015,11 +1045,15 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           plo[h / 2] = *reinterpret_cast<const uint32_t*>(&lo2);
         }
         uint8_t* pb = smem + Smem::p;
-        const uint32_t base = (row >> 3) * 256 + (row & 7) * 16;
-        *reinterpret_cast<uint4*>(pb + base) = make_uint4(phi[0], phi[1], phi[2], phi[3]);
-        *reinterpret_cast<uint4*>(pb + base + 128) = make_uint4(phi[4], phi[5], phi[6], phi[7]);
-        *reinterpret_cast<uint4*>(pb + kPHalf + base) = make_uint4(plo[0], plo[1], plo[2], plo[3]);
-        *reinterpret_cast<uint4*>(pb + kPHalf + base + 128) = make_uint4(plo[4], plo[5], plo[6], plo[7]);
+        // P^T [128 rows][G heads]: 8-row x 8-head core matrices, heads 8..15 at +128
+        const uint32_t base = (row >> 3) * (16 * kG) + (row & 7) * 16;
+#pragma unroll
+        for (int c = 0; c < kG / 8; ++c) {
+          *reinterpret_cast<uint4*>(pb + base + 128 * c) =
+              make_uint4(phi[4 * c], phi[4 * c + 1], phi[4 * c + 2], phi[4 * c + 3]);
+          *reinterpret_cast<uint4*>(pb + kPHalf + base + 128 * c) =
+              make_uint4(plo[4 * c], plo[4 * c + 1], plo[4 * c + 2], plo[4 * c + 3]);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
@@ -1127,13 +1161,15 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
           mbar_wait(o_full, tp_prev);
           tc_fence_after();
           float o[kG];
-          tmem_ld16(tmem + lane_base + kColO, o);
+          tmem_ld_n<kG>(tmem + lane_base + kColO, o);
           tmem_wait_ld();
           tc_fence_before();
+          if (row < kD) {
 #pragma unroll
-          for (int h = 0; h < kG; ++h) pt[h * kD + row] = o[h];   // O^T lane == d
-          const float v = warp_reduce16(lrow, lane, [](float a, float b) { return a + b; });
-          if ((lane & 1) == 0) red_s[quad * kG + reduce_head(lane)] = v;
+            for (int h = 0; h < kG; ++h) pt[h * kD + row] = o[h];   // O^T lane == d
+          }
+          const float v = warp_reduce_n<kG>(lrow, lane, [](float a, float b) { return a + b; });
+          if (reduce_writer_n<kG>(lane)) red_s[quad * kG + reduce_head_n<kG>(lane)] = v;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(o_empty);               // once per segment, with or without tiles
@@ -1150,10 +1186,12 @@ decode_cluster_kernel(const __grid_constant__ CUtensorMap tm_q, const Params p) 
       if (tid == 0) trace(tr, 14);
       CYC(15);
       {
-        // ---- combine: piece r merges heads r, r + P, ... of the P partials (DSMEM)
-        const int hh = tid >> 6, dp = tid & 63;
-        for (int j2 = 0; (int)rank + P * 2 * j2 < kG; ++j2) {
-          const int h = (int)rank + P * (2 * j2 + hh);
+        // ---- combine: piece r merges heads r, r + P, ... of the P partials (DSMEM);
+        // a head is D/2 threads (float2 each), 256/D heads per pass
+        constexpr int kHPass = 256 / kD;
+        const int hh = tid / (kD / 2), dp = tid % (kD / 2);
+        for (int j2 = 0; (int)rank + P * kHPass * j2 < kG; ++j2) {
+          const int h = (int)rank + P * (kHPass * j2 + hh);
           const bool act = h < kG;
           const int hs = act ? h : (int)rank;
           float mq[kMaxCl], lq[kMaxCl];
@@ -1218,6 +1256,7 @@ size_t decode_fused_workspace_bytes(int n_seq, int hkv) {
   return 0;
 }
 
+template <int G, int D>
 static int max_active_clusters(int np) {
   constexpr int kMaxDev = 64;
   static int cached[kMaxDev][kMaxCl + 1];
@@ -1229,8 +1268,8 @@ static int max_active_clusters(int np) {
   }
   const int dev = current_device() % kMaxDev;   // occupancy is per device
   if (cached[dev][np] >= 0) return cached[dev][np];
-  const size_t smem = Smem::total + 1024;
-  if (smem_attr_once((const void*)decode_cluster_kernel, (int)smem) != cudaSuccess) return cached[dev][np] = 0;
+  const size_t smem = FCfg<G, D>::Smem::total + 1024;
+  if (smem_attr_once((const void*)decode_cluster_kernel<G, D>, (int)smem) != cudaSuccess) return cached[dev][np] = 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1243,7 +1282,7 @@ static int max_active_clusters(int np) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel, &cfg) != cudaSuccess) n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel<G, D>, &cfg) != cudaSuccess) n = 0;
   return cached[dev][np] = n;
 }
 
@@ -1252,17 +1291,18 @@ static int max_active_clusters(int np) {
 // B200 (1 CTA/SM) 8-CTA clusters reach 15 co-resident clusters, 6-CTA ones 22.
 // `share` launches of this kernel run concurrently (decode micro-batches on
 // separate streams): each may use 1/share of the co-resident clusters.
+template <int G, int D>
 static int choose_cluster(int nseg, int64_t max_len_after, int share) {
   const int64_t nb_max = max_len_after / kM + 1;
   static const int forced = getenv("INFLLM2_DECODE_P") ? atoi(getenv("INFLLM2_DECODE_P")) : 0;   // diagnostic
   if (forced >= 3 && forced <= kMaxCl && (nb_max + forced - 1) / forced + 1 <= kMaxPieceBlocks &&
-      max_active_clusters(forced) / share > 0)
+      max_active_clusters<G, D>(forced) / share > 0)
     return forced;
   int best = 0;
   double best_score = -1.0;
   for (int np = kMaxCl; np >= 3; --np) {
     if ((nb_max + np - 1) / np + 1 > kMaxPieceBlocks) continue;
-    const int n = max_active_clusters(np) / share;
+    const int n = max_active_clusters<G, D>(np) / share;
     if (n <= 0) continue;
     const int rounds = (nseg + n - 1) / n;
     const double score = (double)np / rounds;
@@ -1274,18 +1314,58 @@ static int choose_cluster(int nseg, int64_t max_len_after, int share) {
   return best;
 }
 
+static int choose_cluster_geom(int hq, int hkv, int d, int nseg, int64_t max_len_after, int share) {
+  if (hq == 16 * hkv && d == 128) return choose_cluster<16, 128>(nseg, max_len_after, share);
+  if (hq == 8 * hkv && d == 64) return choose_cluster<8, 64>(nseg, max_len_after, share);
+  return 0;
+}
+
 // Host-side eligibility: pieces must fit the TMEM-resident z tiles for every
 // length up to max_len_after and budgets must fit the warp top-k.
-bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hkv, int64_t max_len_after, int share) {
+bool decode_fused_supported(const infllm2_geometry& g, int n_seq, int hq, int hkv, int d, int64_t max_len_after,
+                            int share) {
   if (getenv("INFLLM2_DECODE_LEGACY")) return false;
   if (n_seq > kMaxSeq || n_seq < 1) return false;
   if (g.top_k > kMaxBudget || g.top_k < 1) return false;
   if (infllm2_max_selected(&g) > 96) return false;
-  return choose_cluster(n_seq * hkv, max_len_after, share) > 0;
+  return choose_cluster_geom(hq, hkv, d, n_seq * hkv, max_len_after, share) > 0;
+}
+
+template <int G, int D>
+static int fused_launch(const Params& p, const void* q, int n_seq, int hq, int hkv, int64_t max_len_after, int share,
+                        cudaStream_t stream) {
+  CUtensorMap tq;
+  const uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)n_seq};
+  const uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)hq * D * 2};
+  const uint32_t box[3] = {64, (uint32_t)G, 1};
+  if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
+  const int nseg = n_seq * hkv;
+  const int np = choose_cluster<G, D>(nseg, max_len_after, share);
+  if (np <= 0) return INFLLM2_ERR_UNSUPPORTED;
+  int ncl = max_active_clusters<G, D>(np) / share;
+  if (ncl > nseg) ncl = nseg;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = np;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = getenv("INFLLM2_DECODE_NOPDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * np));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = FCfg<G, D>::Smem::total + 1024;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  count_launch();
+  if (cudaLaunchKernelEx(&cfg, decode_cluster_kernel<G, D>, tq, p) != cudaSuccess) return INFLLM2_ERR_CUDA;
+  return INFLLM2_OK;
 }
 
 int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t max_len_after, int hq, int hkv,
-                      const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
+                      int d, const void* q, const void* k_new, const void* v_new, int32_t* selection, void* out,
                       int out_f32, float* lse, void* ws, cudaStream_t stream, int share, int early) {
   (void)ws;
   Params p;
@@ -1307,7 +1387,7 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t
   p.out = out;
   p.out_f32 = out_f32;
   p.lse = lse;
-  p.zscale = 1.4426950408889634f / sqrtf((float)kD);
+  p.zscale = 1.4426950408889634f / sqrtf((float)d);
   // L2 prefetch of the linked next layer's means: measured neutral to slightly
   // slower (the means stream already runs at ~6.2 TB/s; DESIGN §4 K4), so opt-in
   static const bool pf = getenv("INFLLM2_DECODE_PREFETCH") != nullptr;
@@ -1315,34 +1395,9 @@ int decode_fused_step(const infllm2_geometry& g, void* table, int n_seq, int64_t
   static const bool tr = getenv("INFLLM2_DECODE_TRACE") != nullptr;
   static int launches = 0;
   p.trace = tr ? 1 + (launches++ % kTraceRing) : 0;
-  CUtensorMap tq;
-  const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)n_seq};
-  const uint64_t strides[2] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2};
-  const uint32_t box[3] = {64, (uint32_t)kG, 1};
-  if (!encode_tmap_3d_bf16(&tq, q, dims, strides, box)) return INFLLM2_ERR_SHAPE;
-  const int nseg = n_seq * hkv;
-  const int np = choose_cluster(nseg, max_len_after, share);
-  if (np <= 0) return INFLLM2_ERR_UNSUPPORTED;
-  int ncl = max_active_clusters(np) / share;
-  if (ncl > nseg) ncl = nseg;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = np;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  static const bool pdl = getenv("INFLLM2_DECODE_NOPDL") == nullptr;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ncl * np));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Smem::total + 1024;
-  cfg.stream = stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 2 : 1;
-  count_launch();
-  if (cudaLaunchKernelEx(&cfg, decode_cluster_kernel, tq, p) != cudaSuccess) return INFLLM2_ERR_CUDA;
-  return INFLLM2_OK;
+  if (hq == 16 * hkv && d == 128) return fused_launch<16, 128>(p, q, n_seq, hq, hkv, max_len_after, share, stream);
+  if (hq == 8 * hkv && d == 64) return fused_launch<8, 64>(p, q, n_seq, hq, hkv, max_len_after, share, stream);
+  return INFLLM2_ERR_UNSUPPORTED;
 }
 
 }  // namespace infllm2

@@ -1,8 +1,9 @@
 """Batched decode for the MiniCPM4-0.5B head geometry (G = 8 heads per KV
-group, D = 64): the five-launch decode path (csrc/decode.cu: append + compress,
-tcgen05 stage-1 split-K, block scores + top-k, stage 2 on attend_tc_kernel<8, 64>
-with per-sequence K/V maps, split-K combine) instead of stepping every sequence
-through the prefill kernels.
+group, D = 64): the one-launch cluster kernel decode_cluster_kernel<8, 64>
+(csrc/decode_fused.cu) and the five-launch path (csrc/decode.cu, forced with
+INFLLM2_DECODE_LEGACY=1: append + compress, tcgen05 stage-1 split-K, block
+scores + top-k, stage 2 on attend_tc_kernel<8, 64>, split-K combine) — instead
+of stepping every sequence through the prefill kernels.
 
 Checks, per step (the reference's decode = append then attend n = 1,
 /root/reference/pkg/src/deskinfer/model.py:434-444):
@@ -63,9 +64,18 @@ def _verify(batch, cfg, q, sel, out, lse):
         assert (lse[i] - l2[0]).abs().max().item() <= LSE_TC
 
 
+@pytest.fixture(params=["fused", "legacy"])
+def path(request, monkeypatch):
+    if request.param == "legacy":
+        monkeypatch.setenv("INFLLM2_DECODE_LEGACY", "1")
+    else:
+        monkeypatch.delenv("INFLLM2_DECODE_LEGACY", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("lengths,topk", [([3000, 5000, 777, 8190], 16), ([127, 1000, 4093], 8),
-                                          ([64, 2111], 64), ([20000, 12000], 32)])
-def test_decode_05b_eager_vs_verifier(lengths, topk):
+                                          ([64, 2111], 64), ([20000, 12000], 32), ([131072 - 3, 70000], 16)])
+def test_decode_05b_eager_vs_verifier(lengths, topk, path):
     cfg = P.SparseAttentionConfig(top_k=topk)
     steps = 4
     layers, gen = _caches(lengths, cfg, 61 + topk, steps + 4)
@@ -80,7 +90,9 @@ def test_decode_05b_eager_vs_verifier(lengths, topk):
         n0 = lib.infllm2_launch_count()
         out, sel, lse = batch.step(q, kn, vn, return_selection=True, return_lse=True, out_dtype=torch.float32)
         torch.cuda.synchronize()
-        assert lib.infllm2_launch_count() - n0 <= 5, "0.5B decode fell back to the per-sequence path"
+        n_launch = lib.infllm2_launch_count() - n0
+        # the cluster kernel's budgets stop at top_k 32: top_k 64 takes the five-launch path
+        assert n_launch == 1 if (path == "fused" and topk <= 32) else 1 < n_launch <= 5, (path, n_launch)
         assert [l.length for l in layers] == [L + st + 1 for L in lengths]
         assert _device_lengths(batch) == [l.length for l in layers]
         _verify(batch, cfg, q, sel, out, lse)
@@ -100,7 +112,7 @@ def test_decode_05b_eager_vs_verifier(lengths, topk):
         assert (err <= OUT_ABS + OUT_REL * np.abs(ref.out[0])).all(), err.max()
 
 
-def test_decode_05b_graph_replay_equals_eager():
+def test_decode_05b_graph_replay_equals_eager(path):
     cfg = P.SparseAttentionConfig(top_k=16)
     lengths, steps = [9000, 20000, 4097], 5
     extra = steps + 8
@@ -145,7 +157,7 @@ def test_decode_05b_graph_replay_equals_eager():
 
 
 @pytest.mark.parametrize("top_k", [2, 3])
-def test_decode_05b_consume_budget_zero(top_k):
+def test_decode_05b_consume_budget_zero(top_k, path):
     cfg = P.SparseAttentionConfig(top_k=top_k, forced_consume_budget=True)
     layers, gen = _caches([5000, 777, 130], cfg, 9, 8)
     batch = P.DecodeBatch(layers, cfg)

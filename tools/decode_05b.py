@@ -1,6 +1,6 @@
 """Batched decode timing for the MiniCPM4-0.5B head geometry (16 q heads, 2 KV
-heads, D = 64): the five-launch batched path (eager and CUDA-graph replay) vs
-stepping every sequence through the prefill kernels (the path it replaced).
+heads, D = 64): the cluster kernel and the five-launch path (eager and
+CUDA-graph replay) vs stepping every sequence through the prefill kernels.
 
     python tools/decode_05b.py [--seqs 8] [--len 131072] [--steps 20]
 """
@@ -28,7 +28,7 @@ def main():
     torch.cuda.set_device(0)
     cfg = P.SparseAttentionConfig(top_k=a.topk)
     S, L, n = a.seqs, a.len, a.steps
-    extra = 4 * n + 16
+    extra = 8 * n + 32
     gen = torch.Generator(device="cuda").manual_seed(3)
     layers = []
     for _ in range(S):
@@ -55,25 +55,32 @@ def main():
         return e0.elapsed_time(e1) / reps * 1e3          # us per step
 
     res = {"seqs": S, "len": L, "top_k": a.topk}
-    res["batched_eager_us"] = timed(lambda: batch.step(q, kn, kn, max_len=bound), n)
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(side):
-        with torch.cuda.graph(graph, stream=side):
-            batch.step(q, kn, kn, max_len=bound, bookkeep=False)
-    torch.cuda.synchronize()
 
-    def replay():
-        graph.replay()
-        batch.advance(1)
+    def measure(tag):
+        res[f"{tag}_eager_us"] = timed(lambda: batch.step(q, kn, kn, max_len=bound), n)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                batch.step(q, kn, kn, max_len=bound, bookkeep=False)
+        torch.cuda.synchronize()
 
-    res["batched_graph_us"] = timed(replay, n)
+        def replay():
+            graph.replay()
+            batch.advance(1)
+
+        res[f"{tag}_graph_us"] = timed(replay, n)
+
+    measure("fused")
+    os.environ["INFLLM2_DECODE_LEGACY"] = "1"
+    measure("five_launch")
+    del os.environ["INFLLM2_DECODE_LEGACY"]
     res["per_sequence_us"] = timed(lambda: batch._step_per_sequence(q, kn, kn, False, False, None, True), n)
     nk = L // 16
     per_seq = HKV * nk * D * 4 + HKV * (a.topk + 3) * 64 * D * 2 * 2
     res["algorithmic_bytes_per_step"] = per_seq * S
-    res["graph_hbm_GBps"] = per_seq * S / (res["batched_graph_us"] * 1e-6) / 1e9
+    res["fused_graph_hbm_GBps"] = per_seq * S / (res["fused_graph_us"] * 1e-6) / 1e9
     print(json.dumps(res))
 
 
