@@ -603,25 +603,63 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
     # e2e: per step H2D of every layer's q/k/v from pinned host memory into the
     # captured step's input buffers, one replay of the captured 32-layer step
     # (DecodeBatch's documented graph workflow), D2H of every sequence's
-    # last-layer output
+    # last-layer output.  Two captured copies of the step with their own input
+    # and output buffers alternate, so step i+1's H2D (copy stream) overlaps
+    # step i's replay; a buffer set is rewritten only after the replay that read
+    # it and the D2H of the outputs it produced.
+    outs_a = [row[:] for row in outs]
+    q2, kn2, vn2 = torch.empty_like(q), torch.empty_like(kn), torch.empty_like(vn)
+    graph_b = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph_b, stream=side):
+            step(q2, kn2, vn2, bookkeep=False)
+    torch.cuda.synchronize(dev)
+    outs_b = [row[:] for row in outs]
+    sets = [(q, kn, vn, graph, outs_a), (q2, kn2, vn2, graph_b, outs_b)]
     hq_ = q.cpu().pin_memory()
     hk_ = kn.cpu().pin_memory()
     hv_ = vn.cpu().pin_memory()
-    out_host = torch.empty((S, HQ, D), dtype=torch.bfloat16).pin_memory()
+    out_host = [torch.empty((S, HQ, D), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    copy = torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    comp_done = [torch.cuda.Event() for _ in range(2)]
+    d2h_done = [torch.cuda.Event() for _ in range(2)]
+
+    def h2d(k):
+        qq, kk, vv = sets[k][:3]
+        with torch.cuda.stream(copy):
+            qq.copy_(hq_, non_blocking=True)
+            kk.copy_(hk_, non_blocking=True)
+            vv.copy_(hv_, non_blocking=True)
+            h2d_done[k].record(copy)
+
     te0 = torch.cuda.Event(enable_timing=True)
     te1 = torch.cuda.Event(enable_timing=True)
     barrier()
-    te0.record()
-    for _ in range(args.steps):
-        q.copy_(hq_, non_blocking=True)
-        kn.copy_(hk_, non_blocking=True)
-        vn.copy_(hv_, non_blocking=True)
-        graph.replay()
-        for m, (lo, hi) in enumerate(bounds):      # the last layer's output of every sequence
-            out_host[lo:hi].copy_(outs[m][layers - 1], non_blocking=True)
+    te0.record(cur)
+    copy.wait_stream(cur)
+    h2d(0)
+    for i in range(args.steps):
+        k = i & 1
+        cur.wait_event(h2d_done[k])
+        if i >= 2:
+            cur.wait_event(d2h_done[k])          # this set's outputs of step i-2 are on the host
+        sets[k][3].replay()
+        comp_done[k].record(cur)
         for b in all_batches:
             b.advance(1)
-    te1.record()
+        if i + 1 < args.steps:
+            if i >= 1:
+                copy.wait_event(comp_done[1 - k])  # step i-1 has read the other set's inputs
+            h2d(1 - k)
+        with torch.cuda.stream(copy):
+            copy.wait_event(comp_done[k])
+            for m, (lo, hi) in enumerate(bounds):  # the last layer's output of every sequence
+                out_host[k][lo:hi].copy_(sets[k][4][m][layers - 1], non_blocking=True)
+            d2h_done[k].record(copy)
+    cur.wait_stream(copy)
+    te1.record(cur)
     barrier()
     ms_e2e = te0.elapsed_time(te1)
     if world > 1:
@@ -650,7 +688,8 @@ def run_decode(args, P, cfg, world, rank, dev, barrier, dist):
             "e2e": {"ms_per_step": round(ms_e2e / args.steps, 4),
                     "us_per_token": round(ms_e2e / args.steps * 1e3 / (S * world), 2),
                     "h2d_bytes_per_step": int((q.numel() + kn.numel() + vn.numel()) * 2),
-                    "d2h_bytes_per_step": int(out_host.numel() * 2)},
+                    "d2h_bytes_per_step": int(out_host[0].numel() * 2),
+                    "overlap": "double-buffered inputs: step i+1's H2D on a copy stream during step i's replay"},
             "gpu_launches_per_step": int(launches_per_step),
             "microbatches": mb,
             "graph": f"{layers}-layer step captured once ({launches_per_step // max(1, layers * mb)} launch(es) per "

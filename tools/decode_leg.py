@@ -16,5 +16,6 @@ dev = torch.device("cuda:0")
 torch.cuda.set_device(dev)
 cfg = P.SparseAttentionConfig(top_k=16)
 res = bench.run_decode(args, P, cfg, 1, 0, dev, lambda: torch.cuda.synchronize(dev), None)
-print(json.dumps({"us_per_token": res["us_per_token"], "ms_per_step": res["ms_per_step"],
+print(json.dumps({"us_per_token": res["us_per_token"], "e2e_us_per_token": res["e2e"]["us_per_token"],
+                  "ms_per_step": res["ms_per_step"],
                   "frac": res["roofline"]["frac"], "early_env": os.environ.get("INFLLM2_DECODE_NOEARLY")}))
