@@ -439,11 +439,12 @@ def run_ours(args):
 
 
 def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dist):
-    from paper_2506_07900_b200 import sharding as S
     """Same metric through two_stage_attention with HOST inputs: per layer the
     pinned q/k/v shards are copied H2D on a copy stream (overlapped with the
     previous layer's compute), and the last layer's output is read back."""
     import torch
+
+    from paper_2506_07900_b200 import sharding as S
 
     layers = args.layers
     nbuf = 2
@@ -457,23 +458,27 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
     my_rows = sum(hi - lo for lo, hi in chunks)
     out_host = torch.empty((my_rows, HQ, D), dtype=torch.bfloat16).pin_memory()   # every row of the last layer
     copy_stream = torch.cuda.Stream(dev)
+    d2h_stream = torch.cuda.Stream(dev)
     chunk_streams = [torch.cuda.Stream(dev) for _ in chunks]
     h2d_bytes = sum(t.numel() * t.element_size() for grp in host[0] for t in grp) * layers
+    # buffer b was last read by the layer that recorded freed[b] (possibly in the previous step)
+    freed = [None] * nbuf
 
     def step():
         ready = [torch.cuda.Event() for _ in range(layers)]
-        done = [torch.cuda.Event() for _ in range(layers)]
+
         def issue_copy(layer):
             b = layer % nbuf
             with torch.cuda.stream(copy_stream):
-                if layer >= nbuf:
-                    copy_stream.wait_event(done[layer - nbuf])
+                if freed[b] is not None:
+                    copy_stream.wait_event(freed[b])
                 for grp_h, grp_d in zip(host[b], dbuf[b]):
                     for th, td in zip(grp_h, grp_d):
                         td.copy_(th, non_blocking=True)
                 ready[layer].record(copy_stream)
+
         issue_copy(0)
-        outs = []
+        r0 = 0
         for layer in range(layers):
             if layer + 1 < layers:
                 issue_copy(layer + 1)
@@ -486,26 +491,34 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
                 with torch.cuda.stream(chunk_streams[h]):
                     o = P.two_stage_attention(qd[h], cache, cfg, lo)
                 if layer == layers - 1:
-                    o.record_stream(stream)          # read back on the main stream
-                    outs.append(o)
+                    # D2H of this chunk's last-layer rows on its own stream: the
+                    # next step's first layer does not wait for it
+                    d2h_stream.wait_stream(chunk_streams[h])
+                    with torch.cuda.stream(d2h_stream):
+                        out_host[r0:r0 + o.shape[0]].copy_(o, non_blocking=True)
+                    o.record_stream(d2h_stream)
+                    r0 += o.shape[0]
             for st in chunk_streams:
                 stream.wait_stream(st)
-            done[layer].record(stream)
-        r0 = 0
-        for o in outs:                  # D2H of this rank's full last-layer output
-            out_host[r0:r0 + o.shape[0]].copy_(o, non_blocking=True)
-            r0 += o.shape[0]
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            freed[layer % nbuf] = ev
         return out_host.numel() * out_host.element_size()
 
     for _ in range(max(1, args.warmup)):
         step()
+    stream.wait_stream(d2h_stream)
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
+    copy_stream.wait_stream(stream)
+    d2h_stream.wait_stream(stream)
     d2h = 0
     for _ in range(args.steps):
         d2h = step()
+    stream.wait_stream(d2h_stream)
+    stream.wait_stream(copy_stream)
     t1.record(stream)
     barrier()
     ms = t0.elapsed_time(t1)
@@ -515,7 +528,8 @@ def run_e2e(args, P, cfg, caches, chunks, world, rank, dev, stream, barrier, dis
         ms = float(t.item())
     return {"value": round(args.seq / (ms / args.steps / 1e3), 1), "unit": "tok/s",
             "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
-            "note": "pinned host q/k/v per layer, H2D overlapped with compute on a copy stream"}
+            "note": "pinned host q/k/v per layer, H2D overlapped with compute on a copy stream; the last "
+                    "layer's output read back per chunk on a D2H stream"}
 
 
 # ----------------------------------------------------------------------------- decode (configs[3])
