@@ -1,6 +1,7 @@
 """BASELINE configs[2] parity at the headline size: one 131 072-token layer of
 the 8B-shaped stack (32 q / 2 KV heads, d 128, m 64, p 32, s 16, init 1,
-local 2), all rows prefilled through ``two_stage_attention`` on the B200 (the
+local 2) — and, for configs[4]'s MiniCPM4-0.5B shape, 16 q / 2 KV heads, d 64 —
+all rows prefilled through ``two_stage_attention`` on the B200 (the
 exact product call bench.py times), checked against the CPU oracle (the
 reference's algorithm, /root/reference/pkg/src/deskinfer/sparse.py:387-468,
 float64 dots) on >= 1024 sampled rows: seeded rows, the first/last rows,
@@ -53,19 +54,21 @@ def sample_positions(seed: int, count: int = 1024) -> np.ndarray:
     return np.asarray(sorted(picks), dtype=np.int64)
 
 
-@pytest.mark.parametrize("top_k", [16, 64])
-def test_config2_128k_layer_vs_oracle(top_k):
+@pytest.mark.parametrize("top_k,shape,rows", [(16, (32, 2, 128), 1024), (64, (32, 2, 128), 1024),
+                                              (16, (16, 2, 64), 512)], ids=["8B-k16", "8B-k64", "0.5B-k16"])
+def test_config2_128k_layer_vs_oracle(top_k, shape, rows):
     torch.cuda.set_device(0)
+    hq, hkv, d = shape
     cfg = P.SparseAttentionConfig(top_k=top_k)
-    g = torch.Generator(device="cuda").manual_seed(1_000_003 + top_k)
-    k = torch.randn((L, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
-    v = torch.randn((L, 2, 128), generator=g, device="cuda").to(torch.bfloat16)
-    q = torch.randn((L, 32, 128), generator=g, device="cuda").to(torch.bfloat16)
-    layer = P.BlockizedLayerCache(2, 128, cfg, capacity=L)
+    g = torch.Generator(device="cuda").manual_seed(1_000_003 + top_k + (0 if d == 128 else d))
+    k = torch.randn((L, hkv, d), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((L, hkv, d), generator=g, device="cuda").to(torch.bfloat16)
+    q = torch.randn((L, hq, d), generator=g, device="cuda").to(torch.bfloat16)
+    layer = P.BlockizedLayerCache(hkv, d, cfg, capacity=L)
     layer.append(k, v)
     out, sel, lse = P.two_stage_attention(q, layer, cfg, 0, return_selection=True, return_lse=True,
                                           out_dtype=torch.float32)
-    pos = sample_positions(top_k)
+    pos = sample_positions(top_k + (0 if d == 128 else d), rows)
     idx = torch.as_tensor(pos, device="cuda")
     got_sel = sel[idx].cpu().numpy()
     got_out = out[idx].cpu().numpy()
@@ -87,7 +90,7 @@ def test_config2_128k_layer_vs_oracle(top_k):
                           f"{[(int(pos[i]), int(gg)) for i, gg in bad[:4]]}"
     err = np.abs(got_out - ref_out)
     lerr = np.abs(got_lse - ref_lse)
-    record(f"config2_k{top_k}", rows=pos.size, out_max_abs=err.max(),
+    record(f"config2_k{top_k}_d{d}", rows=pos.size, out_max_abs=err.max(),
            out_max_rel=(err / (np.abs(ref_out) + 1e-3)).max(), lse_max_abs=lerr.max())
     assert (err <= OUT_ABS + OUT_REL * np.abs(ref_out)).all(), err.max()
     assert lerr.max() <= LSE_TC, lerr.max()
