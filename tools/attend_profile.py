@@ -14,7 +14,9 @@ sys.path.insert(0, ".")
 from sweep import time_layer  # noqa: E402
 from paper_2506_07900_b200 import _lib  # noqa: E402
 
-print("select, attend ms:", time_layer(32, 2, 128, int(os.environ.get("AB_LEN", "131072")), 16, reps=1))
+shape = (16, 2, 64) if os.environ.get("AB_SHAPE") == "0.5B" else (32, 2, 128)
+print("shape", shape, "select, attend ms:", time_layer(*shape, int(os.environ.get("AB_LEN", "131072")),
+                                                      int(os.environ.get("AB_TOPK", "16")), reps=1))
 torch.cuda.synchronize()
 buf = (ctypes.c_longlong * (160 * 24))()
 _lib.load().infllm2_debug_attend_cycles(buf, 160 * 24)
