@@ -6,6 +6,9 @@
 //        2: no ex2 (FFMA only), 3: no max tree, 4: pass 2 (group sums + block max)
 #include <cstdio>
 #include <cstdlib>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
 #include "../paper_2506_07900_b200/csrc/sm100.cuh"
 using namespace infllm2::sm100;
 

@@ -5,6 +5,9 @@
 // accumulators, MMA k writes accumulator k % nacc, 16 MMAs per commit)
 #include <cstdio>
 #include <cstdlib>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
 #include "../paper_2506_07900_b200/csrc/sm100.cuh"
 
 using namespace infllm2::sm100;

@@ -9,6 +9,9 @@
 // Usage: pipe_bench <mode>
 #include <cstdio>
 #include <cstdlib>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
 #include "../paper_2506_07900_b200/csrc/sm100.cuh"
 using namespace infllm2::sm100;
 
