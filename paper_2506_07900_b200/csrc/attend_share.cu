@@ -281,20 +281,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int hh = 0; hh < kDH; ++hh)
           tma_load_3d_hint(qd + hh * kQHalf, &tm_q, q_full + qbuf, 64 * hh, grp * kG, (int)i0, pol_stream);
       }
-      int total = 2;
-#pragma unroll
-      for (int u = 0; u < kU; ++u) total += ur.tiles(u);
-      for (int c = 0; c < total; ++c) {
-        int b0, b1 = -1, nt;
-        if (c == 0) { b0 = 0; b1 = (int)qb - 1; nt = 2; }
-        else if (c == 1) { b0 = (int)qb; nt = 1; }
-        else {
-          int u, k;
-          row_tile<kU>(ur, c - 2, &u, &k);
-          b0 = ur.chosen(u, 2 * k);
-          nt = 2 * k + 1 < ur.nchosen(u) ? 2 : 1;
-          if (nt == 2) b1 = ur.chosen(u, 2 * k + 1);
-        }
+      auto issue = [&](int b0, int b1, int nt) {
         if (lane == 0) {
           mbar_wait(ring_empty + stage, phase ^ 1);
           mbar_arrive_expect_tx(ring_full + stage, nt * kDH * (kM * 128));
@@ -309,6 +296,20 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         __syncwarp();
         if (++stage == nst) { stage = 0; phase ^= 1; }
+      };
+      issue(0, (int)qb - 1, 2);           // shared tile A
+      issue((int)qb, -1, 1);               // shared tile B
+      // the rows' chosen tiles; u unrolled so the unit's registers are
+      // addressed directly (no per-tile row search or select chains)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int nch = ur.nch[u];
+        for (int k = 0; 2 * k < nch; ++k) {
+          const int nt = 2 * k + 1 < nch ? 2 : 1;
+          const int b0 = ur.chosen(u, 2 * k);
+          const int b1 = ur.chosen(u, 2 * k + 1);       // shuffled by every lane; unused when nt == 1
+          issue(b0, b1, nt);
+        }
       }
     }
   } else if (warp == 1) {
@@ -345,12 +346,9 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (++stage == kKSt) { stage = 0; phase ^= 1; }
       }
       // row tiles: S^T = K . Q_u^T (N = 16) through the slot ring
-      int total = 0;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) total += ur.tiles(u);
-      for (int c = 0; c < total; ++c, ++tcount) {
-        int u, k;
-        row_tile<kU>(ur, c, &u, &k);
+      for (int u = 0; u < kU; ++u)
+      for (int k = 0; k < ur.tiles(u); ++k, ++tcount) {
         const int slot = tcount % kSlots;
         mbar_wait(k_full + stage, phase);
         mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1);
@@ -422,12 +420,13 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       int c = 0;
       for (int u = 0; u < kU; ++u) {
         const int tiles = ur.tiles(u);
+        const int nch = ur.nchosen(u);
         for (int k = 0; k < tiles; ++k, ++c, ++pcount) {
           const int pbuf = pcount & 1;
           mbar_wait(v_full + stage, vphase);
           mbar_wait(p_full + pbuf, (pcount >> 1) & 1);
           tc_fence_after();
-          const int ksteps = 2 * k + 1 < ur.nchosen(u) ? 8 : 4;
+          const int ksteps = 2 * k + 1 < nch ? 8 : 4;
           if (elect_one()) {
             const uint64_t dv = sdesc_mn_sw128(smem_u32(smem + Smem::kv + (kKSt + stage) * kTile), kHalf, 1024);
             const uint64_t dp = sdesc_interleave(smem_u32(smem + Smem::prow + pbuf * kPRow), 16 * kG, 128);
@@ -575,6 +574,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
         for (int h = 0; h < kSH; ++h) { mst[h] = su[h0 + h]; mrun[h] = mst[h]; lsum[h] = 0.f; lsx[h] = 0.f; }
         const int tiles = ur.tiles(u);
+        const int nch = ur.nchosen(u);
         const int ob = it & 1;
         const uint32_t oa = tmem + lane_base + kColO + 128 * ob + u * kG + h0;
         for (int k = 0; k < tiles; ++k) {
@@ -588,7 +588,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_empty + sslot);
-          const bool valid = 2 * k + (row >> 6) < ur.nchosen(u);   // chosen blocks lie below qb - 1
+          const bool valid = 2 * k + (row >> 6) < nch;   // chosen blocks lie below qb - 1
 #pragma unroll
           for (int h = 0; h < kSH; h += 2) upk2(ffma2(pk2(z[h], z[h + 1]), c2x2, 0ull), z[h], z[h + 1]);
 #pragma unroll
