@@ -56,6 +56,32 @@ constexpr int kSoftWarps = 8;
 constexpr int kPvWarp = 2 + kSoftWarps;       // 10
 constexpr int kVWarp = kPvWarp + 5;           // 15
 constexpr int kThreads = 32 * (kVWarp + 1);   // 512
+#ifdef SHARE_PROF
+// per-role wait cycles (variant builds: tools/build_variant.sh ... -DSHARE_PROF; tools/share_prof.py):
+// [0] K producer total, [1] its ring waits, [2] V producer total, [3] its ring waits, [4] QK total,
+// [5] QK k_full, [6] QK s_empty, [7] PV total, [8] PV v_full, [9] PV p_full, [10] PV o_empty,
+// [11] softmax (warp 2) total, [12] s_full, [13] p_empty, [14] epilogue (warp 11) total, [15] o_full
+__device__ long long g_sp[160][16];
+#define SP_INIT()                                  \
+  long long sp_acc[16];                            \
+  for (int i_ = 0; i_ < 16; ++i_) sp_acc[i_] = 0;  \
+  const long long sp_t0 = clock64()
+#define SP_W(slot, call) do { const long long t_ = clock64(); call; sp_acc[slot] += clock64() - t_; } while (0)
+#define SP_FLUSH()                                                                                       \
+  do {                                                                                                   \
+    const int tot_ = warp == 0 ? 0 : warp == kVWarp ? 2 : warp == 1 ? 4 : warp == kPvWarp ? 7 :          \
+                     warp == 2 ? 11 : warp == 11 ? 14 : -1;                                              \
+    if (tot_ >= 0) sp_acc[tot_] = clock64() - sp_t0;                                                     \
+    if (lane == 0 && blockIdx.x < 160 && tot_ >= 0)                                                      \
+      for (int i_ = 0; i_ < 16; ++i_)                                                                    \
+        if (sp_acc[i_]) atomicAdd(reinterpret_cast<unsigned long long*>(&g_sp[blockIdx.x][i_]),         \
+                                  (unsigned long long)sp_acc[i_]);                                       \
+  } while (0)
+#else
+#define SP_INIT()
+#define SP_W(slot, call) call
+#define SP_FLUSH()
+#endif
 constexpr int kMaxSel = 80;
 constexpr int64_t kShareFrom = 2048;          // first position on this kernel
 constexpr uint32_t kHalf = 128 * 128;         // 16 KB: 128 rows x 64 d (bf16)
@@ -254,6 +280,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  SP_INIT();
 
   if (warp == 0 || warp == kVWarp) {
     // ------------------------------------------------------------ producers
@@ -283,7 +310,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       }
       auto issue = [&](int b0, int b1, int nt) {
         if (lane == 0) {
-          mbar_wait(ring_empty + stage, phase ^ 1);
+          SP_W(is_k ? 1 : 3, mbar_wait(ring_empty + stage, phase ^ 1));
           mbar_arrive_expect_tx(ring_full + stage, nt * kDH * (kM * 128));
           uint8_t* dst = ring + stage * kTile;
           for (int x = 0; x < nt; ++x) {
@@ -350,8 +377,8 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       for (int u = 0; u < kU; ++u)
       for (int k = 0; k < ur.tiles(u); ++k, ++tcount) {
         const int slot = tcount % kSlots;
-        mbar_wait(k_full + stage, phase);
-        mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1);
+        SP_W(5, mbar_wait(k_full + stage, phase));
+        SP_W(6, mbar_wait(s_empty + slot, ((tcount / kSlots) & 1) ^ 1));
         tc_fence_after();
         if (elect_one()) {
           const uint32_t ka = smem_u32(smem + Smem::kv + stage * kTile);
@@ -383,7 +410,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const URows ur = load_unit<kU>(p, w, lane);
       const int ob = it & 1;
       const uint32_t obase = tmem + kColO + 128 * ob;
-      mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1);
+      SP_W(10, mbar_wait(o_empty + ob, ((it >> 1) & 1) ^ 1));
       mbar_wait(psh_full, it & 1);
       // shared PVs: O^T[all U rows] = V_A^T . P_A^T + V_B^T . P_B^T (N = 64);
       // even K-steps -> O_a region, odd -> O_b region
@@ -423,8 +450,8 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int nch = ur.nchosen(u);
         for (int k = 0; k < tiles; ++k, ++c, ++pcount) {
           const int pbuf = pcount & 1;
-          mbar_wait(v_full + stage, vphase);
-          mbar_wait(p_full + pbuf, (pcount >> 1) & 1);
+          SP_W(8, mbar_wait(v_full + stage, vphase));
+          SP_W(9, mbar_wait(p_full + pbuf, (pcount >> 1) & 1));
           tc_fence_after();
           const int ksteps = 2 * k + 1 < nch ? 8 : 4;
           if (elect_one()) {
@@ -579,7 +606,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const uint32_t oa = tmem + lane_base + kColO + 128 * ob + u * kG + h0;
         for (int k = 0; k < tiles; ++k) {
           const int sslot = tcount % kSlots;
-          mbar_wait(s_full + sslot, (tcount / kSlots) & 1);
+          SP_W(12, mbar_wait(s_full + sslot, (tcount / kSlots) & 1));
           ++tcount;
           tc_fence_after();
           float z[kSH];
@@ -638,7 +665,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
               tc_fence_before();
             }
           }
-          mbar_wait(p_empty + pbuf, p_ph[pbuf] ^ 1);
+          SP_W(13, mbar_wait(p_empty + pbuf, p_ph[pbuf] ^ 1));
           p_ph[pbuf] ^= 1;
           uint32_t phi[kSH / 2];
 #pragma unroll
@@ -709,7 +736,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const int ob = it & 1;
       for (int u = 0; u < kU; ++u, ++rcount) {
         const int sb = rcount & 1;
-        mbar_wait(o_full + ob * kU + u, (it >> 1) & 1);
+        SP_W(15, mbar_wait(o_full + ob * kU + u, (it >> 1) & 1));
         mbar_wait(st_full + sb, (rcount >> 1) & 1);
         tc_fence_after();
         float o[kG], o2[kG];
@@ -750,6 +777,7 @@ attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
   tc_fence_before();
   __syncthreads();
+  SP_FLUSH();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -844,3 +872,9 @@ cudaError_t launch_attend_share(const CallShape& cs, int64_t row0, int64_t row1,
 }
 
 }  // namespace infllm2
+
+#ifdef SHARE_PROF
+extern "C" int infllm2_debug_share_cycles(long long* host) {
+  return cudaMemcpyFromSymbol(host, infllm2::g_sp, sizeof(long long) * 160 * 16) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -1,6 +1,6 @@
-"""Per-role wait split of attend_share_kernel from a profiling build (the
-SP_W-instrumented variant described in DESIGN §4 K3s; INFLLM2_LIB_PATH=<variant>.so,
-AB_SHAPE=0.5B|8B, AB_TOPK=16).  A role that rarely waits is the one pacing the kernel."""
+"""Per-role wait split of attend_share_kernel (a role that rarely waits paces the kernel):
+  tools/build_variant.sh variants/sprof.so paper_2506_07900_b200/csrc/attend_share.cu -DSHARE_PROF
+  INFLLM2_LIB_PATH=variants/sprof.so AB_SHAPE=0.5B|8B AB_TOPK=16 python tools/share_prof.py"""
 import ctypes, os, sys
 import numpy as np, torch
 sys.path.insert(0, "tools"); sys.path.insert(0, ".")
