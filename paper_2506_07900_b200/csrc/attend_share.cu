@@ -198,15 +198,6 @@ __device__ __forceinline__ UnitRows<kU> load_unit(const Params& p, int64_t w, in
   return ur;
 }
 
-// Row tile c (0-based, after the two shared tiles) of a unit -> (row u, tile k of that row).
-template <int kU>
-__device__ __forceinline__ void row_tile(const UnitRows<kU>& ur, int c, int* u, int* k) {
-  int uu = 0;
-  while (uu < kU - 1 && c >= ur.tiles(uu)) { c -= ur.tiles(uu); ++uu; }
-  *u = uu;
-  *k = c;
-}
-
 template <int G, int D>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_share_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
