@@ -792,10 +792,9 @@ bool attend_share_range(const infllm2_geometry& g, const CallShape& cs, int p_sp
   // with top-k <= 4) attends too few keys for bf16 weights: attend_tc.cu's
   // hi + lo weights serve it
   if (g.forced_consume_budget && g.top_k <= 4) return false;
-  // 0.5B: eight rows per unit pay off while the forced blocks are a large share
-  // of a row's blocks (measured: k = 8 / 16 -40 / -16 % stage-2 time at 128K,
-  // k = 32 neutral, k = 64 +14 %)
-  if (cs.group == 8 && cs.max_sel > 19) return false;
+  // 0.5B runs here at every top-k since the producer-loop fix (128K stage 2 vs
+  // attend_tc: k = 32 15.7 -> 11.4 ms, k = 64 27.4 -> 20.4 ms; before it, k >= 32
+  // was neutral or slower and stayed on attend_tc)
   const int u = kNS / cs.group;
   // rows below position 2048 attend at most 32 blocks and carry the largest
   // relative bf16-weight rounding error: they stay on attend_tc.cu (whose

@@ -38,8 +38,9 @@ def _layer(length, seed, topk=16, shape=(32, 2, 128), consume=False):
 
 @pytest.mark.parametrize("length,topk,shape", [(8192, 16, (32, 2, 128)), (12000, 32, (32, 2, 128)),
                                                (9000, 64, (32, 2, 128)), (8192, 16, (16, 2, 64)),
-                                               (10000, 8, (16, 2, 64))], ids=["8B-k16", "8B-k32", "8B-k64",
-                                                                               "0.5B-k16", "0.5B-k8"])
+                                               (10000, 8, (16, 2, 64)), (11000, 32, (16, 2, 64)),
+                                               (9500, 64, (16, 2, 64))],
+                         ids=["8B-k16", "8B-k32", "8B-k64", "0.5B-k16", "0.5B-k8", "0.5B-k32", "0.5B-k64"])
 def test_shared_kernel_vs_float64_verifier(length, topk, shape):
     cfg, q, layer = _layer(length, 11 + length, topk, shape)
     group = shape[0] // shape[1]
