@@ -1,7 +1,9 @@
 // Stage-2 block-sparse attention with the forced blocks shared across query
 // rows (tcgen05 + TMEM + TMA), for prefill rows at positions >= 2048 of the
-// production geometry (G = 16, D = 128, m = 64, one init block, two local
-// blocks: the MiniCPM4 defaults).
+// production geometries (G = 16, D = 128 and G = 8, D = 64; m = 64, one init
+// block, two local blocks: the MiniCPM4 defaults), every top-k up to 80
+// selected blocks.  (The description below uses the 8B numbers; the 0.5B shape
+// runs U = 8 rows per unit with the same N = 64 shared tiles.)
 //
 // attend_tc.cu gathers every selected block once per (row, KV group) item and
 // is bound by shared-memory traffic: each 128-key tile moves 64 KB by TMA and
@@ -28,7 +30,10 @@
 //
 // Warp roles (16 warps, as attend_tc.cu): 0 = Q + K TMA, 1 = QK issuer,
 // 2..9 = softmax (thread = tile row x 8 heads), 10 = PV issuer, 11..14 =
-// epilogue (thread = d lane of O^T), 15 = V TMA.
+// epilogue (thread = d lane of O^T), 15 = V TMA.  The producers and the QK
+// issuer walk a unit's rows with the row index unrolled: a per-tile search
+// over runtime-indexed register arrays kept both TMA warps ~90 % busy
+// (-DSHARE_PROF role counters, DESIGN §4 K3s).
 #include <float.h>
 #include <stdlib.h>
 
